@@ -61,6 +61,7 @@ extern "C" {
 #define BS_FLAG_PACK_CAPACITY 0x10 /* packed output exceeded out_capacity; batches beyond it not packed   */
 #define BS_FLAG_NONPOS_LEN    0x20 /* a batch holds a length < 1: waste_ratio raises, memory_model.py:96  */
 #define BS_FLAG_BATCH_CAP     0x40 /* more batches than batches_cap                                       */
+#define BS_FLAG_BAD_EDGES     0x80 /* init_edges not strictly increasing from 0 to l_max: ValueError      */
 
 /* ---- enums ------------------------------------------------------------------ */
 /* Dispatch order inside one (bucket, class) segment, batch_controller.py:33-41.

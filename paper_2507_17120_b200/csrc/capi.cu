@@ -1,0 +1,373 @@
+// capi.cu — the extern "C" boundary (include/bucketserve.h): context lifetime,
+// scratch layout, argument validation and stage orchestration.  No C++
+// exception crosses this boundary; every entry returns a BS_* status.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "ctx.cuh"
+
+void* bs_chain_kernel_ptr();  // k_size.cu
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_err;
+
+int fail(bs_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(bs_ctx* ctx, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  const bool unavailable = e == cudaErrorNoKernelImageForDevice || e == cudaErrorNoDevice ||
+                           e == cudaErrorInsufficientDriver || e == cudaErrorInvalidDevice;
+  return fail(ctx, unavailable ? BS_ERR_NOT_BUILT : BS_ERR_CUDA, m);
+}
+
+#define BS_CUDA(call, where)                       \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, where); \
+  } while (0)
+
+int check_params(bs_ctx* ctx, const bs_window_params* p) {
+  if (!p) return fail(ctx, BS_ERR_INVALID_ARG, "params is NULL");
+  if (p->l_max < 1) return fail(ctx, BS_ERR_INVALID_ARG, "max_seq_len must be >= 1");
+  if (p->l_max > ctx->l_cap)
+    return fail(ctx, BS_ERR_CAPACITY, "l_max " + std::to_string(p->l_max) + " exceeds context capacity " +
+                                          std::to_string(ctx->l_cap));
+  if (p->n_classes < 1 || p->n_classes > ctx->c_max)
+    return fail(ctx, BS_ERR_INVALID_ARG, "n_classes must be in [1, " + std::to_string(ctx->c_max) + "]");
+  for (int c = 0; c < p->n_classes; ++c)
+    if (p->policy[c] < BS_POLICY_FCFS || p->policy[c] > BS_POLICY_LJF)
+      return fail(ctx, BS_ERR_INVALID_ARG, "unknown dispatch policy");
+  if (!(p->split_threshold > 0.0 && p->split_threshold <= 1.0))
+    return fail(ctx, BS_ERR_INVALID_ARG, "split_threshold must be in (0, 1]");
+  if (p->kv_bytes_per_token < 1) return fail(ctx, BS_ERR_CONFIG, "kv_bytes_per_token must be >= 1");
+  if (p->current_safe < 0) return fail(ctx, BS_ERR_INVALID_ARG, "safe memory must be >= 0");
+  if (p->accounting != BS_ACCOUNTING_PADDED && p->accounting != BS_ACCOUNTING_EXACT)
+    return fail(ctx, BS_ERR_INVALID_ARG, "unknown memory accounting");
+  return BS_OK;
+}
+
+int check_n(bs_ctx* ctx, int64_t n) {
+  if (n < 0) return fail(ctx, BS_ERR_INVALID_ARG, "n must be >= 0");
+  if (n > ctx->max_n)
+    return fail(ctx, BS_ERR_CAPACITY, "window of " + std::to_string(n) + " requests exceeds context capacity " +
+                                          std::to_string(ctx->max_n));
+  return BS_OK;
+}
+
+template <typename T>
+cudaError_t alloc(bs_ctx* ctx, T** p, size_t count) {
+  size_t bytes = sizeof(T) * (count ? count : 1);
+  ctx->scratch_bytes += (int64_t)bytes;
+  return cudaMalloc(reinterpret_cast<void**>(p), bytes);
+}
+
+void free_all(bs_ctx* c) {
+  void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->bin_base, c->kinfo,
+                  c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
+                  c->bmax, c->bcnt, c->bsum, c->J, c->is_start, c->listA, c->listB,
+                  c->node_batch, c->misc};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bs_abi_version(void) { return BS_ABI_VERSION; }
+
+const char* bs_last_error(const bs_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_err.c_str();
+}
+
+int64_t bs_scratch_bytes(const bs_ctx* ctx) { return ctx ? ctx->scratch_bytes : 0; }
+
+int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_t max_classes) {
+  if (!out) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx out-pointer is NULL");
+  *out = nullptr;
+  if (max_n < 0 || max_n >= (int64_t)1 << 30)
+    return fail(nullptr, BS_ERR_INVALID_ARG, "max_n must be in [0, 2^30)");
+  if (l_max_cap < 1 || l_max_cap > (1 << 24))
+    return fail(nullptr, BS_ERR_INVALID_ARG, "l_max_cap must be in [1, 2^24]");
+  if (max_classes < 1 || max_classes > BS_MAX_CLASSES)
+    return fail(nullptr, BS_ERR_INVALID_ARG, "max_classes must be in [1, 8]");
+  bs_ctx* ctx = new (std::nothrow) bs_ctx();
+  if (!ctx) return fail(nullptr, BS_ERR_CUDA, "out of host memory");
+  ctx->device = device;
+  ctx->max_n = max_n;
+  ctx->l_cap = l_max_cap;
+  ctx->c_max = max_classes;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { int rc = cuda_fail(ctx, e, "cudaSetDevice"); delete ctx; return rc; }
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { int rc = cuda_fail(ctx, e, "cudaGetDeviceProperties"); delete ctx; return rc; }
+  if (prop.major != 10) {
+    int rc = fail(ctx, BS_ERR_NOT_BUILT, std::string("device ") + prop.name +
+                                             " is not sm_100 (this library is built for B200 sm_100a)");
+    delete ctx;
+    return rc;
+  }
+  if (!prop.cooperativeLaunch) {
+    int rc = fail(ctx, BS_ERR_NOT_BUILT, "device lacks cooperative launch");
+    delete ctx;
+    return rc;
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  int r = 1;
+  while (((int64_t)1 << r) < max_n + 1) ++r;
+  ctx->r_cap = r + 2;
+  const int64_t L = l_max_cap, C = max_classes, N = max_n;
+  ctx->max_tiles = (N + 4095) / 4096 + 1;
+  const int64_t groups = (N + 31) / 32 + 1;
+#define A(ptr, cnt)                                                        \
+  if ((e = alloc(ctx, &ctx->ptr, (size_t)(cnt))) != cudaSuccess) {         \
+    int rc = cuda_fail(ctx, e, "cudaMalloc " #ptr);                        \
+    free_all(ctx);                                                         \
+    delete ctx;                                                            \
+    return rc;                                                             \
+  }
+  A(P, L + 1);
+  A(PcL, C * (L + 1));
+  A(E, L + 1);
+  A(lut, L);
+  A(seg_base, L * C);
+  A(seg_off, L * C + 1);
+  A(slot_lut, C * L);
+  A(bin_base, 4 * 256);
+  A(kinfo, 8);
+  A(keysA, N); A(keysB, N); A(valsA, N); A(valsB, N);
+  A(status, 4 * ctx->max_tiles * 256);
+  A(tile_ctr, 4);
+  A(sorted_len, N);
+  A(bmax, groups); A(bcnt, groups); A(bsum, groups);
+  A(J, (int64_t)ctx->r_cap * N);
+  A(is_start, N);
+  A(listA, N + 1); A(listB, N + 1);
+  A(node_batch, N + 1);
+  A(misc, 128);
+#undef A
+  // co-resident blocks for the cooperative chain kernel (512 threads)
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(), 512, 0);
+  if (e != cudaSuccess || per_sm < 1) {
+    int rc = e != cudaSuccess ? cuda_fail(ctx, e, "occupancy(k_chain)")
+                              : fail(ctx, BS_ERR_NOT_BUILT, "k_chain cannot be resident");
+    free_all(ctx);
+    delete ctx;
+    return rc;
+  }
+  ctx->chain_blocks = per_sm * ctx->num_sms;
+  *out = ctx;
+  return BS_OK;
+}
+
+int bs_destroy(bs_ctx* ctx) {
+  if (!ctx) return BS_OK;
+  cudaSetDevice(ctx->device);
+  free_all(ctx);
+  delete ctx;
+  return BS_OK;
+}
+
+int bs_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
+                 const bs_window_params* p, uint32_t* hist_out, bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_n(ctx, n)) != BS_OK) return rc;
+  if (!hist_out || (n > 0 && (!len || !cls))) return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (summary) BS_CUDA(bsk::launch_init_summary(summary, n, st), "init_summary");
+  BS_CUDA(bsk::launch_histogram(ctx, len, cls, n, *p, hist_out, summary, st), "k_histogram");
+  return BS_OK;
+}
+
+static int boundaries_impl(bs_ctx* ctx, const uint32_t* hist_local, const uint32_t* hist_global,
+                           const bs_window_params* p, const int32_t* init_edges, int32_t k_init,
+                           int32_t* edges_out, int32_t* changes_out, int32_t changes_cap,
+                           int32_t* seg_off_out, bs_summary* summary, cudaStream_t st) {
+  if (!hist_local || !edges_out || !summary || !seg_off_out)
+    return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  if (init_edges && (k_init < 1 || k_init > p->l_max))
+    return fail(ctx, BS_ERR_INVALID_ARG, "k_init out of range");
+  if (changes_cap < 0 || (changes_cap > 0 && !changes_out))
+    return fail(ctx, BS_ERR_INVALID_ARG, "bad change-log buffer");
+  BS_CUDA(bsk::launch_boundaries(ctx, hist_local, hist_global, *p, init_edges, k_init, edges_out,
+                                 changes_out, changes_cap, seg_off_out, summary, st),
+          "k_boundaries");
+  return BS_OK;
+}
+
+int bs_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uint32_t* hist_global,
+                  const bs_window_params* p, const int32_t* init_edges, int32_t k_init,
+                  int32_t* edges_out, int32_t* changes_out, int32_t changes_cap,
+                  bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK) return rc;
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  // the segment table stays in ctx scratch; bs_order hands a copy to the caller
+  return boundaries_impl(ctx, hist_local, hist_global, p, init_edges, k_init, edges_out,
+                         changes_out, changes_cap, ctx->seg_off, summary,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int bs_assign(bs_ctx* ctx, const int32_t* len, int64_t n, const bs_window_params* p,
+              int32_t* bucket_out, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_n(ctx, n)) != BS_OK) return rc;
+  if (n > 0 && (!len || !bucket_out)) return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_assign(ctx, len, n, *p, bucket_out, static_cast<cudaStream_t>(stream)),
+          "k_assign");
+  return BS_OK;
+}
+
+int bs_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
+             const bs_window_params* p, int32_t* perm_out, int32_t* seg_off_out,
+             int32_t* bucket_out, bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_n(ctx, n)) != BS_OK) return rc;
+  if (n > 0 && (!len || !cls || !perm_out)) return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (seg_off_out)
+    BS_CUDA(cudaMemcpyAsync(seg_off_out, ctx->seg_off,
+                            sizeof(int32_t) * ((size_t)p->l_max * p->n_classes + 1),
+                            cudaMemcpyDeviceToDevice, st),
+            "copy seg_off");
+  BS_CUDA(bsk::launch_order(ctx, len, cls, n, *p, perm_out, bucket_out, summary, st), "k_sort_pass");
+  return BS_OK;
+}
+
+int bs_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t* seg_off,
+            int64_t n, const bs_window_params* p, bs_batch* batches_out, int32_t batches_cap,
+            int32_t* req_batch_out, int32_t* req_row_out, bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_n(ctx, n)) != BS_OK) return rc;
+  if (!summary || !batches_out || batches_cap < 0 ||
+      (n > 0 && (!len || !perm || !seg_off || !req_batch_out || !req_row_out)))
+    return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_size(ctx, len, perm, seg_off, n, *p, batches_out, batches_cap, req_batch_out,
+                           req_row_out, summary, static_cast<cudaStream_t>(stream)),
+          "k_size");
+  return BS_OK;
+}
+
+int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t* req_batch,
+            const int32_t* req_row, const int64_t* tok_off, const int32_t* tokens,
+            const bs_window_params* p, const bs_batch* batches, int64_t batch_begin,
+            int64_t batch_end, int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+            bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK) return rc;
+  if (!len || !perm || !req_batch || !req_row || !tok_off || !tokens || !batches || !out_tokens)
+    return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  if (batch_end < 0 && !summary)
+    return fail(ctx, BS_ERR_INVALID_ARG, "batch_end < 0 needs the summary of bs_size");
+  if (batch_begin < 0) return fail(ctx, BS_ERR_INVALID_ARG, "batch_begin must be >= 0");
+  if (reinterpret_cast<uintptr_t>(out_tokens) & 15)
+    return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
+  if (out_mask && (reinterpret_cast<uintptr_t>(out_mask) & 3))
+    return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_pack(ctx, len, perm, req_batch, req_row, tok_off, tokens, *p, batches,
+                           batch_begin, batch_end, INT32_MAX, out_tokens, out_mask, out_capacity,
+                           summary, static_cast<cudaStream_t>(stream)),
+          "k_pack");
+  return BS_OK;
+}
+
+static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
+                                 cudaStream_t st) {
+  int rc;
+  if ((rc = boundaries_impl(ctx, io->hist, io->hist_global ? io->hist_global : io->hist, p,
+                            io->init_edges, io->k_init, io->edges, io->changes, io->changes_cap,
+                            io->seg_off, io->summary, st)) != BS_OK)
+    return rc;
+  BS_CUDA(bsk::launch_order(ctx, io->len, io->cls, io->n, *p, io->perm, io->bucket, io->summary, st),
+          "k_sort_pass");
+  BS_CUDA(bsk::launch_size(ctx, io->len, io->perm, io->seg_off, io->n, *p, io->batches,
+                           io->batches_cap, io->req_batch, io->req_row, io->summary, st),
+          "k_size");
+  if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
+    if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
+      return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
+    if (io->out_mask && (reinterpret_cast<uintptr_t>(io->out_mask) & 3))
+      return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
+    BS_CUDA(bsk::launch_pack(ctx, io->len, io->perm, io->req_batch, io->req_row, io->tok_off,
+                             io->tokens, *p, io->batches, 0, -1, io->batches_cap, io->out_tokens,
+                             io->out_mask, io->out_capacity, io->summary, st),
+            "k_pack");
+  }
+  return BS_OK;
+}
+
+static int check_io(bs_ctx* ctx, const bs_window_io* io) {
+  if (!io) return fail(ctx, BS_ERR_INVALID_ARG, "io is NULL");
+  int rc;
+  if ((rc = check_n(ctx, io->n)) != BS_OK) return rc;
+  if (!io->hist || !io->edges || !io->perm || !io->seg_off || !io->batches || !io->req_batch ||
+      !io->req_row || !io->summary)
+    return fail(ctx, BS_ERR_INVALID_ARG, "a required window buffer is NULL");
+  if (io->n > 0 && (!io->len || !io->cls)) return fail(ctx, BS_ERR_INVALID_ARG, "NULL input");
+  if (io->batches_cap < 0 || io->changes_cap < 0 || io->out_capacity < 0)
+    return fail(ctx, BS_ERR_INVALID_ARG, "negative capacity");
+  return BS_OK;
+}
+
+int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
+                       void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_io(ctx, io)) != BS_OK) return rc;
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  BS_CUDA(bsk::launch_init_summary(io->summary, io->n, st), "init_summary");
+  BS_CUDA(bsk::launch_histogram(ctx, io->len, io->cls, io->n, *p, io->hist, io->summary, st),
+          "k_histogram");
+  bs_window_io local = *io;
+  local.hist_global = io->hist;
+  return window_from_hist_impl(ctx, &local, p, st);
+}
+
+int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
+                        void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_io(ctx, io)) != BS_OK) return rc;
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  return window_from_hist_impl(ctx, io, p, static_cast<cudaStream_t>(stream));
+}
+
+int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
+                    uint64_t* out, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK) return rc;
+  if (!hist || !out || bins < 1 || bins > 4096) return fail(ctx, BS_ERR_INVALID_ARG, "bad arguments");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_monitor_bins(hist, *p, bins, out, static_cast<cudaStream_t>(stream)),
+          "k_monitor_bins");
+  return BS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// ctx.cuh — the scratch-owning context behind bs_ctx and the internal launchers.
+#pragma once
+
+#include <string>
+
+#include "common.cuh"
+
+struct bs_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int64_t max_n = 0;
+  int32_t l_cap = 0;
+  int32_t c_max = 0;
+  int r_cap = 0;            // doubling levels stored for the K5 chain
+  int64_t max_tiles = 0;    // K4 tiles per pass
+  int chain_blocks = 0;     // co-resident blocks of the cooperative chain kernel
+  int64_t scratch_bytes = 0;
+  std::string err;
+
+  // K2 tables
+  uint32_t* P = nullptr;         // [l_cap+1] exclusive prefix of the (global) total histogram
+  uint32_t* PcL = nullptr;       // [c_max][l_cap+1] exclusive prefix of the local per-class hist
+  int32_t* E = nullptr;          // [l_cap+1] compacted edges of the last bs_boundaries call
+  int32_t* lut = nullptr;        // [l_cap] bucket index per length
+  int32_t* seg_base = nullptr;   // [l_cap*c_max] first radix slot of each segment
+  int32_t* seg_off = nullptr;    // [l_cap*c_max+1] segment offsets of the last bs_boundaries
+  uint32_t* slot_lut = nullptr;  // [c_max*l_cap] radix slot per (class, length)
+  uint32_t* bin_base = nullptr;  // [4][256] global digit offsets per radix pass
+  int32_t* kinfo = nullptr;      // [8]: K, D, ...
+  // K4
+  uint32_t *keysA = nullptr, *keysB = nullptr, *valsA = nullptr, *valsB = nullptr;
+  uint32_t* status = nullptr;    // [4][max_tiles][256]
+  uint32_t* tile_ctr = nullptr;  // [4]
+  // K5
+  int32_t* sorted_len = nullptr; // [max_n] effective length in drain order
+  int32_t* bmax = nullptr;       // [max_n/32+1] per 32-position group: max non-rejected length
+  int32_t* bcnt = nullptr;       //   non-rejected count
+  int32_t* bsum = nullptr;       //   non-rejected length sum
+  int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
+  uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
+  int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)
+  int32_t* listB = nullptr;
+  int32_t* node_batch = nullptr; // [max_n + 1] batch id of each chain node (-1: empty tail)
+  int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
+                                 //        [66] n_batches, [67] pack rows cursor
+};
+
+namespace bsk {
+
+struct SortPlan {
+  int passes;  // radix passes
+  int bits;    // digit bits per pass (<= 8)
+};
+SortPlan sort_plan(int32_t l_max, int32_t n_classes);
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
+                             const bs_window_params& p, uint32_t* hist, bs_summary* summary,
+                             cudaStream_t st);
+cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uint32_t* hist_global,
+                              const bs_window_params& p, const int32_t* init_edges, int32_t k_init,
+                              int32_t* edges_out, int32_t* changes_out, int32_t changes_cap,
+                              int32_t* seg_off_out, bs_summary* summary, cudaStream_t st);
+cudaError_t launch_assign(bs_ctx* ctx, const int32_t* len, int64_t n, const bs_window_params& p,
+                          int32_t* bucket_out, cudaStream_t st);
+cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
+                         const bs_window_params& p, int32_t* perm_out, int32_t* bucket_out,
+                         bs_summary* summary, cudaStream_t st);
+cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                        const int32_t* seg_off, int64_t n, const bs_window_params& p,
+                        bs_batch* batches, int32_t batches_cap, int32_t* req_batch,
+                        int32_t* req_row, bs_summary* summary, cudaStream_t st);
+cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                        const int32_t* req_batch, const int32_t* req_row, const int64_t* tok_off,
+                        const int32_t* tokens, const bs_window_params& p, const bs_batch* batches,
+                        int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                        int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                        bs_summary* summary, cudaStream_t st);
+cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
+                                uint64_t* out, cudaStream_t st);
+cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);
+
+}  // namespace bsk

@@ -1,0 +1,108 @@
+"""Data model shared by the window API and the drop-in classes.
+
+Names and fields follow the reference (workload.py:25-51,
+batch_controller.py:21-67, bucket_manager.py:56-69).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+from . import _native as N
+
+
+class TaskClass(Enum):
+    """workload.py:25-27 (class 0 = ONLINE dispatches first, pd_sim.py:449-450)."""
+    ONLINE = "online"
+    OFFLINE = "offline"
+
+
+class DispatchPolicy(Enum):
+    """batch_controller.py:21-25."""
+    SJF = "sjf"
+    LJF = "ljf"
+    EARLIEST_ARRIVAL = "earliest_arrival"
+    FCFS = "fcfs"
+
+
+class MemoryAccounting(Enum):
+    """batch_controller.py:28-30."""
+    PADDED = "padded"
+    EXACT = "exact"
+
+
+def policy_code(p) -> int:
+    if isinstance(p, int):
+        if p not in (N.POLICY_FCFS, N.POLICY_SJF, N.POLICY_LJF):
+            raise ValueError(f"unknown dispatch policy {p}")
+        return p
+    p = DispatchPolicy(p) if not isinstance(p, DispatchPolicy) else p
+    return {DispatchPolicy.SJF: N.POLICY_SJF, DispatchPolicy.LJF: N.POLICY_LJF,
+            DispatchPolicy.FCFS: N.POLICY_FCFS,
+            DispatchPolicy.EARLIEST_ARRIVAL: N.POLICY_FCFS}[p]
+
+
+def accounting_code(a) -> int:
+    if isinstance(a, int):
+        return a
+    a = MemoryAccounting(a) if not isinstance(a, MemoryAccounting) else a
+    return N.ACCOUNTING_PADDED if a is MemoryAccounting.PADDED else N.ACCOUNTING_EXACT
+
+
+@dataclass
+class Request:
+    """workload.py:30-51 (only the fields the scheduling path reads are required)."""
+    id: int
+    arrival_time: float
+    input_len: int
+    output_len: int | None
+    task_class: object
+    slo_ttft: float | None = None
+    slo_e2e: float | None = None
+    enqueue_time: float | None = None
+    prefill_start: float | None = None
+    first_token_time: float | None = None
+    completion_time: float | None = None
+
+
+@dataclass(frozen=True)
+class StructuralChange:
+    """bucket_manager.py:56-63."""
+    kind: str  # "split" | "merge" | "skip"
+    parent_low: int
+    parent_up: int
+    midpoint: int | None = None
+
+
+@dataclass(frozen=True)
+class PartitionViolation:
+    """bucket_manager.py:66-69."""
+    kind: str
+    detail: str
+
+
+@dataclass(frozen=True)
+class BatchPlan:
+    """batch_controller.py:44-56."""
+    request_ids: tuple
+    requests: tuple
+    max_input_len: int
+    token_sum: int
+    footprint: int
+    created_at: float
+    source_bucket: tuple
+
+    def __len__(self) -> int:
+        return len(self.requests)
+
+
+@dataclass(frozen=True)
+class OversizeRejection:
+    """batch_controller.py:59-67."""
+    request: Request
+    footprint: int
+    safe_mem: int
+
+
+CHANGE_KIND = {N.CHANGE_SPLIT: "split", N.CHANGE_MERGE: "merge", N.CHANGE_SKIP: "skip"}
