@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""bench.py — requests bucketed+packed per second on B200 (BASELINE.json metric).
+
+One step = one window of the BucketServe scheduling hot path over a fresh-in-HBM
+synthetic window: K1 histogram -> [C1 NCCL histogram all-reduce when N>1] -> K2
+boundaries -> K3/K4 assign+order -> K5 size -> K6 pack (padded [n, pitch] int32
+tokens + u8 mask).  Default workload = BASELINE configs[1] (C2): 1M requests per
+GPU, lognormal ShareGPT-like lengths, Llama-2-7B KV model on 180 GiB / 14 GiB.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
+    python bench.py --impl reference ...                      (CPU reference arm)
+
+Prints ONE JSON line on rank 0.  `value` is device-timed (CUDA events, max over
+ranks) with inputs resident in HBM; `e2e` is the same metric through the public
+API from pinned HOST buffers with the H2D of every input and the D2H of the
+schedule inside the timed region.  Inputs (1.75 GB token store per GPU) exceed the
+126 MB L2, so no explicit flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "requests bucketed+packed/sec"
+UNIT = "requests/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _profile_traffic(cfg_name):
+    """dram bytes per pack launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        ent = d.get("k_pack", {}).get(cfg_name)
+        return ent.get("dram_bytes") if ent else None
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        for r in self.rows:
+            for nm, v in zip(names, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def cpu_port_window(cfg, lens, cls, tok_off, tokens, threads, out_capacity=None):
+    from oracle import cpu
+    ws = cpu.WindowSpec(l_max=cfg.l_max, n_classes=cfg.n_classes, policies=cfg.policies,
+                        theta=cfg.theta, adjust=cfg.adjust, kvpt=cfg.kvpt,
+                        current_safe=cfg.current_safe, accounting=cfg.accounting,
+                        init_edges=cfg.init_edges)
+    return cpu.window(ws, lens, cls, tok_off, tokens, threads=threads, out_capacity=out_capacity)
+
+
+def cpu_baseline(cfg_name, n_sample, budget_s=12.0):
+    """The oracle port (oracle/bso.c, all host threads) on bounded C2-shaped windows."""
+    from paper_2507_17120_b200 import workloads as W
+    cfg, lens, cls = W.make_window(cfg_name, n=n_sample, seed=99)
+    tok_off, tokens = W.token_store(lens)
+    threads = os.cpu_count() or 1
+    r = cpu_port_window(cfg, lens, cls, tok_off, tokens, threads)
+    cap = int(r.summary["packed_elems"])
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        cpu_port_window(cfg, lens, cls, tok_off, tokens, threads, out_capacity=cap)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 50:
+            break
+    med = statistics.median(times)
+    return {"value": n_sample / med, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{cfg_name} distribution, {n_sample}-request windows incl. pack, "
+                      f"{len(times)} runs, median {med:.3f} s (oracle/bso.c, OpenMP)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference path's CPU implementation (oracle port) on the
+    same config / metric, rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2507_17120_b200 import workloads as W
+    cfg, lens, cls = W.make_window(args.config, n=args.requests, seed=1234)
+    tok_off, tokens = W.token_store(lens)
+    threads = os.cpu_count() or 1
+    r = cpu_port_window(cfg, lens, cls, tok_off, tokens, threads)
+    cap = int(r.summary["packed_elems"])
+    for _ in range(args.warmup):
+        cpu_port_window(cfg, lens, cls, tok_off, tokens, threads, out_capacity=cap)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_port_window(cfg, lens, cls, tok_off, tokens, threads, out_capacity=cap)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = len(lens) / dt
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded lengths, hashed token ids)", "impl": "reference",
+        "config": {"workload": f"{args.config}: {cfg.note}", "requests_per_step": len(lens),
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full {args.config} window of {len(lens)} requests per step "
+                                   "(reference composition restated in C, oracle/bso.c)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--requests", type=int, default=None, help="requests per GPU (default: config)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=250_000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2507_17120_b200 import workloads as W
+    cfg0 = W.CONFIGS[args.config]
+    if args.requests is None:
+        args.requests = cfg0.n // world if args.config == "c5" else cfg0.n
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    from paper_2507_17120_b200.window import WindowScheduler
+
+    cfg, lens_np, cls_np = W.make_window(args.config, n=args.requests, seed=1234 + rank)
+    n = len(lens_np)
+    lens = torch.as_tensor(lens_np).to(dev)
+    cls = torch.as_tensor(cls_np).to(dev)
+    tok_off, tokens = W.token_store_device(lens, seed=rank)
+    sched = WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
+                            policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
+                            buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
+                            current_safe=cfg.current_safe, accounting=cfg.accounting,
+                            device=dev, process_group=pg)
+    # first window sizes the reusable packed-output buffer
+    res = sched.schedule(lens, cls, tok_off, tokens)
+    s0 = res.summary()
+    for _ in range(args.warmup):
+        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False)
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: device-resident windows ----------------------
+    sampler = ClockSampler(local)
+    sched.ctx.profile_enable(args.steps)
+    l0 = sched.ctx.launches
+    if pg is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False)
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    if pg is not None:
+        dist.barrier()
+    launches = sched.ctx.launches - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    stage_ms, prof_steps = sched.ctx.profile_read()
+    stage_ms = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
+    res = sched.schedule(lens, cls, tok_off, tokens)  # check the steady-state result
+    s = res.summary()
+    assert s["n_batches"] == s0["n_batches"] and s["packed_elems"] == s0["packed_elems"]
+
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if pg is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n / (ms_max / 1e3)
+
+    # ---------------- pack roofline ------------------------------------------------
+    peak, peak_src = _peaks()
+    admitted = int(s["admitted_tokens"])
+    n_adm = n - int(s["n_rejected"]) - int(s["n_pending"])
+    pack_bytes = 4 * admitted + 24 * n_adm + 5 * int(s["packed_elems"])
+    pack_ms = stage_ms["pack"]
+    pack_gbs = pack_bytes / (pack_ms / 1e3) / 1e9 if pack_ms > 0 else None
+    sched_bytes = 17 * n
+    sched_ms = sum(v for k, v in stage_ms.items() if k != "pack")
+
+    # ---------------- e2e through the public API from pinned host buffers ---------
+    e2e = None
+    if not args.no_e2e:
+        h_lens = lens.cpu().pin_memory()
+        h_cls = cls.cpu().pin_memory()
+        h_off = tok_off.cpu().pin_memory()
+        h_tok = tokens.cpu().pin_memory()
+        d_lens, d_cls = torch.empty_like(lens), torch.empty_like(cls)
+        d_off, d_tok = torch.empty_like(tok_off), torch.empty_like(tokens)
+        nb = int(s["n_batches"])
+        h_rb = torch.empty(n, dtype=torch.int32).pin_memory()
+        h_bt = torch.empty(64 * nb, dtype=torch.uint8).pin_memory()
+        h_sm = torch.empty(256, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            d_lens.copy_(h_lens, non_blocking=True)
+            d_cls.copy_(h_cls, non_blocking=True)
+            d_off.copy_(h_off, non_blocking=True)
+            d_tok.copy_(h_tok, non_blocking=True)
+            sched.schedule(d_lens, d_cls, d_off, d_tok, sync=False, check=False)
+            h_rb.copy_(sched.req_batch[:n], non_blocking=True)
+            h_bt.copy_(sched.batches_raw[:64 * nb], non_blocking=True)
+            h_sm.copy_(sched.summary, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if pg is not None:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        k_e2e = max(3, min(args.steps, 10))
+        e0.record()
+        for _ in range(k_e2e):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=dev)
+        if pg is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = h_lens.numel() * 4 + h_cls.numel() + h_off.numel() * 8 + h_tok.numel() * 4
+        d2h = n * 4 + 64 * nb + 256
+        e2e = {"value": world * n / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.item()), "steps": k_e2e}
+
+    if rank != 0:
+        if pg is not None:
+            dist.destroy_process_group()
+        return
+
+    cpu_base = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu_base = cpu_baseline(args.config, min(args.cpu_sample, n))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded lengths per BASELINE config, hashed token ids; generated on device)",
+        "impl": "b200",
+        "config": {
+            "workload": f"{args.config}: {cfg.note}", "requests_per_gpu": n,
+            "l_max": cfg.l_max, "classes": cfg.n_classes,
+            "kv_bytes_per_token": cfg.kvpt, "safe_memory_bytes": cfg.current_safe,
+            "accounting": "padded" if cfg.accounting == 0 else "exact",
+            "parallelism": f"dp{world} (request shards, NCCL histogram all-reduce)",
+            "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
+                  % (tokens.numel() * 4 / 1e9, int(s["packed_elems"]) * 5 / 1e9),
+        },
+        "roofline": {"bound": "hbm", "kernel": "k_pack", "achieved": pack_gbs, "peak": peak,
+                     "unit": "GB/s", "frac": (pack_gbs / peak) if pack_gbs else None,
+                     "traffic": _profile_traffic(args.config), "algorithmic_bytes": pack_bytes,
+                     "avg_launch_ms": pack_ms, "peak_source": peak_src},
+        "stages_ms": stage_ms,
+        "schedule_roofline": {"bytes": sched_bytes, "ms": sched_ms,
+                              "achieved_gbs": sched_bytes / (sched_ms / 1e3) / 1e9 if sched_ms else None},
+        "window": {"buckets": int(s["k_buckets"]), "n_max": int(s["n_max"]),
+                   "batches": int(s["n_batches"]), "rejected": int(s["n_rejected"]),
+                   "mean_batch_waste": (s["waste_sum"] / s["n_batches"]) if s["n_batches"] else None},
+        "e2e": e2e,
+        "cpu_baseline": cpu_base,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -258,6 +258,19 @@ int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_par
 int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
                     uint64_t* out, void* stream);
 
+/* ---- instrumentation ---------------------------------------------------------------
+ * Stage timing of the fused window call, recorded with CUDA events on the call's
+ * stream at the K1|K2|K4|K5|K6 boundaries (no host synchronisation while
+ * recording).  bs_profile_enable(ctx, max_steps) arms a ring of max_steps event
+ * sets (0 disarms); bs_profile_read synchronises the recorded events, writes the
+ * summed milliseconds per stage (BS_STAGES floats) and the number of recorded
+ * steps, and resets the ring.  bs_launch_count: kernels launched by ctx so far. */
+#define BS_STAGES 9   /* 0 histogram, 1 boundaries, 2 order, 3 size.prep, 4 size.next,
+                         5 size.chain, 6 size.describe, 7 size.offsets, 8 pack */
+int bs_profile_enable(bs_ctx* ctx, int32_t max_steps);
+int bs_profile_read(bs_ctx* ctx, float* stage_ms, int32_t* steps_out);
+int64_t bs_launch_count(const bs_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

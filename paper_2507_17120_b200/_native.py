@@ -42,7 +42,10 @@ PACK_ALIGN = 4
 
 EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "bs_destroy",
            "bs_histogram", "bs_boundaries", "bs_assign", "bs_order", "bs_size", "bs_pack",
-           "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins")
+           "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_profile_enable",
+           "bs_profile_read", "bs_launch_count")
+STAGES = ("histogram", "boundaries", "order", "size.prep", "size.next", "size.chain",
+          "size.describe", "size.offsets", "pack")
 
 
 class NativeUnavailable(RuntimeError):
@@ -114,6 +117,9 @@ def load():
         "bs_window_schedule": (C.c_int, [vp, C.POINTER(WindowIO), P, vp]),
         "bs_window_from_hist": (C.c_int, [vp, C.POINTER(WindowIO), P, vp]),
         "bs_monitor_bins": (C.c_int, [vp, vp, P, i32, vp, vp]),
+        "bs_profile_enable": (C.c_int, [vp, i32]),
+        "bs_profile_read": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(i32)]),
+        "bs_launch_count": (i64, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -182,6 +188,21 @@ class Context:
     @property
     def scratch_bytes(self) -> int:
         return int(self._lib.bs_scratch_bytes(self.ptr))
+
+    @property
+    def launches(self) -> int:
+        """Kernels launched through this context so far."""
+        return int(self._lib.bs_launch_count(self.ptr))
+
+    def profile_enable(self, max_steps: int):
+        check(self._lib.bs_profile_enable(self.ptr, int(max_steps)), self.ptr)
+
+    def profile_read(self) -> tuple[dict, int]:
+        """(summed ms per stage, steps) of the profiled fused calls since the last read."""
+        ms = (C.c_float * len(STAGES))()
+        steps = C.c_int32(0)
+        check(self._lib.bs_profile_read(self.ptr, ms, C.byref(steps)), self.ptr)
+        return {k: float(ms[i]) for i, k in enumerate(STAGES)}, int(steps.value)
 
     def close(self):
         if self.ptr:

@@ -74,8 +74,8 @@ cudaError_t alloc(bs_ctx* ctx, T** p, size_t count) {
 void free_all(bs_ctx* c) {
   void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->bin_base, c->kinfo,
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
-                  c->bmax, c->bcnt, c->bsum, c->J, c->is_start, c->listA, c->listB,
-                  c->node_batch, c->misc};
+                  c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
+                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->misc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -152,13 +152,14 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(status, 4 * ctx->max_tiles * 256);
   A(tile_ctr, 4);
   A(sorted_len, N);
-  A(bmax, groups); A(bcnt, groups); A(bsum, groups);
+  A(bmax, groups); A(bcnt, groups); A(bsum, groups); A(bmin, groups); A(bmask, groups);
+  A(Rg, groups);
   A(J, (int64_t)ctx->r_cap * N);
   A(is_start, N);
   A(listA, N + 1); A(listB, N + 1);
   A(node_batch, N + 1);
+  A(node_j0, N + 1);
   A(misc, 128);
-#undef A
   // co-resident blocks for the cooperative chain kernel (512 threads)
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(), 512, 0);
@@ -170,6 +171,8 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
     return rc;
   }
   ctx->chain_blocks = per_sm * ctx->num_sms;
+  A(btot, ctx->chain_blocks);
+#undef A
   *out = ctx;
   return BS_OK;
 }
@@ -177,6 +180,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
 int bs_destroy(bs_ctx* ctx) {
   if (!ctx) return BS_OK;
   cudaSetDevice(ctx->device);
+  for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
   free_all(ctx);
   delete ctx;
   return BS_OK;
@@ -190,7 +194,10 @@ int bs_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
   if (!hist_out || (n > 0 && (!len || !cls))) return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (summary) BS_CUDA(bsk::launch_init_summary(summary, n, st), "init_summary");
+  if (summary) {
+    BS_CUDA(bsk::launch_init_summary(summary, n, st), "init_summary");
+    ++ctx->launches;
+  }
   BS_CUDA(bsk::launch_histogram(ctx, len, cls, n, *p, hist_out, summary, st), "k_histogram");
   return BS_OK;
 }
@@ -303,11 +310,14 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                             io->init_edges, io->k_init, io->edges, io->changes, io->changes_cap,
                             io->seg_off, io->summary, st)) != BS_OK)
     return rc;
+  bsk::prof_mark(ctx, 2, st);
   BS_CUDA(bsk::launch_order(ctx, io->len, io->cls, io->n, *p, io->perm, io->bucket, io->summary, st),
           "k_sort_pass");
+  bsk::prof_mark(ctx, 3, st);
   BS_CUDA(bsk::launch_size(ctx, io->len, io->perm, io->seg_off, io->n, *p, io->batches,
                            io->batches_cap, io->req_batch, io->req_row, io->summary, st),
           "k_size");
+  bsk::prof_mark(ctx, 8, st);
   if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
     if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
       return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
@@ -318,6 +328,7 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                              io->out_mask, io->out_capacity, io->summary, st),
             "k_pack");
   }
+  bsk::prof_mark(ctx, 9, st);
   return BS_OK;
 }
 
@@ -341,12 +352,18 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
   if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_io(ctx, io)) != BS_OK) return rc;
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ctx->prof_in_window = true;
+  bsk::prof_mark(ctx, 0, st);
   BS_CUDA(bsk::launch_init_summary(io->summary, io->n, st), "init_summary");
+  ++ctx->launches;
   BS_CUDA(bsk::launch_histogram(ctx, io->len, io->cls, io->n, *p, io->hist, io->summary, st),
           "k_histogram");
+  bsk::prof_mark(ctx, 1, st);
   bs_window_io local = *io;
   local.hist_global = io->hist;
-  return window_from_hist_impl(ctx, &local, p, st);
+  rc = window_from_hist_impl(ctx, &local, p, st);
+  ctx->prof_in_window = false;
+  return rc;
 }
 
 int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
@@ -355,7 +372,13 @@ int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_par
   int rc;
   if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_io(ctx, io)) != BS_OK) return rc;
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  return window_from_hist_impl(ctx, io, p, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ctx->prof_in_window = true;
+  bsk::prof_mark(ctx, 0, st);  // K1 ran in bs_histogram; its stage reads as ~0 here
+  bsk::prof_mark(ctx, 1, st);
+  rc = window_from_hist_impl(ctx, io, p, st);
+  ctx->prof_in_window = false;
+  return rc;
 }
 
 int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
@@ -369,5 +392,43 @@ int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p
           "k_monitor_bins");
   return BS_OK;
 }
+
+int bs_profile_enable(bs_ctx* ctx, int32_t max_steps) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  if (max_steps < 0) return fail(ctx, BS_ERR_INVALID_ARG, "max_steps must be >= 0");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+  ctx->prof_events.clear();
+  ctx->prof_steps = 0;
+  ctx->prof_recorded = 0;
+  const size_t ne = (size_t)max_steps * (BS_STAGES + 1);
+  for (size_t i = 0; i < ne; ++i) {
+    cudaEvent_t e;
+    BS_CUDA(cudaEventCreate(&e), "cudaEventCreate");
+    ctx->prof_events.push_back(e);
+  }
+  ctx->prof_steps = max_steps;
+  return BS_OK;
+}
+
+int bs_profile_read(bs_ctx* ctx, float* stage_ms, int32_t* steps_out) {
+  if (!ctx || !stage_ms || !steps_out) return fail(ctx, BS_ERR_INVALID_ARG, "NULL argument");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  for (int s = 0; s < BS_STAGES; ++s) stage_ms[s] = 0.f;
+  for (int k = 0; k < ctx->prof_recorded; ++k) {
+    cudaEvent_t* ev = &ctx->prof_events[(size_t)k * (BS_STAGES + 1)];
+    BS_CUDA(cudaEventSynchronize(ev[BS_STAGES]), "cudaEventSynchronize");
+    for (int s = 0; s < BS_STAGES; ++s) {
+      float ms = 0.f;
+      BS_CUDA(cudaEventElapsedTime(&ms, ev[s], ev[s + 1]), "cudaEventElapsedTime");
+      stage_ms[s] += ms;
+    }
+  }
+  *steps_out = ctx->prof_recorded;
+  ctx->prof_recorded = 0;
+  return BS_OK;
+}
+
+int64_t bs_launch_count(const bs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 }  // extern "C"

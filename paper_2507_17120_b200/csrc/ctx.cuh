@@ -2,6 +2,7 @@
 #pragma once
 
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -15,7 +16,13 @@ struct bs_ctx {
   int64_t max_tiles = 0;    // K4 tiles per pass
   int chain_blocks = 0;     // co-resident blocks of the cooperative chain kernel
   int64_t scratch_bytes = 0;
+  int64_t launches = 0;     // kernels launched through this ctx
   std::string err;
+  // stage profiler: ring of (BS_STAGES+1) events per recorded step
+  std::vector<cudaEvent_t> prof_events;
+  int prof_steps = 0;       // ring capacity (0 = disabled)
+  int prof_recorded = 0;    // steps recorded since the last read
+  bool prof_in_window = false;  // only the fused window call records stage events
 
   // K2 tables
   uint32_t* P = nullptr;         // [l_cap+1] exclusive prefix of the (global) total histogram
@@ -36,6 +43,11 @@ struct bs_ctx {
   int32_t* bmax = nullptr;       // [max_n/32+1] per 32-position group: max non-rejected length
   int32_t* bcnt = nullptr;       //   non-rejected count
   int32_t* bsum = nullptr;       //   non-rejected length sum
+  int32_t* bmin = nullptr;       //   non-rejected length min
+  uint32_t* bmask = nullptr;     //   bit l: position 32g+l is admissible (len <= S)
+  int32_t* Rg = nullptr;         // [max_n/32+1] exclusive prefix of bcnt
+  int32_t* btot = nullptr;       // [chain_blocks] per-block partials of the Rg scan
+  int32_t* node_j0 = nullptr;    // [max_n + 1] first admissible position at/after each chain node
   int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
   uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
   int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)
@@ -46,6 +58,13 @@ struct bs_ctx {
 };
 
 namespace bsk {
+
+// records boundary event `stage` (0..BS_STAGES) of the current profiled step
+inline void prof_mark(bs_ctx* ctx, int stage, cudaStream_t st) {
+  if (!ctx->prof_in_window || ctx->prof_steps <= 0 || ctx->prof_recorded >= ctx->prof_steps) return;
+  cudaEventRecord(ctx->prof_events[(size_t)ctx->prof_recorded * (BS_STAGES + 1) + stage], st);
+  if (stage == BS_STAGES) ++ctx->prof_recorded;
+}
 
 struct SortPlan {
   int passes;  // radix passes

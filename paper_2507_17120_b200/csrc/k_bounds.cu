@@ -343,6 +343,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
                                      changes_cap, seg_off_out, ctx->P, ctx->PcL, ctx->E, ctx->lut,
                                      ctx->seg_base, ctx->slot_lut, ctx->bin_base, ctx->kinfo,
                                      summary);
+  ++ctx->launches;
   return cudaGetLastError();
 }
 

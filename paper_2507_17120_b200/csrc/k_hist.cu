@@ -93,15 +93,16 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
     attr_set = true;
   }
   const int threads = 512;
-  // each CTA should read >= 8x its flushed bin count
-  int64_t blocks = n / (8LL * C * H) + 1;
+  // >= 8 elements per thread; the flush only touches non-zero bins, so its cost
+  // is bounded by the elements each CTA read
+  int64_t blocks = (n + 8LL * threads - 1) / (8LL * threads);
   blocks = std::min<int64_t>(blocks, 3LL * ctx->num_sms);
-  blocks = std::min<int64_t>(blocks, (n + threads - 1) / threads);
   blocks = std::max<int64_t>(blocks, 1);
   const int vec_ok = ((reinterpret_cast<uintptr_t>(len) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(cls) & 3) == 0);
   k_histogram<<<(unsigned)blocks, threads, smem, st>>>(len, cls, n, L, C, p.truncate, H, vec_ok,
                                                        hist, summary);
+  ++ctx->launches;
   return cudaGetLastError();
 }
 

@@ -104,6 +104,7 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                           p.truncate, p.pad_id, batches, batch_begin, batch_end,
                                           summary, batches_cap, out_tokens, out_mask, out_capacity,
                                           summary);
+  ++ctx->launches;
   return cudaGetLastError();
 }
 

@@ -11,20 +11,23 @@
 // and S = floor(current_safe/kvpt) this is a greedy segmentation: drop len > S,
 // cut where max*(n+1) > T (PADDED) or sum+len > T (EXACT).
 //
-// B200 design (no sequential walk over requests):
-//   K5a  gather lengths into drain order + per-32-position summaries
-//        (max / count / sum of the non-rejected lengths)
-//   K5b  next(j) for EVERY position in parallel: where a form_batch call that
-//        starts at j would stop — a gallop over the 32-position summaries, exact
-//        element steps only at the two ends
-//   K5c  pointer doubling J[r] = next^(2^r) in one cooperative kernel (grid.sync
-//        between levels, stops when every segment's chain is covered), then a
-//        top-down expansion from the segment starts emits every batch start in
-//        emission order — O(N log B) work, O(log B) depth instead of a walk of B
-//        dependent steps per segment
-//   K5d  one CTA per batch: rows (block scan over admitted positions),
-//        reductions, BatchPlan fields, per-request outcome
-//   K5e  one CTA: packed-buffer offsets (exclusive scan of n*pitch) + totals
+// B200 design (no sequential walk over requests; positions = drain order):
+//   K5a  prep      gather lengths into drain order + per-32-position ("group")
+//                  summaries of the admissible lengths: bitmask, count, sum, max, min
+//   K5b  next      next(j) = where a form_batch call starting at j stops, for
+//                  EVERY j.  One warp owns the 32 starts of a group: in-group
+//                  suffix stats by shuffles, then a warp-cooperative gallop over
+//                  32 group summaries per step (shuffle scans + per-lane binary
+//                  search), then <= 32 element steps per lane.  Work per start is
+//                  O(1 + span/1024) warp steps instead of O(span/32) serial loads.
+//   K5c  chain     one cooperative kernel: group-count prefix scan, pointer
+//                  doubling J[r] = next^(2^r) (grid.sync per level, stops when
+//                  every segment's chain is covered), then a top-down expansion
+//                  from the segment starts emitting every batch start in
+//                  emission order — O(N log B) work, O(log B) depth.
+//   K5d  describe  one warp per batch: n / sum / max / min from group summaries
+//   K5e  outcome   one warp per 32 positions: batch id / row / rejected / pending
+//   K5f  offsets   one CTA: packed-buffer offsets (scan of n*pitch) + totals
 #include <cooperative_groups.h>
 
 #include "ctx.cuh"
@@ -44,10 +47,18 @@ struct SizeArgs {
   int32_t pad0;
 };
 
+struct Stat {
+  int64_t m, c, s;  // max, count, sum of the admitted lengths so far
+};
+
+__device__ __forceinline__ bool violates(const SizeArgs& a, int64_t m, int64_t c, int64_t s) {
+  return a.padded ? (m * c > a.T) : (s > a.T);
+}
+
 __device__ __forceinline__ int64_t seg_of(const int32_t* __restrict__ seg_off, int32_t n_segs,
                                           int64_t j) {
   // largest s with seg_off[s] <= j  (upper_bound - 1 over seg_off[0..n_segs])
-  int32_t lo = 0, hi = n_segs;  // answer in [0, n_segs-1]
+  int32_t lo = 0, hi = n_segs;
   while (hi - lo > 1) {
     const int32_t mid = (lo + hi) >> 1;
     if (seg_off[mid] <= j) lo = mid; else hi = mid;
@@ -55,69 +66,68 @@ __device__ __forceinline__ int64_t seg_of(const int32_t* __restrict__ seg_off, i
   return lo;
 }
 
+// first admissible (non-rejected) position in [j, end), or end
 __device__ __forceinline__ int64_t first_nonrej(int64_t j, int64_t end,
-                                                const int32_t* __restrict__ slen,
-                                                const int32_t* __restrict__ bcnt, int64_t S) {
+                                                const uint32_t* __restrict__ bmask) {
   int64_t k = j;
-  while (k < end && (k & 31)) {
-    if (slen[k] <= S) return k;
-    ++k;
-  }
-  while (k + 32 <= end && bcnt[k >> 5] == 0) k += 32;
   while (k < end) {
-    if (slen[k] <= S) return k;
-    ++k;
+    const uint32_t m = bmask[k >> 5] & (0xffffffffu << (k & 31));
+    if (m) {
+      const int64_t p = (k & ~31LL) + (__ffs(m) - 1);
+      return p < end ? p : end;
+    }
+    k = (k & ~31LL) + 32;
   }
   return end;
 }
 
-__device__ __forceinline__ bool fits(const SizeArgs& a, int64_t m, int64_t c, int64_t s) {
-  return a.padded ? (m * c <= a.T) : (s <= a.T);
-}
-
-// first position where the batch that admits j0 first stops (or `end`)
-__device__ int64_t greedy_stop(int64_t j0, int64_t end, const SizeArgs& a,
-                               const int32_t* __restrict__ slen, const int32_t* __restrict__ bmax,
-                               const int32_t* __restrict__ bcnt,
-                               const int32_t* __restrict__ bsum) {
-  int64_t m = slen[j0], c = 1, s = m;
-  int64_t k = j0 + 1;
-  while (k < end && (k & 31)) {
+// admit elements from k while the batch stays feasible; first violating position or end
+__device__ __forceinline__ int64_t extend_elems(int64_t k, int64_t end, Stat& st,
+                                                const SizeArgs& a,
+                                                const int32_t* __restrict__ slen) {
+  for (; k < end; ++k) {
     const int64_t x = slen[k];
     if (x <= a.S) {
-      const int64_t nm = x > m ? x : m;
-      if (!fits(a, nm, c + 1, s + x)) return k;
-      m = nm; ++c; s += x;
+      const int64_t nm = x > st.m ? x : st.m;
+      if (violates(a, nm, st.c + 1, st.s + x)) return k;
+      st.m = nm; ++st.c; st.s += x;
     }
-    ++k;
   }
+  return end;
+}
+
+// per-lane greedy with a serial gallop over group summaries (rare paths only)
+__device__ int64_t greedy_serial(int64_t j0, int64_t end, const SizeArgs& a,
+                                 const int32_t* __restrict__ slen,
+                                 const int32_t* __restrict__ bmax,
+                                 const int32_t* __restrict__ bcnt,
+                                 const int32_t* __restrict__ bsum) {
+  Stat st{slen[j0], 1, slen[j0]};
+  int64_t k = j0 + 1;
+  const int64_t a32 = (k + 31) & ~31LL;
+  const int64_t lim = a32 < end ? a32 : end;
+  k = extend_elems(k, lim, st, a, slen);
+  if (k < lim) return k;  // violated before alignment
   while (k + 32 <= end) {
     const int g = (int)(k >> 5);
     const int64_t bc = bcnt[g];
     if (bc) {
       const int64_t bm = bmax[g];
-      const int64_t nm = bm > m ? bm : m;
-      if (!fits(a, nm, c + bc, s + bsum[g])) break;
-      m = nm; c += bc; s += bsum[g];
+      const int64_t nm = bm > st.m ? bm : st.m;
+      if (violates(a, nm, st.c + bc, st.s + bsum[g])) break;
+      st.m = nm; st.c += bc; st.s += bsum[g];
     }
     k += 32;
   }
-  while (k < end) {
-    const int64_t x = slen[k];
-    if (x <= a.S) {
-      const int64_t nm = x > m ? x : m;
-      if (!fits(a, nm, c + 1, s + x)) return k;
-      m = nm; ++c; s += x;
-    }
-    ++k;
-  }
-  return end;
+  return extend_elems(k, end, st, a, slen);
 }
 
-// K5a
-__global__ void k_size_prep(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
-                            SizeArgs a, int32_t* __restrict__ slen, int32_t* __restrict__ bmax,
-                            int32_t* __restrict__ bcnt, int32_t* __restrict__ bsum) {
+// ---------------------------------------------------------------------------- K5a
+__global__ void __launch_bounds__(256)
+    k_size_prep(const int32_t* __restrict__ len, const int32_t* __restrict__ perm, SizeArgs a,
+                int32_t* __restrict__ slen, uint32_t* __restrict__ bmask,
+                int32_t* __restrict__ bmax, int32_t* __restrict__ bmin,
+                int32_t* __restrict__ bcnt, int32_t* __restrict__ bsum) {
   const int lane = threadIdx.x & 31;
   const int64_t groups = (a.n + 31) >> 5;
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -132,40 +142,134 @@ __global__ void k_size_prep(const int32_t* __restrict__ len, const int32_t* __re
       slen[j] = x;
     }
     const bool nr = valid && (int64_t)x <= a.S;
-    const int32_t v = nr ? x : 0;
-    const int32_t m = warp_max(v);
-    const int32_t s = warp_sum(v);
-    const int32_t c = __popc(__ballot_sync(0xffffffffu, nr));
-    if (lane == 0) { bmax[g] = m; bcnt[g] = c; bsum[g] = s; }
-  }
-}
-
-// K5b
-__global__ void k_size_next(SizeArgs a, const int32_t* __restrict__ kinfo,
-                            const int32_t* __restrict__ seg_off,
-                            const int32_t* __restrict__ slen, const int32_t* __restrict__ bmax,
-                            const int32_t* __restrict__ bcnt, const int32_t* __restrict__ bsum,
-                            int32_t* __restrict__ J0, uint8_t* __restrict__ is_start,
-                            int32_t* __restrict__ alive) {
-  const int32_t n_segs = kinfo[2];
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = seg_of(seg_off, n_segs, j);
-    const int64_t end = seg_off[s + 1];
-    const bool start = seg_off[s] == j;
-    int32_t nx = kEnd;
-    const int64_t j0 = first_nonrej(j, end, slen, bcnt, a.S);
-    if (j0 < end && (int64_t)slen[j0] <= a.T) {
-      const int64_t st = greedy_stop(j0, end, a, slen, bmax, bcnt, bsum);
-      if (st < end) nx = (int32_t)st;
+    const uint32_t m = __ballot_sync(0xffffffffu, nr);
+    const int32_t mx = warp_max(nr ? x : 0);
+    const int32_t mn = -warp_max(nr ? -x : -INT32_MAX);
+    const int32_t s = warp_sum(nr ? x : 0);
+    if (lane == 0) {
+      bmask[g] = m; bcnt[g] = __popc(m); bmax[g] = mx; bmin[g] = mn; bsum[g] = s;
     }
-    J0[j] = nx;
-    is_start[j] = start;
-    if (start && nx != kEnd) alive[0] = 1;
   }
 }
 
-// K5c
+// ---------------------------------------------------------------------------- K5b
+__global__ void __launch_bounds__(256)
+    k_size_next(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
+                const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
+                const int32_t* __restrict__ bmax, const int32_t* __restrict__ bcnt,
+                const int32_t* __restrict__ bsum, int32_t* __restrict__ J0,
+                uint8_t* __restrict__ is_start, int32_t* __restrict__ alive) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int32_t n_segs = kinfo[2];
+  const int64_t G = (a.n + 31) >> 5;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = wg; g < G; g += wstride) {
+    const int64_t j = (g << 5) + lane;
+    const bool valid = j < a.n;
+    const uint32_t nrm = bmask[g];
+    const int32_t x = valid ? slen[j] : 0;
+    int64_t e = 0;
+    bool start = false;
+    if (valid) {
+      const int64_t s = seg_of(seg_off, n_segs, j);
+      e = seg_off[s + 1];
+      start = seg_off[s] == j;
+    }
+    const int64_t gend = ((g << 5) + 32) < a.n ? ((g << 5) + 32) : a.n;
+    const bool nr = valid && ((nrm >> lane) & 1u);
+    // suffix max / sum of the admissible lengths at lanes >= lane
+    int32_t vm = nr ? x : 0;
+    int64_t vs = nr ? x : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t tm = __shfl_down_sync(FULL, vm, o);
+      const int64_t ts = __shfl_down_sync(FULL, vs, o);
+      if (lane + o < 32) { vm = tm > vm ? tm : vm; vs += ts; }
+    }
+    const uint32_t rem = nrm & (FULL << lane);
+    int mode = 0;  // 0 done, 1 gallop, 2 serial fallback, 3 element scan from p
+    int32_t nx = kEnd;
+    Stat st{0, 0, 0};
+    int64_t p = 0;
+    if (valid) {
+      if (e <= gend || rem == 0) {
+        mode = 2;
+      } else {
+        const int64_t f = (g << 5) + (__ffs(rem) - 1);
+        const int64_t xf = slen[f];
+        if (xf > a.T) {
+          mode = 0;  // blocked: form_batch admits nothing, the drain stops here
+        } else if (violates(a, vm, __popc(rem), vs)) {
+          mode = 3; p = f + 1; st = Stat{xf, 1, xf};
+        } else {
+          mode = 1; st = Stat{vm, __popc(rem), vs};
+        }
+      }
+    }
+    // warp-cooperative gallop over 32 group summaries per step
+    int64_t base = g + 1;
+    while (__any_sync(FULL, mode == 1)) {
+      const int64_t gi = base + lane;
+      int32_t pc = 0, pm = 0;
+      int64_t ps = 0;
+      if (gi < G) { pc = bcnt[gi]; pm = bmax[gi]; ps = bsum[gi]; }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t tc = __shfl_up_sync(FULL, pc, o);
+        const int32_t tm = __shfl_up_sync(FULL, pm, o);
+        const int64_t ts = __shfl_up_sync(FULL, ps, o);
+        if (lane >= o) { pc += tc; pm = tm > pm ? tm : pm; ps += ts; }
+      }
+      int ng = 0;
+      if (mode == 1) {
+        const int64_t lim = e / 32 - base;  // full groups of this segment from `base`
+        ng = lim < 0 ? 0 : (lim > 32 ? 32 : (int)lim);
+      }
+      int lo = 0, hi = ng;
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const int src = mid < 31 ? mid : 31;
+        const int32_t qc = __shfl_sync(FULL, pc, src);
+        const int32_t qm = __shfl_sync(FULL, pm, src);
+        const int64_t qs = __shfl_sync(FULL, ps, src);
+        if (lo < hi) {
+          const int64_t nm = qm > st.m ? qm : st.m;
+          if (violates(a, nm, st.c + qc, st.s + qs)) hi = mid; else lo = mid + 1;
+        }
+      }
+      const int src2 = lo - 1 < 0 ? 0 : (lo - 1 > 31 ? 31 : lo - 1);
+      const int32_t bc = __shfl_sync(FULL, pc, src2);
+      const int32_t bm = __shfl_sync(FULL, pm, src2);
+      const int64_t bs = __shfl_sync(FULL, ps, src2);
+      if (mode == 1) {
+        if (lo > 0) { st.m = bm > st.m ? bm : st.m; st.c += bc; st.s += bs; }
+        if (lo < ng) { mode = 3; p = (base + lo) << 5; }        // violation inside that group
+        else if (ng < 32) { mode = 3; p = (base + ng) << 5; }   // segment tail (< 32 elements)
+      }
+      base += 32;
+    }
+    if (mode == 3) {
+      const int64_t k = extend_elems(p, e, st, a, slen);
+      nx = k < e ? (int32_t)k : kEnd;
+    } else if (mode == 2) {
+      const int64_t j0 = first_nonrej(j, e, bmask);
+      if (j0 < e && (int64_t)slen[j0] <= a.T) {
+        const int64_t k = greedy_serial(j0, e, a, slen, bmax, bcnt, bsum);
+        nx = k < e ? (int32_t)k : kEnd;
+      }
+    }
+    if (valid) {
+      J0[j] = nx;
+      is_start[j] = start;
+      if (start && nx != kEnd) alive[0] = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- K5c
 struct ChainShared {
   int32_t si[33];
   int32_t flag;
@@ -177,16 +281,44 @@ __device__ __forceinline__ int32_t ld_rel_i32(const int32_t* p) {
 
 __global__ void __launch_bounds__(512)
     k_chain(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
-            int32_t* J, int r_cap,
-            const uint8_t* __restrict__ is_start, int32_t* alive, int32_t* listA, int32_t* listB,
-            int32_t* node_batch, int32_t* misc, const int32_t* __restrict__ slen,
-            const int32_t* __restrict__ bcnt, int32_t batches_cap, bs_summary* sum) {
+            int32_t* J, int r_cap, const uint8_t* __restrict__ is_start, int32_t* alive,
+            int32_t* listA, int32_t* listB, int32_t* node_batch, int32_t* node_j0, int32_t* misc,
+            const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
+            const int32_t* __restrict__ bcnt, int32_t* __restrict__ Rg, int32_t* btot,
+            int32_t batches_cap, bs_summary* sum) {
   cg::grid_group grid = cg::this_grid();
   __shared__ ChainShared sh;
   const int64_t n = a.n;
   const int32_t n_segs = kinfo[2];
+  const int tid = threadIdx.x, bt = blockDim.x;
+  // ---- phase 0: Rg = exclusive prefix of admissible counts per 32-position group ----
+  {
+    const int64_t G = (n + 31) >> 5;
+    const int64_t per = (G + gridDim.x - 1) / gridDim.x;
+    const int64_t g0 = (int64_t)blockIdx.x * per;
+    const int64_t g1 = g0 + per < G ? g0 + per : G;
+    int32_t loc = 0;
+    for (int64_t g = g0 + tid; g < g1; g += bt) loc += bcnt[g];
+    int32_t tot;
+    block_excl_scan<int32_t>(loc, sh.si, &tot);
+    if (tid == 0) btot[blockIdx.x] = tot;
+    grid.sync();
+    int32_t pre = 0;
+    for (int b = tid; b < (int)blockIdx.x; b += bt) pre += ld_rel_i32(btot + b);
+    int32_t off;
+    block_excl_scan<int32_t>(pre, sh.si, &off);
+    int32_t run = off;
+    for (int64_t base = g0; base < g1; base += bt) {
+      const int64_t g = base + tid;
+      const int32_t v = g < g1 ? bcnt[g] : 0;
+      int32_t t;
+      const int32_t o = block_excl_scan<int32_t>(v, sh.si, &t);
+      if (g < g1) Rg[g] = run + o;
+      run += t;
+    }
+  }
   int r = 0;
-  // ---- pointer doubling -------------------------------------------------------------
+  // ---- phase 1: pointer doubling ---------------------------------------------------------
   while (r + 1 < r_cap && ld_rel_i32(alive + r)) {
     const int32_t* Jr = J + (int64_t)r * n;
     int32_t* Jn = J + (int64_t)(r + 1) * n;
@@ -203,9 +335,8 @@ __global__ void __launch_bounds__(512)
     ++r;
   }
   if (blockIdx.x != 0) return;
-  const int tid = threadIdx.x, bt = blockDim.x;
   if (tid == 0) sh.flag = (r + 1 >= r_cap && ld_rel_i32(alive + r)) ? 1 : 0;
-  // ---- expansion (block 0): segment starts -> all chain nodes, emission order ----------
+  // ---- phase 2 (block 0): expansion from the segment starts, emission order ----------
   int32_t cnt = 0;
   for (int base = 0; base < n_segs; base += bt) {
     const int s = base + tid;
@@ -239,7 +370,7 @@ __global__ void __launch_bounds__(512)
     cnt = run;
     __syncthreads();
   }
-  // ---- batch ids: a chain node is a batch unless it is a segment's empty tail --------
+  // ---- batch ids: a chain node is a batch unless it is its segment's empty tail -----------
   int32_t nb = 0;
   for (int base = 0; base < cnt; base += bt) {
     const int i = base + tid;
@@ -248,8 +379,9 @@ __global__ void __launch_bounds__(512)
       const int64_t c = cur[i];
       const int64_t s = seg_of(seg_off, n_segs, c);
       const int64_t end = seg_off[s + 1];
-      const int64_t j0 = first_nonrej(c, end, slen, bcnt, a.S);
+      const int64_t j0 = first_nonrej(c, end, bmask);
       f = (j0 < end) && ((int64_t)slen[j0] <= a.T);
+      node_j0[i] = (int32_t)j0;
     }
     int32_t tot;
     const int32_t off = block_excl_scan<int32_t>(f, sh.si, &tot);
@@ -267,107 +399,144 @@ __global__ void __launch_bounds__(512)
   }
 }
 
-// K5d
+// ---------------------------------------------------------------------------- K5d
 __global__ void __launch_bounds__(256)
     k_size_describe(SizeArgs a, const int32_t* __restrict__ kinfo,
-                    const int32_t* __restrict__ seg_off,
-                    const int32_t* __restrict__ perm, const int32_t* __restrict__ slen,
-                    const int32_t* __restrict__ bcnt, const int32_t* __restrict__ J0,
-                    const int32_t* __restrict__ listA, const int32_t* __restrict__ listB,
-                    const int32_t* __restrict__ node_batch, const int32_t* __restrict__ misc,
-                    bs_batch* __restrict__ batches, int32_t batches_cap,
-                    int32_t* __restrict__ req_batch, int32_t* __restrict__ req_row,
-                    bs_summary* sum) {
-  __shared__ int32_t s_i[33];
-  __shared__ int64_t s_l[33];
-  __shared__ int32_t s_m[32], s_mn[32];
+                    const int32_t* __restrict__ seg_off, const int32_t* __restrict__ slen,
+                    const int32_t* __restrict__ bmax, const int32_t* __restrict__ bmin,
+                    const int32_t* __restrict__ bcnt, const int32_t* __restrict__ bsum,
+                    const int32_t* __restrict__ J0, const int32_t* __restrict__ listA,
+                    const int32_t* __restrict__ listB, const int32_t* __restrict__ node_batch,
+                    const int32_t* __restrict__ misc, bs_batch* __restrict__ batches,
+                    int32_t batches_cap, bs_summary* sum) {
   const int M = misc[64];
   const int32_t n_segs = kinfo[2];
   const int32_t* list = misc[68] ? listB : listA;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  int64_t rej_acc = 0, pend_acc = 0;
-  for (int i = blockIdx.x; i < M; i += gridDim.x) {
-    const int64_t c = list[i];
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned fl = 0;
+  for (int64_t i = wg; i < M; i += wstride) {
     const int32_t b = node_batch[i];
+    if (b < 0 || b >= batches_cap) continue;
+    const int64_t c = list[i];
     const int64_t s = seg_of(seg_off, n_segs, c);
-    const int64_t send = seg_off[s + 1];
-    if (b >= 0) {
-      const int32_t nx = J0[c];
-      const int64_t e = nx == kEnd ? send : nx;
-      int32_t run = 0, mx = 0, mn = 0x7fffffff;
-      int64_t tsum = 0;
-      for (int64_t base = c; base < e; base += blockDim.x) {
-        const int64_t j = base + tid;
-        int32_t x = 0;
-        bool nr = false;
-        if (j < e) { x = slen[j]; nr = (int64_t)x <= a.S; }
-        int32_t tot;
-        const int32_t off = block_excl_scan<int32_t>(nr, s_i, &tot);
-        if (j < e) {
-          const int32_t r = perm[j];
-          if (nr) { req_batch[r] = b; req_row[r] = run + off; }
-          else { req_batch[r] = BS_REQ_REJECTED; req_row[r] = -1; }
-        }
-        if (nr) { mx = x > mx ? x : mx; mn = x < mn ? x : mn; tsum += x; }
-        run += tot;
+    const int32_t nx = J0[c];
+    const int64_t e = nx == kEnd ? (int64_t)seg_off[s + 1] : (int64_t)nx;
+    int64_t cnt = 0, tsum = 0;
+    int32_t mx = 0, mn = INT32_MAX;
+    const int64_t ca = (c + 31) & ~31LL, eb = e & ~31LL;
+    if (ca >= eb) {
+      for (int64_t k = c + lane; k < e; k += 32) {
+        const int32_t x = slen[k];
+        if ((int64_t)x <= a.S) { ++cnt; tsum += x; mx = x > mx ? x : mx; mn = x < mn ? x : mn; }
       }
-      // block reductions
-      int32_t wm = warp_max(mx);
-      int32_t wmn = -warp_max(-mn);
-      int64_t ws = warp_sum(tsum);
-      if (lane == 0) { s_m[wid] = wm; s_mn[wid] = wmn; s_l[wid] = ws; }
-      __syncthreads();
-      if (tid == 0) {
-        int32_t m = 0, mnv = 0x7fffffff;
-        int64_t ssum = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-          m = s_m[w] > m ? s_m[w] : m;
-          mnv = s_mn[w] < mnv ? s_mn[w] : mnv;
-          ssum += s_l[w];
-        }
-        if (b < batches_cap) {
-          bs_batch B;
-          B.segment = (int32_t)s;
-          B.start = (int32_t)c;
-          B.end = (int32_t)e;
-          B.n = run;
-          B.max_input_len = m;
-          B.pitch = (m + BS_PACK_ALIGN - 1) / BS_PACK_ALIGN * BS_PACK_ALIGN;
-          B.token_sum = ssum;
-          B.footprint = a.kvpt * (a.padded ? (int64_t)m * run : ssum);
-          B.out_offset = 0;
-          // waste_ratio (memory_model.py:98-100): (s_max - s_avg) / s_max, float64
-          const double s_avg = __ddiv_rn((double)ssum, (double)run);
-          double wr = __ddiv_rn(__dsub_rn((double)m, s_avg), (double)m);
-          if (mnv < 1) {  // waste_ratio raises ValueError for lengths < 1
-            wr = __longlong_as_double(0x7ff8000000000000ll);
-            latch_flags(sum, BS_FLAG_NONPOS_LEN);
-          }
-          B.waste = wr;
-          B.reserved = 0;
-          batches[b] = B;
-        }
-        rej_acc += (e - c) - run;
-      }
-      __syncthreads();
     } else {
-      // empty tail: rejected up to the first admissible request, pending after it
-      const int64_t j0 = first_nonrej(c, send, slen, bcnt, a.S);
-      for (int64_t j = c + tid; j < send; j += blockDim.x) {
-        const int32_t r = perm[j];
-        req_batch[r] = j < j0 ? BS_REQ_REJECTED : BS_REQ_PENDING;
-        req_row[r] = -1;
+      for (int64_t k = c + lane; k < ca; k += 32) {
+        const int32_t x = slen[k];
+        if ((int64_t)x <= a.S) { ++cnt; tsum += x; mx = x > mx ? x : mx; mn = x < mn ? x : mn; }
       }
-      if (tid == 0) { rej_acc += j0 - c; pend_acc += send - j0; }
+      for (int64_t gg = (ca >> 5) + lane; gg < (eb >> 5); gg += 32) {
+        const int32_t bc = bcnt[gg];
+        if (bc) {
+          cnt += bc; tsum += bsum[gg];
+          mx = bmax[gg] > mx ? bmax[gg] : mx;
+          mn = bmin[gg] < mn ? bmin[gg] : mn;
+        }
+      }
+      for (int64_t k = eb + lane; k < e; k += 32) {
+        const int32_t x = slen[k];
+        if ((int64_t)x <= a.S) { ++cnt; tsum += x; mx = x > mx ? x : mx; mn = x < mn ? x : mn; }
+      }
+    }
+    cnt = warp_sum(cnt);
+    tsum = warp_sum(tsum);
+    mx = warp_max(mx);
+    mn = -warp_max(-mn);
+    if (lane == 0) {
+      bs_batch B;
+      B.segment = (int32_t)s;
+      B.start = (int32_t)c;
+      B.end = (int32_t)e;
+      B.n = (int32_t)cnt;
+      B.max_input_len = mx;
+      B.pitch = (mx + BS_PACK_ALIGN - 1) / BS_PACK_ALIGN * BS_PACK_ALIGN;
+      B.token_sum = tsum;
+      B.footprint = a.kvpt * (a.padded ? (int64_t)mx * cnt : tsum);
+      B.out_offset = 0;
+      // waste_ratio (memory_model.py:98-100): (s_max - s_avg) / s_max, float64
+      const double s_avg = __ddiv_rn((double)tsum, (double)cnt);
+      double wr = __ddiv_rn(__dsub_rn((double)mx, s_avg), (double)mx);
+      if (mn < 1) {  // waste_ratio raises ValueError for lengths < 1 (memory_model.py:96-97)
+        wr = __longlong_as_double(0x7ff8000000000000ll);
+        fl |= BS_FLAG_NONPOS_LEN;
+      }
+      B.waste = wr;
+      B.reserved = 0;
+      batches[b] = B;
     }
   }
-  if (tid == 0) {
-    if (rej_acc) add_i64(&sum->n_rejected, rej_acc);
-    if (pend_acc) add_i64(&sum->n_pending, pend_acc);
+  if (lane == 0) latch_flags(sum, fl);
+}
+
+// ---------------------------------------------------------------------------- K5e
+__global__ void __launch_bounds__(256)
+    k_size_outcome(SizeArgs a, const int32_t* __restrict__ perm, const uint32_t* __restrict__ bmask,
+                   const int32_t* __restrict__ Rg, const int32_t* __restrict__ listA,
+                   const int32_t* __restrict__ listB, const int32_t* __restrict__ node_batch,
+                   const int32_t* __restrict__ node_j0, const int32_t* __restrict__ misc,
+                   int32_t* __restrict__ req_batch, int32_t* __restrict__ req_row,
+                   bs_summary* sum) {
+  const int M = misc[64];
+  const int32_t* list = misc[68] ? listB : listA;
+  const int lane = threadIdx.x & 31;
+  const int64_t G = (a.n + 31) >> 5;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t rej = 0, pend = 0;
+  for (int64_t g = wg; g < G; g += wstride) {
+    const int64_t j = (g << 5) + lane;
+    if (j >= a.n) continue;
+    // chain node covering j: last node position <= j (nodes ascend and every segment
+    // start is a node, so the node lies in j's segment)
+    int lo = 0, hi = M;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (list[mid] <= j) lo = mid; else hi = mid;
+    }
+    const int64_t c = list[lo];
+    const int32_t b = node_batch[lo];
+    const uint32_t m = bmask[g];
+    const bool nr = (m >> lane) & 1u;
+    const int32_t r = perm[j];
+    if (b >= 0) {
+      if (nr) {
+        const int64_t gc = c >> 5;
+        const int32_t Rj = Rg[g] + __popc(m & ((1u << lane) - 1u));
+        const int32_t Rc = Rg[gc] + __popc(bmask[gc] & ((1u << (c & 31)) - 1u));
+        req_batch[r] = b;
+        req_row[r] = Rj - Rc;
+      } else {
+        req_batch[r] = BS_REQ_REJECTED;
+        req_row[r] = -1;
+        ++rej;
+      }
+    } else {  // a segment's empty tail: rejected up to the first admissible request, pending after
+      const int64_t j0 = node_j0[lo];
+      req_row[r] = -1;
+      if (j < j0) { req_batch[r] = BS_REQ_REJECTED; ++rej; }
+      else { req_batch[r] = BS_REQ_PENDING; ++pend; }
+    }
+  }
+  rej = warp_sum(rej);
+  pend = warp_sum(pend);
+  if (lane == 0) {
+    if (rej) add_i64(&sum->n_rejected, rej);
+    if (pend) add_i64(&sum->n_pending, pend);
   }
 }
 
-// K5e
+// ---------------------------------------------------------------------------- K5f
 __global__ void __launch_bounds__(1024)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
                    const int32_t* __restrict__ misc, bs_summary* sum) {
@@ -429,10 +598,13 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         int32_t* req_row, bs_summary* summary, cudaStream_t st) {
   cudaError_t e;
   const int64_t H = p.current_safe - p.pledged;
+  if (n == 0 || H <= 0)
+    for (int s = 4; s <= 7; ++s) prof_mark(ctx, s, st);
   if (n == 0) return cudaSuccess;
   if (H <= 0) {  // form_batch returns None before touching the queue (:150-152)
-    k_fill_pending<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4LL * ctx->num_sms), 256, 0, st>>>(
-        n, req_batch, req_row, summary);
+    k_fill_pending<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4LL * ctx->num_sms), 256, 0,
+                     st>>>(n, req_batch, req_row, summary);
+    ++ctx->launches;
     return cudaGetLastError();
   }
   SizeArgs a;
@@ -448,37 +620,51 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   e = cudaMemsetAsync(misc, 0, sizeof(int32_t) * 128, st);
   if (e != cudaSuccess) return e;
   const int64_t groups = (n + 31) >> 5;
-  const unsigned pb = (unsigned)std::min<int64_t>((groups * 32 + 255) / 256, 8LL * ctx->num_sms);
-  k_size_prep<<<pb, 256, 0, st>>>(len, perm, a, ctx->sorted_len, ctx->bmax, ctx->bcnt, ctx->bsum);
+  const unsigned wblocks = (unsigned)std::min<int64_t>((groups + 7) / 8, 16LL * ctx->num_sms);
+  k_size_prep<<<wblocks, 256, 0, st>>>(len, perm, a, ctx->sorted_len, ctx->bmask, ctx->bmax,
+                                       ctx->bmin, ctx->bcnt, ctx->bsum);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const unsigned nbk = (unsigned)std::min<int64_t>((n + 255) / 256, 8LL * ctx->num_sms);
-  k_size_next<<<nbk, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax, ctx->bcnt, ctx->bsum,
-                                   ctx->J, ctx->is_start, misc);
+  prof_mark(ctx, 4, st);
+  k_size_next<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmask,
+                                       ctx->bmax, ctx->bcnt, ctx->bsum, ctx->J, ctx->is_start,
+                                       misc);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  prof_mark(ctx, 5, st);
   {
     int r_cap = ctx->r_cap;
-    const int32_t* so = seg_off;
     const int32_t* ki = ctx->kinfo;
+    const int32_t* so = seg_off;
     int32_t* J = ctx->J;
     const uint8_t* is_start = ctx->is_start;
     int32_t* alive = misc;
-    int32_t *la = ctx->listA, *lb = ctx->listB, *nbp = ctx->node_batch;
+    int32_t *la = ctx->listA, *lb = ctx->listB, *nbp = ctx->node_batch, *nj0 = ctx->node_j0;
     const int32_t* sl = ctx->sorted_len;
+    const uint32_t* bm = ctx->bmask;
     const int32_t* bc = ctx->bcnt;
+    int32_t* rg = ctx->Rg;
+    int32_t* bt = ctx->btot;
     int32_t bcap = batches_cap;
     bs_summary* sm = summary;
-    void* args[] = {&a, (void*)&ki, (void*)&so, &J, &r_cap, (void*)&is_start, &alive, &la, &lb, &nbp, &misc,
-                    (void*)&sl, (void*)&bc, &bcap, &sm};
+    void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
+                    &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
+                    (void*)&bc, &rg,   &bt,        &bcap, &sm};
     e = cudaLaunchCooperativeKernel((void*)k_chain, dim3(ctx->chain_blocks), dim3(512), args, 0,
                                     st);
     if (e != cudaSuccess) return e;
   }
-  const unsigned db = (unsigned)(4 * ctx->num_sms);
-  k_size_describe<<<db, 256, 0, st>>>(a, ctx->kinfo, seg_off, perm, ctx->sorted_len, ctx->bcnt, ctx->J,
-                                      ctx->listA, ctx->listB, ctx->node_batch, misc, batches,
-                                      batches_cap, req_batch, req_row, summary);
+  prof_mark(ctx, 6, st);
+  k_size_describe<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax,
+                                           ctx->bmin, ctx->bcnt, ctx->bsum, ctx->J, ctx->listA,
+                                           ctx->listB, ctx->node_batch, misc, batches,
+                                           batches_cap, summary);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_size_outcome<<<wblocks, 256, 0, st>>>(a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB,
+                                          ctx->node_batch, ctx->node_j0, misc, req_batch,
+                                          req_row, summary);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  prof_mark(ctx, 7, st);
   k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, summary);
+  ctx->launches += 6;
   return cudaGetLastError();
 }
 

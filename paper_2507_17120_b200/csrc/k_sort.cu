@@ -164,6 +164,7 @@ cudaError_t launch_assign(bs_ctx* ctx, const int32_t* len, int64_t n, const bs_w
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8LL * ctx->num_sms);
   k_assign<<<(unsigned)blocks, 256, 0, st>>>(len, n, p.l_max, p.truncate, ctx->lut, bucket_out,
                                               nullptr);
+  ++ctx->launches;
   return cudaGetLastError();
 }
 
@@ -208,6 +209,7 @@ cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, in
           ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    ++ctx->launches;
     kin = kout;
     vin = vout;
   }

@@ -108,18 +108,36 @@ def gen_arrivals(cfg: Config, n: int, rng: np.random.Generator, rate: float = 10
     return np.sort(starts)
 
 
+_HASH_MUL = 2654435761
+
+
 def token_store(lens: np.ndarray, rng: np.random.Generator | None = None, vocab: int = 32000,
                 align: int = 4, seed: int = 0):
     """CSR token store: row i starts at tok_off[i] (multiple of `align` tokens so
-    rows are 16-byte aligned for 128-bit loads) and holds lens[i] synthetic ids."""
+    rows are 16-byte aligned for 128-bit loads) and holds lens[i] synthetic ids.
+    Token at global slot p is ((p * 2654435761 + seed) mod 2^32) mod vocab."""
     lens = np.asarray(lens, np.int64)
     pitch = (lens + align - 1) // align * align
     tok_off = np.zeros(len(lens) + 1, np.int64)
     np.cumsum(pitch, out=tok_off[1:])
     total = int(tok_off[-1])
-    # deterministic ids without a huge RNG call: hash of the global position
-    pos = np.arange(total, dtype=np.uint64)
-    tokens = ((pos * np.uint64(2654435761) + np.uint64(seed * 97 + 1)) % np.uint64(vocab)).astype(np.int32)
+    pos = np.arange(total, dtype=np.uint32)
+    pos *= np.uint32(_HASH_MUL)
+    pos += np.uint32(seed & 0xFFFFFFFF)
+    pos %= np.uint32(vocab)
+    return tok_off, pos.view(np.int32)
+
+
+def token_store_device(lens, vocab: int = 32000, align: int = 4, seed: int = 0):
+    """Same store as token_store(), generated on the GPU (torch tensors)."""
+    import torch
+    lens = lens.to(torch.int64)
+    pitch = (lens + align - 1) // align * align
+    tok_off = torch.zeros(lens.numel() + 1, dtype=torch.int64, device=lens.device)
+    torch.cumsum(pitch, 0, out=tok_off[1:])
+    total = int(tok_off[-1].item())
+    pos = torch.arange(total, dtype=torch.int64, device=lens.device)
+    tokens = (((pos * _HASH_MUL + (seed & 0xFFFFFFFF)) & 0xFFFFFFFF) % vocab).to(torch.int32)
     return tok_off, tokens
 
 

@@ -69,3 +69,157 @@ def test_gpu_matches_reference_fixture(name):
     assert h["summary"]["n_rejected"] == o.summary["n_rejected"]
     assert h["summary"]["n_pending"] == o.summary["n_pending"]
     sched.close()
+
+
+def _cfg_spec(cfg):
+    return dict(l_max=cfg.l_max, n_classes=cfg.n_classes, policies=cfg.policies,
+                theta=cfg.theta, adjust=cfg.adjust, max_passes=0, init_edges=cfg.init_edges,
+                kvpt=cfg.kvpt, current_safe=cfg.current_safe, pledged=0,
+                accounting=cfg.accounting, truncate=True)
+
+
+def _compare_with_oracle(spec, lens, cls, pack=True, sample_rows=None):
+    n = len(lens)
+    tok_off = tokens = None
+    if pack:
+        tok_off, tokens = W.token_store(lens)
+    sched = _sched(spec, n)
+    dev = torch.device("cuda", 0)
+    res = sched.schedule(torch.as_tensor(lens).to(dev), torch.as_tensor(cls).to(dev),
+                         None if tok_off is None else torch.as_tensor(tok_off).to(dev),
+                         None if tokens is None else torch.as_tensor(tokens).to(dev))
+    h = res.to_host()
+    o = _oracle(spec, lens, cls, tok_off if (pack and sample_rows is None) else None,
+                tokens if (pack and sample_rows is None) else None)
+    want = canonical(edges=o.edges, bucket=o.bucket, perm=o.perm, req_batch=o.req_batch,
+                     req_row=o.req_row, batches=o.batches, n_max=o.summary["n_max"],
+                     changes=o.changes, n_passes=o.summary["n_passes"])
+    errs = diff(_canon_gpu(h), want, bit_exact_waste=True)
+    assert not errs, "; ".join(errs)
+    assert np.array_equal(h["perm"], o.perm)
+    assert np.array_equal(h["seg_off"], o.seg_off)
+    b = h["batches"]
+    for f in ("segment", "start", "end", "n", "max_input_len", "pitch", "token_sum", "footprint",
+              "out_offset"):
+        assert np.array_equal(b[f], o.batches[f]), f
+    if pack:
+        m = int(h["summary"]["packed_elems"])
+        assert m == int(o.summary["packed_elems"])
+        if sample_rows is None:
+            assert np.array_equal(h["out_tokens"][:m], o.out_tokens[:m])
+            assert np.array_equal(h["out_mask"][:m], o.out_mask[:m])
+        else:  # size-independent property at full scale: sampled rows equal the token store
+            rng = np.random.default_rng(0)
+            adm = np.nonzero(h["req_batch"] >= 0)[0]
+            for r in rng.choice(adm, size=min(sample_rows, len(adm)), replace=False):
+                bb = b[h["req_batch"][r]]
+                row = int(h["req_row"][r])
+                off = int(bb["out_offset"]) + row * int(bb["pitch"])
+                x = int(min(lens[r], spec["l_max"] - 1))
+                assert np.array_equal(h["out_tokens"][off:off + x], tokens[tok_off[r]:tok_off[r] + x])
+                assert not h["out_tokens"][off + x:off + int(bb["pitch"])].any()
+                assert h["out_mask"][off:off + x].all()
+                assert not h["out_mask"][off + x:off + int(bb["pitch"])].any()
+            # every admitted token lands exactly once: packed mask total == admitted tokens
+            assert int(h["out_mask"][:m].sum(dtype=np.int64)) == int(h["summary"]["admitted_tokens"])
+    sched.close()
+    return h
+
+
+def test_c2_full_1m_bit_exact():
+    """BASELINE configs[1] at full size (1M): schedule + pack bit-exact vs the oracle."""
+    cfg, lens, cls = W.make_window("c2", seed=1234)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+
+
+def test_c1_fixed_edges_1k():
+    cfg, lens, cls = W.make_window("c1", seed=5)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+
+
+def test_c3_four_class_4m():
+    cfg, lens, cls = W.make_window("c3", n=4_000_000, seed=21)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True, sample_rows=2000)
+
+
+def test_c4_long_context_pack():
+    cfg, lens, cls = W.make_window("c4", n=20_000, seed=8)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_configs_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    L = int(rng.choice([16, 100, 1000, 4096, 65536]))
+    n = int(rng.integers(1, 60_000))
+    C = int(rng.integers(1, 5))
+    pol = tuple(int(v) for v in rng.integers(0, 3, size=C))
+    kvpt = int(rng.choice([2, 6, 524288]))
+    lens = np.clip(np.rint(rng.lognormal(np.log(L / 8) + 0.1, 1.2, size=n)), 0, L + 10).astype(np.int32)
+    cls = rng.integers(0, C, size=n).astype(np.uint8)
+    budget_tokens = int(rng.integers(1, 40 * L))
+    spec = dict(l_max=L, n_classes=C, policies=pol, theta=float(rng.choice([0.29, 0.5, 0.7, 1.0])),
+                adjust=bool(rng.random() < 0.85), max_passes=int(rng.choice([0, 0, 1, 3])),
+                init_edges=None, kvpt=kvpt, current_safe=kvpt * budget_tokens + int(rng.integers(0, kvpt)),
+                pledged=int(rng.choice([0, 0, kvpt * int(rng.integers(0, budget_tokens))])),
+                accounting=int(rng.integers(0, 2)), truncate=True)
+    _compare_with_oracle(spec, lens, cls, pack=bool(L <= 4096))
+
+
+def test_repeated_windows_reuse_buffers():
+    cfg, lens, cls = W.make_window("c2", n=200_000, seed=77)
+    spec = _cfg_spec(cfg)
+    sched = _sched(spec, 300_000)
+    dev = torch.device("cuda", 0)
+    outs = []
+    for k in range(3):
+        l = lens[: 200_000 - 50_000 * k]
+        c = cls[: len(l)]
+        tok_off, tokens = W.token_store(l)
+        res = sched.schedule(torch.as_tensor(l).to(dev), torch.as_tensor(c).to(dev),
+                             torch.as_tensor(tok_off).to(dev), torch.as_tensor(tokens).to(dev))
+        h = res.to_host()
+        o = _oracle(spec, l, c)
+        assert np.array_equal(h["perm"], o.perm)
+        assert np.array_equal(h["req_batch"], o.req_batch)
+        outs.append(h["summary"]["n_batches"])
+    sched.close()
+
+
+def test_length_out_of_range_raises_like_assign():
+    spec = dict(l_max=1024, n_classes=2, policies=(0, 1), theta=0.5, adjust=True, max_passes=0,
+                init_edges=None, kvpt=2, current_safe=2 * 10000, pledged=0, accounting=0,
+                truncate=False)
+    sched = _sched(spec, 100)
+    with pytest.raises(ValueError):
+        sched.schedule(np.array([5, 1024, 7], np.int32), np.array([0, 1, 0], np.uint8))
+    with pytest.raises(ValueError):
+        sched.schedule(np.array([5, -1], np.int32), np.array([0, 1], np.uint8))
+    with pytest.raises(ValueError):
+        sched.schedule(np.array([5, 6], np.int32), np.array([0, 2], np.uint8))
+    sched.close()
+
+
+def test_bad_initial_edges_raise():
+    spec = dict(l_max=1024, n_classes=2, policies=(0, 1), theta=0.5, adjust=True, max_passes=1,
+                init_edges=(0, 500, 400, 1024), kvpt=2, current_safe=2 * 10000, pledged=0,
+                accounting=0, truncate=True)
+    sched = _sched(spec, 10)
+    with pytest.raises(ValueError):
+        sched.schedule(np.array([5, 6], np.int32), np.array([0, 1], np.uint8))
+    sched.close()
+
+
+def test_monitor_bins_match_numpy_histogram():
+    cfg, lens, cls = W.make_window("c2", n=100_000, seed=4)
+    sched = _sched(_cfg_spec(cfg), len(lens))
+    sched.schedule(lens, cls)
+    got = sched.monitor_bins(64)
+    want, _ = np.histogram(lens.astype(float), bins=64, range=(0, cfg.l_max))
+    assert np.array_equal(got, want)
+    sched.close()
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
