@@ -110,7 +110,7 @@ typedef struct bs_batch {
   int64_t footprint;      /* BatchPlan.footprint (bytes, accounting mode)             */
   int64_t out_offset;     /* element offset of row 0 in the packed token/mask buffers */
   double  waste;          /* waste_ratio(lengths), memory_model.py:92-100             */
-  int64_t reserved;
+  int64_t row_base;       /* admitted rows of the window before this batch            */
 } bs_batch;               /* 64 bytes */
 
 /* ---- window summary (device memory) ----------------------------------------- */
@@ -202,15 +202,15 @@ int bs_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t*
             int32_t* req_batch_out, int32_t* req_row_out, bs_summary* summary, void* stream);
 
 /* ---- K6: pack ------------------------------------------------------------------------
- * For batches [batch_begin, batch_end) (batch_end < 0: all), writes each admitted
- * request's tokens tokens[tok_off[i] .. tok_off[i]+len_i) into row req_row[i] of
- * its batch: out_tokens[out_offset + row*pitch + t], pad_id beyond len_i, and
- * out_mask (1 for real tokens, 0 for padding; may be NULL).  Offsets are relative
- * to the first packed batch of the call (chunked packing into a reusable buffer);
- * out_capacity is in elements.  Rows are 16-byte aligned when tok_off[i] % 4 == 0. */
-int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t* req_batch,
-            const int32_t* req_row, const int64_t* tok_off, const int32_t* tokens,
-            const bs_window_params* p, const bs_batch* batches,
+ * For batches [batch_begin, batch_end) (batch_end < 0: all), writes row q of batch b —
+ * the q-th admitted request i of that form_batch call — as
+ * out_tokens[out_offset + q*pitch + t] = tokens[tok_off[i] + t] for t < len_i, pad_id
+ * beyond, and out_mask (1 for real tokens, 0 for padding; may be NULL).  Offsets are
+ * relative to the first packed batch of the call (chunked packing into a reusable
+ * buffer); out_capacity is in elements.  Uses the row map of the last bs_size call on
+ * ctx.  Rows are moved with 128-bit accesses when tok_off[i] % 4 == 0. */
+int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int64_t* tok_off,
+            const int32_t* tokens, const bs_window_params* p, const bs_batch* batches,
             int64_t batch_begin, int64_t batch_end, int32_t* out_tokens, uint8_t* out_mask,
             int64_t out_capacity, bs_summary* summary, void* stream);
 
@@ -266,7 +266,7 @@ int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p
  * summed milliseconds per stage (BS_STAGES floats) and the number of recorded
  * steps, and resets the ring.  bs_launch_count: kernels launched by ctx so far. */
 #define BS_STAGES 9   /* 0 histogram, 1 boundaries, 2 order, 3 size.prep, 4 size.next,
-                         5 size.chain, 6 size.describe, 7 size.offsets, 8 pack */
+                         5 size.chain, 6 size.describe(+offsets), 7 size.outcome, 8 pack */
 int bs_profile_enable(bs_ctx* ctx, int32_t max_steps);
 int bs_profile_read(bs_ctx* ctx, float* stage_ms, int32_t* steps_out);
 int64_t bs_launch_count(const bs_ctx* ctx);

@@ -38,7 +38,7 @@ typedef struct {
   int32_t segment, start, end, n, max_input_len, pitch;
   int64_t token_sum, footprint, out_offset;
   double waste;
-  int64_t reserved;
+  int64_t row_base;
 } bso_batch;
 
 typedef struct {
@@ -314,7 +314,7 @@ int bso_size(const int32_t* len, const int32_t* perm, const int32_t* seg_off, in
   for (int64_t i = 0; i < n; ++i) { req_batch[i] = REQ_PENDING; req_row[i] = -1; }
   const int64_t kvpt = p->kvpt;
   const int64_t H = p->current_safe - p->pledged;
-  int64_t nb = 0, nrej = 0, admitted = 0, padded = 0, packed = 0, peak = 0;
+  int64_t nb = 0, nrej = 0, admitted = 0, padded = 0, packed = 0, peak = 0, admitted_rows = 0;
   double wsum = 0.0;
   if (H > 0) {
     const int64_t T = H / kvpt;
@@ -349,7 +349,7 @@ int bso_size(const int32_t* len, const int32_t* perm, const int32_t* seg_off, in
           B->waste = ((double)m - s_avg) / (double)m;
           /* waste_ratio raises for any length < 1 (memory_model.py:96-97): NaN + flag */
           if (nonpos) B->waste = NAN;
-          B->reserved = 0;
+          B->row_base = admitted_rows;
           wsum += B->waste;
           if (B->footprint > peak) peak = B->footprint;
           packed += (int64_t)B->pitch * cnt;
@@ -357,7 +357,7 @@ int bso_size(const int32_t* len, const int32_t* perm, const int32_t* seg_off, in
           fl |= F_BATCH_CAP;
         }
         if (nonpos) fl |= F_NONPOS;
-        admitted += tsum; padded += m * cnt;
+        admitted += tsum; padded += m * cnt; admitted_rows += cnt;
         ++nb;
       }
     }

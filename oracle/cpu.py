@@ -37,7 +37,7 @@ class Summary(C.Structure):
 BATCH_DTYPE = np.dtype([("segment", "<i4"), ("start", "<i4"), ("end", "<i4"), ("n", "<i4"),
                         ("max_input_len", "<i4"), ("pitch", "<i4"), ("token_sum", "<i8"),
                         ("footprint", "<i8"), ("out_offset", "<i8"), ("waste", "<f8"),
-                        ("reserved", "<i8")])
+                        ("row_base", "<i8")])
 assert BATCH_DTYPE.itemsize == 64
 
 

@@ -45,7 +45,7 @@ EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "
            "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_profile_enable",
            "bs_profile_read", "bs_launch_count")
 STAGES = ("histogram", "boundaries", "order", "size.prep", "size.next", "size.chain",
-          "size.describe", "size.offsets", "pack")
+          "size.describe", "size.outcome", "pack")
 
 
 class NativeUnavailable(RuntimeError):
@@ -74,7 +74,7 @@ class WindowIO(C.Structure):
 BATCH_DTYPE = np.dtype([("segment", "<i4"), ("start", "<i4"), ("end", "<i4"), ("n", "<i4"),
                         ("max_input_len", "<i4"), ("pitch", "<i4"), ("token_sum", "<i8"),
                         ("footprint", "<i8"), ("out_offset", "<i8"), ("waste", "<f8"),
-                        ("reserved", "<i8")])
+                        ("row_base", "<i8")])
 SUMMARY_FIELDS = ("n_requests", "total_global", "sum_len_global", "n_max", "k_buckets",
                   "n_changes", "n_passes", "n_batches", "n_rejected", "n_pending",
                   "admitted_tokens", "padded_tokens", "packed_elems", "peak_footprint",
@@ -113,7 +113,7 @@ def load():
         "bs_assign": (C.c_int, [vp, vp, i64, P, vp, vp]),
         "bs_order": (C.c_int, [vp, vp, vp, i64, P, vp, vp, vp, vp, vp]),
         "bs_size": (C.c_int, [vp, vp, vp, vp, i64, P, vp, i32, vp, vp, vp, vp]),
-        "bs_pack": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P, vp, i64, i64, vp, vp, i64, vp, vp]),
+        "bs_pack": (C.c_int, [vp, vp, vp, vp, vp, P, vp, i64, i64, vp, vp, i64, vp, vp]),
         "bs_window_schedule": (C.c_int, [vp, C.POINTER(WindowIO), P, vp]),
         "bs_window_from_hist": (C.c_int, [vp, C.POINTER(WindowIO), P, vp]),
         "bs_monitor_bins": (C.c_int, [vp, vp, P, i32, vp, vp]),

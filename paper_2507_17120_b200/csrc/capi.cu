@@ -72,10 +72,12 @@ cudaError_t alloc(bs_ctx* ctx, T** p, size_t count) {
 }
 
 void free_all(bs_ctx* c) {
-  void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->bin_base, c->kinfo,
+  void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->bins_cnt,
+                  c->tile_tot, c->tile_slen, c->tile_carry, c->bmw, c->wp, c->kinfo,
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
                   c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
-                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->misc};
+                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->task_base,
+                  c->misc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -99,8 +101,8 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   *out = nullptr;
   if (max_n < 0 || max_n >= (int64_t)1 << 30)
     return fail(nullptr, BS_ERR_INVALID_ARG, "max_n must be in [0, 2^30)");
-  if (l_max_cap < 1 || l_max_cap > (1 << 24))
-    return fail(nullptr, BS_ERR_INVALID_ARG, "l_max_cap must be in [1, 2^24]");
+  if (l_max_cap < 1 || l_max_cap > (1 << 20))
+    return fail(nullptr, BS_ERR_INVALID_ARG, "l_max_cap must be in [1, 2^20]");
   if (max_classes < 1 || max_classes > BS_MAX_CLASSES)
     return fail(nullptr, BS_ERR_INVALID_ARG, "max_classes must be in [1, 8]");
   bs_ctx* ctx = new (std::nothrow) bs_ctx();
@@ -130,7 +132,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;
   const int64_t L = l_max_cap, C = max_classes, N = max_n;
-  ctx->max_tiles = (N + 4095) / 4096 + 1;
+  ctx->max_tiles = (N + 2047) / 2048 + 1;  // smallest K4 tile is 2048 keys
   const int64_t groups = (N + 31) / 32 + 1;
 #define A(ptr, cnt)                                                        \
   if ((e = alloc(ctx, &ctx->ptr, (size_t)(cnt))) != cudaSuccess) {         \
@@ -146,7 +148,13 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(seg_base, L * C);
   A(seg_off, L * C + 1);
   A(slot_lut, C * L);
-  A(bin_base, 4 * 256);
+  A(bins_cnt, 4 * 256);
+  const int64_t ntiles = (L + bsk::kTileX - 1) / bsk::kTileX;
+  A(tile_tot, ntiles * (C + 1));
+  A(tile_slen, ntiles);
+  A(tile_carry, (ntiles + 1) * (C + 1));
+  A(bmw, (L + 1 + 31) / 32);
+  A(wp, (L + 1 + 31) / 32);
   A(kinfo, 8);
   A(keysA, N); A(keysB, N); A(valsA, N); A(valsB, N);
   A(status, 4 * ctx->max_tiles * 256);
@@ -159,6 +167,8 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(listA, N + 1); A(listB, N + 1);
   A(node_batch, N + 1);
   A(node_j0, N + 1);
+  A(rowpos, N + 1);
+  A(task_base, N + 2);
   A(misc, 128);
   // co-resident blocks for the cooperative chain kernel (512 threads)
   int per_sm = 0;
@@ -278,15 +288,14 @@ int bs_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t*
   return BS_OK;
 }
 
-int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t* req_batch,
-            const int32_t* req_row, const int64_t* tok_off, const int32_t* tokens,
-            const bs_window_params* p, const bs_batch* batches, int64_t batch_begin,
-            int64_t batch_end, int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
-            bs_summary* summary, void* stream) {
+int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int64_t* tok_off,
+            const int32_t* tokens, const bs_window_params* p, const bs_batch* batches,
+            int64_t batch_begin, int64_t batch_end, int32_t* out_tokens, uint8_t* out_mask,
+            int64_t out_capacity, bs_summary* summary, void* stream) {
   if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
   int rc;
   if ((rc = check_params(ctx, p)) != BS_OK) return rc;
-  if (!len || !perm || !req_batch || !req_row || !tok_off || !tokens || !batches || !out_tokens)
+  if (!len || !perm || !tok_off || !tokens || !batches || !out_tokens)
     return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
   if (batch_end < 0 && !summary)
     return fail(ctx, BS_ERR_INVALID_ARG, "batch_end < 0 needs the summary of bs_size");
@@ -296,9 +305,9 @@ int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t*
   if (out_mask && (reinterpret_cast<uintptr_t>(out_mask) & 3))
     return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  BS_CUDA(bsk::launch_pack(ctx, len, perm, req_batch, req_row, tok_off, tokens, *p, batches,
-                           batch_begin, batch_end, INT32_MAX, out_tokens, out_mask, out_capacity,
-                           summary, static_cast<cudaStream_t>(stream)),
+  BS_CUDA(bsk::launch_pack(ctx, len, perm, tok_off, tokens, *p, batches, batch_begin, batch_end,
+                           INT32_MAX, out_tokens, out_mask, out_capacity, summary,
+                           static_cast<cudaStream_t>(stream)),
           "k_pack");
   return BS_OK;
 }
@@ -323,9 +332,9 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
       return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
     if (io->out_mask && (reinterpret_cast<uintptr_t>(io->out_mask) & 3))
       return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
-    BS_CUDA(bsk::launch_pack(ctx, io->len, io->perm, io->req_batch, io->req_row, io->tok_off,
-                             io->tokens, *p, io->batches, 0, -1, io->batches_cap, io->out_tokens,
-                             io->out_mask, io->out_capacity, io->summary, st),
+    BS_CUDA(bsk::launch_pack(ctx, io->len, io->perm, io->tok_off, io->tokens, *p, io->batches,
+                             0, -1, io->batches_cap, io->out_tokens, io->out_mask,
+                             io->out_capacity, io->summary, st),
             "k_pack");
   }
   bsk::prof_mark(ctx, 9, st);

@@ -66,7 +66,7 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
 // streaming 128-bit load (read once) / store (write once, evict first)
 __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;

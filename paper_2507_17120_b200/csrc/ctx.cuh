@@ -32,7 +32,12 @@ struct bs_ctx {
   int32_t* seg_base = nullptr;   // [l_cap*c_max] first radix slot of each segment
   int32_t* seg_off = nullptr;    // [l_cap*c_max+1] segment offsets of the last bs_boundaries
   uint32_t* slot_lut = nullptr;  // [c_max*l_cap] radix slot per (class, length)
-  uint32_t* bin_base = nullptr;  // [4][256] global digit offsets per radix pass
+  uint32_t* bins_cnt = nullptr;  // [4][256] per-pass radix digit counts (K2c -> K4)
+  uint32_t* tile_tot = nullptr;  // [ntiles][C+1] K2a tile totals (per class, then total)
+  uint64_t* tile_slen = nullptr; // [ntiles] K2a tile sum of x*h[x]
+  uint32_t* tile_carry = nullptr;// [ntiles+1][C+1] per-class tile carries (K2b)
+  uint32_t* bmw = nullptr;       // [W] final edge bitmask over [0, L]
+  uint32_t* wp = nullptr;        // [W] exclusive popc prefix of bmw
   int32_t* kinfo = nullptr;      // [8]: K, D, ...
   // K4
   uint32_t *keysA = nullptr, *keysB = nullptr, *valsA = nullptr, *valsB = nullptr;
@@ -47,6 +52,9 @@ struct bs_ctx {
   uint32_t* bmask = nullptr;     //   bit l: position 32g+l is admissible (len <= S)
   int32_t* Rg = nullptr;         // [max_n/32+1] exclusive prefix of bcnt
   int32_t* btot = nullptr;       // [chain_blocks] per-block partials of the Rg scan
+  int32_t* rowpos = nullptr;     // [max_n] admitted window row -> drain position (K6)
+  int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
+                                 //   <= kPiece tokens; exclusive prefix, K5f)
   int32_t* node_j0 = nullptr;    // [max_n + 1] first admissible position at/after each chain node
   int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
   uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
@@ -58,6 +66,9 @@ struct bs_ctx {
 };
 
 namespace bsk {
+
+constexpr int kTileX = 4096;  // lengths per K2a tile
+constexpr int kPiece = 2048;  // K6 work unit: at most this many tokens of one row
 
 // records boundary event `stage` (0..BS_STAGES) of the current profiled step
 inline void prof_mark(bs_ctx* ctx, int stage, cudaStream_t st) {
@@ -90,11 +101,10 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         bs_batch* batches, int32_t batches_cap, int32_t* req_batch,
                         int32_t* req_row, bs_summary* summary, cudaStream_t st);
 cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
-                        const int32_t* req_batch, const int32_t* req_row, const int64_t* tok_off,
-                        const int32_t* tokens, const bs_window_params& p, const bs_batch* batches,
-                        int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
-                        int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
-                        bs_summary* summary, cudaStream_t st);
+                        const int64_t* tok_off, const int32_t* tokens, const bs_window_params& p,
+                        const bs_batch* batches, int64_t batch_begin, int64_t batch_end,
+                        int32_t batches_cap, int32_t* out_tokens, uint8_t* out_mask,
+                        int64_t out_capacity, bs_summary* summary, cudaStream_t st);
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);

@@ -11,18 +11,22 @@
 // n_max = BatchController.current_n_max (batch_controller.py:93-104) evaluated
 // with CPython's float floor division, bit-exact.
 //
-// B200 mapping: a single 1024-thread CTA (the whole problem is O(L + K) and sits
-// in L2/shared memory).  Edges live as a bitmask over [0, L] in shared memory; a
-// pass is a block-scan compaction of the bitmask + one thread per bucket; the
-// change log is written in bucket order via a block scan, matching the
-// reference's left-to-right emission.  The same CTA then builds the per-length
-// bucket LUT (K3), the per-(class,length) radix slot table and the per-pass
-// digit offsets for K4 — derived from the histogram, so K4 needs no upsweep.
+// B200 mapping, three launches:
+//   K2a  k_prefix_tiles  one CTA per 4096 lengths: tile-local exclusive prefixes of
+//                        the total and per-class histograms, tile totals, sum(len)
+//   K2b  k_boundaries    one 1024-thread CTA: carries over the tiles, n_max, the
+//                        split/merge passes on an edge bitmask in shared memory
+//                        (block-scan compaction + one thread per bucket, change
+//                        log in bucket order), segment offsets / radix slot bases
+//   K2c  k_tables        grid over (class, length): bucket LUT (K3), radix slot per
+//                        (class, length) and the per-pass digit counts for K4,
+//                        derived from the histogram so K4 needs no upsweep.
 #include "ctx.cuh"
 
 namespace bsk {
 
 constexpr int kBT = 1024;
+constexpr int kEcap = 8192;   // edges kept in shared memory when l_max < kEcap
 
 // CPython _float_div_mod floor quotient (Objects/floatobject.c)
 __device__ double py_floordiv(double vx, double wx) {
@@ -41,13 +45,66 @@ __device__ double py_floordiv(double vx, double wx) {
   return fd;
 }
 
+// ---------------------------------------------------------------------------- K2a
+__global__ void __launch_bounds__(1024)
+    k_prefix_tiles(const uint32_t* __restrict__ hist_local, const uint32_t* __restrict__ hist_global,
+                   int32_t L, int32_t C, uint32_t* __restrict__ P, uint32_t* __restrict__ PcL,
+                   uint32_t* __restrict__ tile_tot, unsigned long long* __restrict__ tile_slen) {
+  __shared__ uint32_t s32[33];
+  __shared__ uint64_t s64[33];
+  const int t = blockIdx.x;
+  const int64_t x0 = (int64_t)t * kTileX + threadIdx.x * 4;
+  uint32_t h[4];
+  uint32_t sum = 0;
+  uint64_t sl = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t x = x0 + i;
+    h[i] = 0;
+    if (x < L)
+      for (int c = 0; c < C; ++c) h[i] += hist_global[(int64_t)c * L + x];
+    sum += h[i];
+    sl += (uint64_t)h[i] * (uint64_t)x;
+  }
+  uint32_t tot;
+  uint32_t run = block_excl_scan<uint32_t>(sum, s32, &tot);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (x0 + i < L) P[x0 + i] = run;
+    run += h[i];
+  }
+  uint64_t sltot;
+  block_excl_scan<uint64_t>(sl, s64, &sltot);
+  if (threadIdx.x == 0) {
+    tile_tot[(int64_t)t * (C + 1) + C] = tot;
+    tile_slen[t] = sltot;
+  }
+  for (int c = 0; c < C; ++c) {
+    uint32_t v[4], s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = (x0 + i < L) ? hist_local[(int64_t)c * L + x0 + i] : 0u;
+      s += v[i];
+    }
+    uint32_t tc;
+    uint32_t rc = block_excl_scan<uint32_t>(s, s32, &tc);
+    uint32_t* Pc = PcL + (int64_t)c * (L + 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (x0 + i < L) Pc[x0 + i] = rc;
+      rc += v[i];
+    }
+    if (threadIdx.x == 0) tile_tot[(int64_t)t * (C + 1) + c] = tc;
+  }
+}
+
+// ---------------------------------------------------------------------------- K2b
 struct BoundsShared {
   uint64_t s64[33];
   uint32_t s32[33];
   int32_t si[33];
   int64_t n_max;
   uint32_t total;
-  int32_t K;
   int32_t bad;
 };
 
@@ -72,55 +129,62 @@ __device__ int32_t compact_edges(const uint32_t* bm, int W, int32_t* E, BoundsSh
 }
 
 __global__ void __launch_bounds__(kBT, 1)
-    k_boundaries(const uint32_t* __restrict__ hist_local, const uint32_t* __restrict__ hist_global,
-                 bs_window_params p, int sort_bits, int sort_passes,
-                 const int32_t* __restrict__ init_edges, int32_t k_init,
+    k_boundaries(const uint32_t* __restrict__ P, const uint32_t* __restrict__ PcL,
+                 const uint32_t* __restrict__ tile_tot,
+                 const unsigned long long* __restrict__ tile_slen, int32_t ntiles,
+                 bs_window_params p, const int32_t* __restrict__ init_edges, int32_t k_init,
                  int32_t* __restrict__ edges_out, int32_t* __restrict__ changes_out,
-                 int32_t changes_cap, int32_t* __restrict__ seg_off_out, uint32_t* __restrict__ P,
-                 uint32_t* __restrict__ PcL, int32_t* __restrict__ E, int32_t* __restrict__ lut,
-                 int32_t* __restrict__ seg_base, uint32_t* __restrict__ slot_lut,
-                 uint32_t* __restrict__ bin_base, int32_t* __restrict__ kinfo, bs_summary* sum) {
+                 int32_t changes_cap, int32_t* __restrict__ seg_off_out,
+                 int32_t* __restrict__ gE, uint32_t* __restrict__ gbm, uint32_t* __restrict__ gwp,
+                 int32_t* __restrict__ seg_base, uint32_t* __restrict__ tile_carry,
+                 uint32_t* __restrict__ bins_cnt, int32_t* __restrict__ kinfo, bs_summary* sum) {
   extern __shared__ uint32_t dyn[];
   __shared__ BoundsShared sh;
   const int32_t L = p.l_max, C = p.n_classes;
   const int W = (L + 1 + 31) / 32;
-  uint32_t* bm = dyn;                 // [W] edge bitmask over [0, L]
-  uint32_t* wp = dyn + W;             // [W] exclusive popc prefix per word
-  uint32_t* sbins = dyn + 2 * W;      // [4][256] radix digit counts
+  uint32_t* bm = dyn;                                          // [W] edge bitmask over [0, L]
+  uint32_t* carry = dyn + W;                                   // [ntiles] total-hist carries
+  int32_t* sE = reinterpret_cast<int32_t*>(dyn + W + ntiles);  // [kEcap] edges (small L)
+  int32_t* E = (L + 1 <= kEcap) ? sE : gE;
   const int tid = threadIdx.x;
-  const int chunk = (L + kBT - 1) / kBT;
-  const int x0 = min(L, tid * chunk), x1 = min(L, x0 + chunk);
 
-  // ---- A. prefix sums: global total P, local per-class PcL, sum(len) ----------
+  // ---- A. carries over the K2a tiles, totals, n_max -------------------------------
   {
-    uint32_t s = 0;
-    uint64_t sl = 0;
-    for (int x = x0; x < x1; ++x) {
-      uint32_t h = 0;
-      for (int c = 0; c < C; ++c) h += hist_global[(int64_t)c * L + x];
-      s += h;
-      sl += (uint64_t)h * (uint64_t)x;
+    uint32_t tot_all = 0;
+    uint64_t sl_all = 0;
+    for (int base = 0; base < ntiles; base += kBT) {
+      const int t = base + tid;
+      const uint32_t v = t < ntiles ? tile_tot[(int64_t)t * (C + 1) + C] : 0u;
+      uint32_t tt;
+      const uint32_t o = block_excl_scan<uint32_t>(v, sh.s32, &tt);
+      if (t < ntiles) carry[t] = tot_all + o;
+      tot_all += tt;
+      const uint64_t s = t < ntiles ? tile_slen[t] : 0ull;
+      uint64_t ts;
+      block_excl_scan<uint64_t>(s, sh.s64, &ts);
+      sl_all += ts;
     }
-    uint32_t tot;
-    uint32_t run = block_excl_scan<uint32_t>(s, sh.s32, &tot);
-    for (int x = x0; x < x1; ++x) {
-      P[x] = run;
-      uint32_t h = 0;
-      for (int c = 0; c < C; ++c) h += hist_global[(int64_t)c * L + x];
-      run += h;
+    for (int c = 0; c < C; ++c) {  // per-class carries (segment counts in E.)
+      uint32_t run = 0;
+      for (int base = 0; base < ntiles; base += kBT) {
+        const int t = base + tid;
+        const uint32_t v = t < ntiles ? tile_tot[(int64_t)t * (C + 1) + c] : 0u;
+        uint32_t tt;
+        const uint32_t o = block_excl_scan<uint32_t>(v, sh.s32, &tt);
+        if (t < ntiles) tile_carry[(int64_t)t * (C + 1) + c] = run + o;
+        run += tt;
+      }
+      if (tid == 0) tile_carry[(int64_t)ntiles * (C + 1) + c] = run;  // class total = Pc(L)
     }
-    uint64_t sltot;
-    block_excl_scan<uint64_t>(sl, sh.s64, &sltot);
     if (tid == 0) {
-      P[L] = tot;
-      sh.total = tot;
+      sh.total = tot_all;
       int64_t nm;
       if (p.n_max > 0) {
         nm = p.n_max;
-      } else if (tot == 0) {
+      } else if (tot_all == 0) {
         nm = 1;  // idle system reports 1 (batch_controller.py:100-102)
       } else {
-        const double mean = __ddiv_rn((double)sltot, (double)tot);
+        const double mean = __ddiv_rn((double)sl_all, (double)tot_all);
         if (mean == 0.0) {
           latch_flags(sum, BS_FLAG_ZERO_MEAN);
           nm = 1;
@@ -132,25 +196,18 @@ __global__ void __launch_bounds__(kBT, 1)
         }
       }
       sh.n_max = nm;
-      sum->total_global = tot;
-      sum->sum_len_global = (int64_t)sltot;
+      sum->total_global = tot_all;
+      sum->sum_len_global = (int64_t)sl_all;
       sum->n_max = nm;
     }
-    for (int c = 0; c < C; ++c) {
-      uint32_t sc = 0;
-      for (int x = x0; x < x1; ++x) sc += hist_local[(int64_t)c * L + x];
-      uint32_t tc;
-      uint32_t rc = block_excl_scan<uint32_t>(sc, sh.s32, &tc);
-      uint32_t* Pc = PcL + (int64_t)c * (L + 1);
-      for (int x = x0; x < x1; ++x) {
-        Pc[x] = rc;
-        rc += hist_local[(int64_t)c * L + x];
-      }
-      if (tid == 0) Pc[L] = tc;
-    }
   }
+  for (int i = tid; i < 4 * 256; i += kBT) bins_cnt[i] = 0;  // K2c accumulates here
+  __syncthreads();
+  const uint32_t total = sh.total;
+  // P(x) = #{requests with length < x} from the tile-local prefix + tile carry
+  auto Pf = [&](int32_t x) -> uint32_t { return x >= L ? total : P[x] + carry[x / kTileX]; };
 
-  // ---- B. initial edges -------------------------------------------------------
+  // ---- B. initial edges -------------------------------------------------------------
   for (int w = tid; w < W; w += kBT) bm[w] = 0;
   if (tid == 0) sh.bad = 0;
   __syncthreads();
@@ -177,9 +234,8 @@ __global__ void __launch_bounds__(kBT, 1)
   }
   __syncthreads();
 
-  // ---- C. adjust_buckets passes --------------------------------------------------
+  // ---- C. adjust_buckets passes ------------------------------------------------------
   const int64_t n_max = sh.n_max;
-  const uint32_t total = sh.total;
   int64_t nch = 0;
   int32_t passes = 0;
   if (p.adjust) {
@@ -210,7 +266,8 @@ __global__ void __launch_bounds__(kBT, 1)
         int kind = 0, lo = 0, up = 0, mid = 0;
         if (k < K) {
           lo = E[k]; up = E[k + 1]; mid = (lo + up) >> 1;
-          const uint32_t c = P[up] - P[lo], s = P[mid] - P[lo];
+          const uint32_t plo = Pf(lo);
+          const uint32_t c = Pf(up) - plo, s = Pf(mid) - plo;
           if ((int64_t)c > n_max && (double)s > __dmul_rn(p.split_threshold, (double)c))
             kind = (mid <= lo) ? BS_CHANGE_SKIP : BS_CHANGE_SPLIT;
         }
@@ -235,9 +292,12 @@ __global__ void __launch_bounds__(kBT, 1)
     }
   }
   const int32_t K = compact_edges(bm, W, E, sh);
-  for (int i = tid; i <= K; i += kBT) edges_out[i] = E[i];
+  for (int i = tid; i <= K; i += kBT) {
+    edges_out[i] = E[i];
+    if (E != gE) gE[i] = E[i];
+  }
 
-  // ---- D. per-length bucket LUT (K3): bucket(x) = #{j >= 1 : e_j <= x} ------------
+  // ---- D. bitmask + per-word popc prefix for the LUT (K2c) ------------------------------
   {
     const int wc = (W + kBT - 1) / kBT;
     const int w0 = tid * wc, w1 = min(W, w0 + wc);
@@ -246,18 +306,13 @@ __global__ void __launch_bounds__(kBT, 1)
     int32_t tot;
     int32_t off = block_excl_scan<int32_t>(cnt, sh.si, &tot);
     for (int w = w0; w < w1; ++w) {
-      wp[w] = off;
+      gwp[w] = off;
+      gbm[w] = bm[w];
       off += __popc(bm[w]);
-    }
-    __syncthreads();
-    for (int x = tid; x < L; x += kBT) {
-      const int w = x >> 5, b = x & 31;
-      const uint32_t lowmask = b == 31 ? 0xffffffffu : ((2u << b) - 1u);
-      lut[x] = (int32_t)(wp[w] + __popc(bm[w] & lowmask)) - 1;
     }
   }
 
-  // ---- E. segments, radix slots, digit offsets (K4) --------------------------------
+  // ---- E. segment offsets (local per-class counts) and radix slot bases ---------------
   const int32_t S = K * C;
   int32_t run_cnt = 0, run_w = 0;
   for (int base = 0; base < S; base += kBT) {
@@ -267,53 +322,74 @@ __global__ void __launch_bounds__(kBT, 1)
       const int b = s / C, c = s % C;
       const int32_t lo = E[b], up = E[b + 1];
       const uint32_t* Pc = PcL + (int64_t)c * (L + 1);
-      cnt = (int32_t)(Pc[up] - Pc[lo]);
+      auto Pcf = [&](int32_t x) -> uint32_t {
+        const int64_t t = x >= L ? ntiles : x / kTileX;
+        return (x >= L ? 0u : Pc[x]) + tile_carry[t * (C + 1) + c];
+      };
+      cnt = (int32_t)(Pcf(up) - Pcf(lo));
       width = p.policy[c] == BS_POLICY_FCFS ? 1 : (up - lo);
     }
-    int32_t tc, tw;
-    const int32_t oc = block_excl_scan<int32_t>(cnt, sh.si, &tc);
+    int32_t tcn, tw;
+    const int32_t oc = block_excl_scan<int32_t>(cnt, sh.si, &tcn);
     const int32_t ow = block_excl_scan<int32_t>(width, sh.si, &tw);
     if (s < S) {
       seg_off_out[s] = run_cnt + oc;
       seg_base[s] = run_w + ow;
     }
-    run_cnt += tc;
+    run_cnt += tcn;
     run_w += tw;
   }
-  if (tid == 0) seg_off_out[S] = run_cnt;
-  for (int i = tid; i < 4 * 256; i += kBT) sbins[i] = 0;
-  __syncthreads();
-  const uint32_t dmask = (1u << sort_bits) - 1u;
-  for (int64_t idx = tid; idx < (int64_t)C * L; idx += kBT) {
-    const int c = (int)(idx / L), x = (int)(idx % L);
-    const int b = lut[x];
-    const int pol = p.policy[c];
-    uint32_t slot = (uint32_t)seg_base[b * C + c];
-    if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - E[b]);
-    else if (pol == BS_POLICY_LJF) slot += (uint32_t)(E[b + 1] - 1 - x);
-    slot_lut[idx] = slot;
-    const uint32_t h = hist_local[idx];
-    if (h)
-      for (int q = 0; q < sort_passes; ++q)
-        atomicAdd(&sbins[q * 256 + ((slot >> (q * sort_bits)) & dmask)], h);
-  }
-  __syncthreads();
-  for (int q = 0; q < sort_passes; ++q) {
-    const uint32_t v = tid < 256 ? sbins[q * 256 + tid] : 0u;
-    uint32_t t;
-    const uint32_t o = block_excl_scan<uint32_t>(v, sh.s32, &t);
-    if (tid < 256) bin_base[q * 256 + tid] = o;
-  }
   if (tid == 0) {
+    seg_off_out[S] = run_cnt;
     kinfo[0] = K;
     kinfo[1] = run_w;  // number of radix slots D
     kinfo[2] = S;
     sum->k_buckets = K;
     sum->n_changes = nch;
     sum->n_passes = passes;
-    sum->sort_passes = sort_passes;
     if (nch > changes_cap) latch_flags(sum, BS_FLAG_CHANGES_TRUNC);
   }
+}
+
+// ---------------------------------------------------------------------------- K2c
+__global__ void __launch_bounds__(256)
+    k_tables(const uint32_t* __restrict__ hist_local, bs_window_params p, int sort_bits,
+             int sort_passes, const int32_t* __restrict__ gE, const uint32_t* __restrict__ gbm,
+             const uint32_t* __restrict__ gwp, const int32_t* __restrict__ seg_base,
+             int32_t* __restrict__ lut, uint32_t* __restrict__ slot_lut,
+             uint32_t* __restrict__ bins_cnt) {
+  __shared__ uint32_t sbins[4 * 256];
+  const int32_t L = p.l_max, C = p.n_classes;
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) sbins[i] = 0;
+  __syncthreads();
+  const uint32_t dmask = (1u << sort_bits) - 1u;
+  const int64_t total = (int64_t)C * L;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / L), x = (int)(idx % L);
+    const int w = x >> 5, bt = x & 31;
+    const uint32_t lowmask = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
+    const int b = (int)(gwp[w] + __popc(gbm[w] & lowmask)) - 1;  // #{j >= 1 : e_j <= x}
+    if (c == 0) lut[x] = b;
+    const int pol = p.policy[c];
+    uint32_t slot = (uint32_t)seg_base[b * C + c];
+    if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - gE[b]);
+    else if (pol == BS_POLICY_LJF) slot += (uint32_t)(gE[b + 1] - 1 - x);
+    slot_lut[idx] = slot;
+    const uint32_t h = hist_local[idx];
+    const unsigned act = __ballot_sync(__activemask(), h != 0);
+    if (h) {
+      for (int q = 0; q < sort_passes; ++q) {
+        const uint32_t d = (slot >> (q * sort_bits)) & dmask;
+        const unsigned peers = __match_any_sync(act, d);
+        const uint32_t tot = __reduce_add_sync(peers, h);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sbins[q * 256 + d], tot);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < sort_passes * 256; i += blockDim.x)
+    if (sbins[i]) atomicAdd(&bins_cnt[i], sbins[i]);
 }
 
 SortPlan sort_plan(int32_t l_max, int32_t n_classes) {
@@ -331,19 +407,33 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
                               int32_t* edges_out, int32_t* changes_out, int32_t changes_cap,
                               int32_t* seg_off_out, bs_summary* summary, cudaStream_t st) {
   const SortPlan sp = sort_plan(p.l_max, p.n_classes);
-  const int W = (p.l_max + 1 + 31) / 32;
-  const size_t smem = sizeof(uint32_t) * (2 * (size_t)W + 4 * 256);
+  const int32_t L = p.l_max, C = p.n_classes;
+  const int ntiles = (L + kTileX - 1) / kTileX;
+  const uint32_t* hg = hist_global ? hist_global : hist_local;
+  k_prefix_tiles<<<ntiles, 1024, 0, st>>>(hist_local, hg, L, C, ctx->P, ctx->PcL, ctx->tile_tot,
+                                          reinterpret_cast<unsigned long long*>(ctx->tile_slen));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int W = (L + 1 + 31) / 32;
+  const size_t smem = sizeof(uint32_t) * ((size_t)W + ntiles + (L + 1 <= kEcap ? kEcap : 0));
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaFuncSetAttribute(k_boundaries, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  k_boundaries<<<1, kBT, smem, st>>>(hist_local, hist_global ? hist_global : hist_local, p, sp.bits,
-                                     sp.passes, init_edges, k_init, edges_out, changes_out,
-                                     changes_cap, seg_off_out, ctx->P, ctx->PcL, ctx->E, ctx->lut,
-                                     ctx->seg_base, ctx->slot_lut, ctx->bin_base, ctx->kinfo,
+  k_boundaries<<<1, kBT, smem, st>>>(ctx->P, ctx->PcL, ctx->tile_tot,
+                                     reinterpret_cast<const unsigned long long*>(ctx->tile_slen),
+                                     ntiles, p, init_edges, k_init, edges_out, changes_out,
+                                     changes_cap, seg_off_out, ctx->E, ctx->bmw, ctx->wp,
+                                     ctx->seg_base, ctx->tile_carry, ctx->bins_cnt, ctx->kinfo,
                                      summary);
-  ++ctx->launches;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int64_t cells = (int64_t)C * L;
+  const unsigned tb = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((cells + 1023) / 1024, 4LL * ctx->num_sms));
+  k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
+                               ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt);
+  ctx->launches += 3;
   return cudaGetLastError();
 }
 

@@ -26,8 +26,9 @@
 //                  from the segment starts emitting every batch start in
 //                  emission order — O(N log B) work, O(log B) depth.
 //   K5d  describe  one warp per batch: n / sum / max / min from group summaries
-//   K5e  outcome   one warp per 32 positions: batch id / row / rejected / pending
-//   K5f  offsets   one CTA: packed-buffer offsets (scan of n*pitch) + totals
+//   K5f  offsets   one CTA: packed-buffer offsets (scan of n*pitch), row bases, totals
+//   K5e  outcome   one warp per 32 positions: batch id / row / rejected / pending,
+//                  and the row map (window row -> drain position) used by K6
 #include <cooperative_groups.h>
 
 #include "ctx.cuh"
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(256)
         fl |= BS_FLAG_NONPOS_LEN;
       }
       B.waste = wr;
-      B.reserved = 0;
+      B.row_base = 0;  // K5f
       batches[b] = B;
     }
   }
@@ -485,8 +486,9 @@ __global__ void __launch_bounds__(256)
                    const int32_t* __restrict__ Rg, const int32_t* __restrict__ listA,
                    const int32_t* __restrict__ listB, const int32_t* __restrict__ node_batch,
                    const int32_t* __restrict__ node_j0, const int32_t* __restrict__ misc,
+                   const bs_batch* __restrict__ batches, int32_t batches_cap,
                    int32_t* __restrict__ req_batch, int32_t* __restrict__ req_row,
-                   bs_summary* sum) {
+                   int32_t* __restrict__ rowpos, bs_summary* sum) {
   const int M = misc[64];
   const int32_t* list = misc[68] ? listB : listA;
   const int lane = threadIdx.x & 31;
@@ -516,6 +518,7 @@ __global__ void __launch_bounds__(256)
         const int32_t Rc = Rg[gc] + __popc(bmask[gc] & ((1u << (c & 31)) - 1u));
         req_batch[r] = b;
         req_row[r] = Rj - Rc;
+        if (b < batches_cap) rowpos[batches[b].row_base + (Rj - Rc)] = (int32_t)j;  // K6 row map
       } else {
         req_batch[r] = BS_REQ_REJECTED;
         req_row[r] = -1;
@@ -539,18 +542,21 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------- K5f
 __global__ void __launch_bounds__(1024)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
-                   const int32_t* __restrict__ misc, bs_summary* sum) {
+                   const int32_t* __restrict__ misc, int64_t* __restrict__ task_base,
+                   bs_summary* sum) {
   __shared__ int64_t s_l[33];
   __shared__ double s_d[32];
   __shared__ int64_t s_a[32], s_p[32], s_pk[32];
   const int nb = min(misc[66], batches_cap);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  int64_t run = 0, adm = 0, pad = 0, peak = 0;
+  int64_t run = 0, rrun = 0, trun = 0, adm = 0, pad = 0, peak = 0;
   double ws = 0.0;
   for (int base = 0; base < nb; base += blockDim.x) {
     const int i = base + tid;
-    int64_t v = 0;
+    int64_t v = 0, rows = 0, tasks = 0;
     if (i < nb) {
+      rows = batches[i].n;
+      tasks = rows * ((batches[i].pitch + kPiece - 1) / kPiece);
       const bs_batch& B = batches[i];
       v = (int64_t)B.n * B.pitch;
       adm += B.token_sum;
@@ -558,11 +564,20 @@ __global__ void __launch_bounds__(1024)
       peak = B.footprint > peak ? B.footprint : peak;
       ws += B.waste;
     }
-    int64_t tot;
+    int64_t tot, rtot, ttot;
     const int64_t off = block_excl_scan<int64_t>(v, s_l, &tot);
-    if (i < nb) batches[i].out_offset = run + off;
+    const int64_t roff = block_excl_scan<int64_t>(rows, s_l, &rtot);
+    const int64_t toff = block_excl_scan<int64_t>(tasks, s_l, &ttot);
+    if (i < nb) {
+      batches[i].out_offset = run + off;
+      batches[i].row_base = rrun + roff;
+      task_base[i] = trun + toff;
+    }
     run += tot;
+    rrun += rtot;
+    trun += ttot;
   }
+  if (tid == 0) task_base[nb] = trun;
   adm = warp_sum(adm);
   pad = warp_sum(pad);
   peak = warp_max(peak);
@@ -658,12 +673,12 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                            ctx->listB, ctx->node_batch, misc, batches,
                                            batches_cap, summary);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k_size_outcome<<<wblocks, 256, 0, st>>>(a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB,
-                                          ctx->node_batch, ctx->node_j0, misc, req_batch,
-                                          req_row, summary);
+  k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 7, st);
-  k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, summary);
+  k_size_outcome<<<wblocks, 256, 0, st>>>(a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB,
+                                          ctx->node_batch, ctx->node_j0, misc, batches,
+                                          batches_cap, req_batch, req_row, ctx->rowpos, summary);
   ctx->launches += 6;
   return cudaGetLastError();
 }

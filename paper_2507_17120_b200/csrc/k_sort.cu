@@ -23,8 +23,10 @@ namespace bsk {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTile = kSortThreads * kItems;  // 4096
+// items per thread: 8 (2048-key tiles) for windows < 4M keys (more CTAs in flight),
+// 16 (4096-key tiles) above (fewer look-back steps)
+constexpr int kItemsSmall = 8;
+constexpr int kItemsLarge = 16;
 
 __global__ void k_assign(const int32_t* __restrict__ len, int64_t n, int32_t L, int32_t truncate,
                          const int32_t* __restrict__ lut, int32_t* __restrict__ bucket_out,
@@ -36,15 +38,16 @@ __global__ void k_assign(const int32_t* __restrict__ len, int64_t n, int32_t L, 
   latch_flags(sum, fl);
 }
 
-template <bool kFirst, bool kLast>
+template <bool kFirst, bool kLast, int kItems>
 __global__ void __launch_bounds__(kSortThreads)
     k_sort_pass(const int32_t* __restrict__ len, const uint8_t* __restrict__ cls,
                 const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t n,
                 int32_t L, int32_t C, int32_t truncate, const uint32_t* __restrict__ slot_lut,
                 const int32_t* __restrict__ lut, int32_t* __restrict__ bucket_out, int shift,
-                int bits, const uint32_t* __restrict__ bin_base, uint32_t* __restrict__ status,
+                int bits, const uint32_t* __restrict__ bins_cnt, uint32_t* __restrict__ status,
                 uint32_t* __restrict__ tile_ctr) {
+  constexpr int kTile = kSortThreads * kItems;
   __shared__ uint32_t s_cnt[kSortWarps][256];
   __shared__ uint32_t s_keys[kTile];
   __shared__ uint32_t s_vals[kTile];
@@ -52,11 +55,17 @@ __global__ void __launch_bounds__(kSortThreads)
   __shared__ int64_t s_gbase[256];
   __shared__ uint32_t s_scan[33];
   __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_binbase[256];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t nb = 1u << bits, dmask = nb - 1u;
   if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
   for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&s_cnt[0][0])[i] = 0;
+  {  // global digit offsets of this pass: exclusive scan of the K2c digit counts
+    uint32_t t_;
+    const uint32_t o = block_excl_scan<uint32_t>(tid < (int)nb ? bins_cnt[tid] : 0u, s_scan, &t_);
+    s_binbase[tid] = o;
+  }
   __syncthreads();
   const uint32_t tile = s_tile;
   const int64_t tbase = (int64_t)tile * kTile;
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(kSortThreads)
       }
       st_relaxed(my, kStatPrefix | (excl + tile_cnt));
     }
-    s_gbase[tid] = (int64_t)bin_base[tid] + excl - dstart;
+    s_gbase[tid] = (int64_t)s_binbase[tid] + excl - dstart;
   }
   __syncthreads();
   // ---- local sort into shared memory -----------------------------------------------
@@ -168,11 +177,11 @@ cudaError_t launch_assign(bs_ctx* ctx, const int32_t* len, int64_t n, const bs_w
   return cudaGetLastError();
 }
 
-cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
-                         const bs_window_params& p, int32_t* perm_out, int32_t* bucket_out,
-                         bs_summary* summary, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  const SortPlan sp = sort_plan(p.l_max, p.n_classes);
+template <int kItems>
+static cudaError_t order_passes(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
+                                const bs_window_params& p, int32_t* perm_out,
+                                int32_t* bucket_out, const SortPlan& sp, cudaStream_t st) {
+  constexpr int kTile = kSortThreads * kItems;
   const int64_t tiles = (n + kTile - 1) / kTile;
   const size_t stat_words = (size_t)tiles * 256;
   cudaError_t e = cudaMemsetAsync(ctx->status, 0, sizeof(uint32_t) * stat_words * sp.passes, st);
@@ -187,34 +196,37 @@ cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, in
     const bool first = q == 0, last = q == sp.passes - 1;
     uint32_t* kout = kbuf[q & 1];
     uint32_t* vout = last ? reinterpret_cast<uint32_t*>(perm_out) : vbuf[q & 1];
-    const uint32_t* bb = ctx->bin_base + q * 256;
+    const uint32_t* bb = ctx->bins_cnt + q * 256;
     uint32_t* stt = ctx->status + stat_words * q;
     uint32_t* tc = ctx->tile_ctr + q;
     const int shift = q * sp.bits;
-    if (first && last)
-      k_sort_pass<true, true><<<(unsigned)tiles, kSortThreads, 0, st>>>(
-          len, cls, kin, vin, kout, vout, n, p.l_max, p.n_classes, p.truncate, ctx->slot_lut,
-          ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc);
-    else if (first)
-      k_sort_pass<true, false><<<(unsigned)tiles, kSortThreads, 0, st>>>(
-          len, cls, kin, vin, kout, vout, n, p.l_max, p.n_classes, p.truncate, ctx->slot_lut,
-          ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc);
-    else if (last)
-      k_sort_pass<false, true><<<(unsigned)tiles, kSortThreads, 0, st>>>(
-          len, cls, kin, vin, kout, vout, n, p.l_max, p.n_classes, p.truncate, ctx->slot_lut,
-          ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc);
-    else
-      k_sort_pass<false, false><<<(unsigned)tiles, kSortThreads, 0, st>>>(
-          len, cls, kin, vin, kout, vout, n, p.l_max, p.n_classes, p.truncate, ctx->slot_lut,
-          ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc);
+#define BS_SORT_LAUNCH(F, LST)                                                                \
+  k_sort_pass<F, LST, kItems><<<(unsigned)tiles, kSortThreads, 0, st>>>(                      \
+      len, cls, kin, vin, kout, vout, n, p.l_max, p.n_classes, p.truncate, ctx->slot_lut,     \
+      ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc)
+    if (first && last) BS_SORT_LAUNCH(true, true);
+    else if (first) BS_SORT_LAUNCH(true, false);
+    else if (last) BS_SORT_LAUNCH(false, true);
+    else BS_SORT_LAUNCH(false, false);
+#undef BS_SORT_LAUNCH
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ++ctx->launches;
     kin = kout;
     vin = vout;
   }
-  (void)summary;
   return cudaSuccess;
+}
+
+cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
+                         const bs_window_params& p, int32_t* perm_out, int32_t* bucket_out,
+                         bs_summary* summary, cudaStream_t st) {
+  (void)summary;
+  if (n == 0) return cudaSuccess;
+  const SortPlan sp = sort_plan(p.l_max, p.n_classes);
+  if (n < (int64_t)4 << 20)
+    return order_passes<kItemsSmall>(ctx, len, cls, n, p, perm_out, bucket_out, sp, st);
+  return order_passes<kItemsLarge>(ctx, len, cls, n, p, perm_out, bucket_out, sp, st);
 }
 
 }  // namespace bsk

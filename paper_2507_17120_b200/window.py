@@ -338,8 +338,7 @@ class WindowScheduler:
                 # first packed window: size the reusable output buffer from the plan
                 need = int(self.summary[96:104].cpu().view(torch.int64).item())  # packed_elems
                 self._ensure_pack(max(need, 64))
-                N.check(lib.bs_pack(self.ctx.ptr, _ptr(lens), _ptr(self.perm),
-                                    _ptr(self.req_batch), _ptr(self.req_row), _ptr(tok_off),
+                N.check(lib.bs_pack(self.ctx.ptr, _ptr(lens), _ptr(self.perm), _ptr(tok_off),
                                     _ptr(tokens), C.byref(p), _ptr(self.batches_raw), 0, -1,
                                     _ptr(self.out_tokens), _ptr(self.out_mask),
                                     self.pack_capacity, _ptr(self.summary), st), self.ctx.ptr)

@@ -100,7 +100,7 @@ def _compare_with_oracle(spec, lens, cls, pack=True, sample_rows=None):
     assert np.array_equal(h["seg_off"], o.seg_off)
     b = h["batches"]
     for f in ("segment", "start", "end", "n", "max_input_len", "pitch", "token_sum", "footprint",
-              "out_offset"):
+              "out_offset", "row_base"):
         assert np.array_equal(b[f], o.batches[f]), f
     if pack:
         m = int(h["summary"]["packed_elems"])
