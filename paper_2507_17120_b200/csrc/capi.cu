@@ -2,6 +2,7 @@
 // scratch layout, argument validation and stage orchestration.  No C++
 // exception crosses this boundary; every entry returns a BS_* status.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -128,6 +129,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
     return rc;
   }
   ctx->num_sms = prop.multiProcessorCount;
+  if (const char* v = getenv("BS_PACK_VARIANT")) ctx->pack_variant = atoi(v);
   int r = 1;
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;

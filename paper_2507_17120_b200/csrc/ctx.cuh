@@ -17,6 +17,7 @@ struct bs_ctx {
   int chain_blocks = 0;     // co-resident blocks of the cooperative chain kernel
   int64_t scratch_bytes = 0;
   int64_t launches = 0;     // kernels launched through this ctx
+  int pack_variant = 0;     // K6 tuning variant (env BS_PACK_VARIANT)
   std::string err;
   // stage profiler: ring of (BS_STAGES+1) events per recorded step
   std::vector<cudaEvent_t> prof_events;

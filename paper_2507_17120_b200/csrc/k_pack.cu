@@ -22,14 +22,15 @@
 namespace bsk {
 
 constexpr int kPackThreads = 256;
-constexpr int kPackU = 4;  // vectors per lane per step (128 vectors = 512 tokens per warp)
 
 __device__ __forceinline__ uint32_t mask_word(int32_t k) {
   // bytes 0..3 = 1 for the first k (0..4) entries
   return k >= 4 ? 0x01010101u : (k <= 0 ? 0u : (0x01010101u >> (8 * (4 - k))));
 }
 
-// copy columns [4*vb, 4*ve) of one row (x real tokens, pad beyond)
+// copy columns [4*vb, 4*ve) of one row (x real tokens, pad beyond); kU vectors of
+// 16 B in flight per lane
+template <int kPackU>
 __device__ __forceinline__ void copy_row_range(const int32_t* src, int32_t* dst, uint8_t* mdst,
                                                int32_t x, int32_t vb, int32_t ve, int lane,
                                                int32_t pad_id) {
@@ -69,7 +70,8 @@ __device__ __forceinline__ void copy_row_range(const int32_t* src, int32_t* dst,
   }
 }
 
-__global__ void __launch_bounds__(kPackThreads)
+template <int kPackU, int kMinBlocks>
+__global__ void __launch_bounds__(kPackThreads, kMinBlocks)
     k_pack(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
            const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
            const int64_t* __restrict__ tok_off, const int32_t* __restrict__ tokens, int32_t L,
@@ -135,10 +137,235 @@ __global__ void __launch_bounds__(kPackThreads)
       const int32_t x_i = __shfl_sync(FULL, x, i);
       const int32_t vb_i = __shfl_sync(FULL, vb, i);
       const int32_t ve_i = __shfl_sync(FULL, ve, i);
-      copy_row_range(s_i, d_i, m_i, x_i, vb_i, ve_i, lane, pad_id);
+      copy_row_range<kPackU>(s_i, d_i, m_i, x_i, vb_i, ve_i, lane, pad_id);
     }
   }
   if (fl) latch_flags(sum, fl);
+}
+
+// ---------------------------------------------------------------------------------
+// TMA variant: the token bytes of each piece are fetched by one elected lane with a
+// bulk asynchronous copy (cp.async.bulk global -> shared, completion counted on an
+// mbarrier), two 8 KB staging slots per warp, so every warp keeps up to 16 KB of
+// reads in flight without spending registers; the lanes then stream the slot out
+// with 128-bit stores (+ padding and the u32 mask words).
+constexpr int kTmaWarps = 4;
+constexpr int kTmaSlots = 2;
+constexpr int kTmaSlotBytes = kPiece * 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct PieceMeta {
+  const int32_t* src;
+  int32_t* dst;
+  uint8_t* mdst;
+  int32_t x, vb, ve;
+};
+
+__global__ void __launch_bounds__(kTmaWarps * 32)
+    k_pack_tma(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
+               const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
+               const int64_t* __restrict__ tok_off, const int32_t* __restrict__ tokens, int32_t L,
+               int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
+               int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
+               int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
+               bs_summary* sum) {
+  extern __shared__ __align__(128) uint8_t tma_smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaWarps][kTmaSlots];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int4* slots = reinterpret_cast<int4*>(tma_smem + (size_t)wib * kTmaSlots * kTmaSlotBytes);
+  if (lane == 0) {
+    for (int k = 0; k < kTmaSlots; ++k) mbar_init(&bars[wib][k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  int64_t b_end = b_end_arg;
+  if (b_end < 0) {
+    b_end = sum_in->n_batches;
+    if (b_end > batches_cap) b_end = batches_cap;
+  }
+  if (b_begin >= b_end) return;
+  const int64_t base_off = batches[b_begin].out_offset;
+  const bs_batch last = batches[b_end - 1];
+  if (last.out_offset + (int64_t)last.n * last.pitch - base_off > out_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
+    return;
+  }
+  const int64_t t0 = task_base[b_begin], t1 = task_base[b_end];
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int4 pad4 = make_int4(pad_id, pad_id, pad_id, pad_id);
+  uint32_t use[kTmaSlots] = {0, 0};
+  unsigned fl = 0;
+  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
+    const int64_t t = gt + lane;
+    PieceMeta my{nullptr, nullptr, nullptr, 0, 0, 0};
+    if (t < t1) {
+      int64_t lo = b_begin, hi = b_end;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (task_base[mid] <= t) lo = mid; else hi = mid;
+      }
+      const bs_batch B = batches[lo];
+      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int64_t local = t - task_base[lo];
+      const int64_t row = local / pieces;
+      const int32_t piece = (int32_t)(local - row * pieces);
+      const int64_t rstart = (B.out_offset - base_off) + row * (int64_t)B.pitch;
+      const int32_t r = perm[rowpos[B.row_base + row]];
+      my.x = eff_len(len[r], L, truncate, fl);
+      my.src = tokens + tok_off[r];
+      my.dst = out_tokens + rstart;
+      my.mdst = out_mask ? out_mask + rstart : nullptr;
+      my.vb = piece * (kPiece / 4);
+      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      my.ve = c1 >> 2;
+    }
+    const int nv = __popc(__ballot_sync(FULL, t < t1));
+    auto get = [&](int i) {
+      PieceMeta m;
+      m.src = reinterpret_cast<const int32_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.src), i));
+      m.dst = reinterpret_cast<int32_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.dst), i));
+      m.mdst = reinterpret_cast<uint8_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.mdst), i));
+      m.x = __shfl_sync(FULL, my.x, i);
+      m.vb = __shfl_sync(FULL, my.vb, i);
+      m.ve = __shfl_sync(FULL, my.ve, i);
+      return m;
+    };
+    // bytes of whole 16-byte vectors of real tokens inside the piece
+    auto bulk_vecs = [](const PieceMeta& m) -> int32_t {
+      const int32_t full = m.x >> 2;
+      const int32_t hi = full < m.ve ? full : m.ve;
+      return hi > m.vb ? hi - m.vb : 0;
+    };
+    auto aligned = [](const PieceMeta& m) {
+      return ((reinterpret_cast<uintptr_t>(m.src) | reinterpret_cast<uintptr_t>(m.dst)) & 15) == 0;
+    };
+    auto issue = [&](const PieceMeta& m, int slot) {
+      const int32_t nvec = aligned(m) ? bulk_vecs(m) : 0;
+      if (nvec > 0 && lane == 0) {
+        mbar_expect_tx(&bars[wib][slot], (uint32_t)nvec * 16u);
+        tma_load_1d(slots + slot * (kTmaSlotBytes / 16), m.src + 4 * m.vb, (uint32_t)nvec * 16u,
+                    &bars[wib][slot]);
+      }
+    };
+    if (nv == 0) continue;
+    PieceMeta cur = get(0);
+    issue(cur, 0);
+    for (int i = 0; i < nv; ++i) {
+      const int slot = i & 1;
+      PieceMeta nxt{nullptr, nullptr, nullptr, 0, 0, 0};
+      if (i + 1 < nv) {
+        nxt = get(i + 1);
+        issue(nxt, slot ^ 1);
+      }
+      if (aligned(cur)) {
+        const int32_t nvec = bulk_vecs(cur);
+        if (nvec > 0) {
+          mbar_wait(&bars[wib][slot], use[slot] & 1u);
+          ++use[slot];
+        }
+        const int32_t full = cur.x >> 2, rem = cur.x & 3;
+        const int4* sl = slots + slot * (kTmaSlotBytes / 16);
+        int4* d4 = reinterpret_cast<int4*>(cur.dst);
+        uint32_t* m4 = reinterpret_cast<uint32_t*>(cur.mdst);
+        for (int32_t v = cur.vb + lane; v < cur.ve; v += 32) {
+          int4 val = v < full ? sl[v - cur.vb] : pad4;
+          if (v == full && rem) {
+            val.x = cur.src[4 * v];
+            if (rem > 1) val.y = cur.src[4 * v + 1];
+            if (rem > 2) val.z = cur.src[4 * v + 2];
+          }
+          st_stream_v4(d4 + v, val);
+          if (m4) st_stream_u32(m4 + v, mask_word(cur.x - 4 * v));
+        }
+      } else {
+        for (int32_t tt = 4 * cur.vb + lane; tt < 4 * cur.ve; tt += 32) {
+          cur.dst[tt] = tt < cur.x ? cur.src[tt] : pad_id;
+          if (cur.mdst) cur.mdst[tt] = tt < cur.x ? 1 : 0;
+        }
+      }
+      __syncwarp();  // slot fully read before it is refilled
+      cur = nxt;
+    }
+  }
+  if (fl) latch_flags(sum, fl);
+}
+
+static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                                   const int64_t* tok_off, const int32_t* tokens,
+                                   const bs_window_params& p, const bs_batch* batches,
+                                   int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                                   int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                                   bs_summary* summary, cudaStream_t st) {
+  const size_t smem = (size_t)kTmaWarps * kTmaSlots * kTmaSlotBytes;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k_pack_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_tma, kTmaWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
+  k_pack_tma<<<blocks, kTmaWarps * 32, smem, st>>>(
+      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
+      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
+      summary);
+  ++ctx->launches;
+  return cudaGetLastError();
+}
+
+template <int kU, int kMinB>
+static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                                 const int64_t* tok_off, const int32_t* tokens,
+                                 const bs_window_params& p, const bs_batch* batches,
+                                 int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                                 int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                                 bs_summary* summary, cudaStream_t st) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack<kU, kMinB>, kPackThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
+  k_pack<kU, kMinB><<<blocks, kPackThreads, 0, st>>>(
+      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
+      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
+      summary);
+  ++ctx->launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
@@ -146,19 +373,25 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const bs_batch* batches, int64_t batch_begin, int64_t batch_end,
                         int32_t batches_cap, int32_t* out_tokens, uint8_t* out_mask,
                         int64_t out_capacity, bs_summary* summary, cudaStream_t st) {
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack, kPackThreads, 0);
-    if (per_sm < 1) per_sm = 1;
+#define BS_PACK_V(U, MB)                                                                  \
+  return launch_pack_v<U, MB>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,   \
+                              batch_end, batches_cap, out_tokens, out_mask, out_capacity, \
+                              summary, st)
+  int v = ctx->pack_variant;
+  // default: the TMA staging variant for long-context windows (rows of many KB),
+  // 128-bit register copies with 6 CTAs/SM otherwise (measured on B200, C2 / C4)
+  if (v == 0) v = p.l_max > 16384 ? 5 : 1;
+  switch (v) {  // tuning hook (BS_PACK_VARIANT)
+    case 1: BS_PACK_V(4, 6);
+    case 2: BS_PACK_V(8, 4);
+    case 3: BS_PACK_V(8, 3);
+    case 4: BS_PACK_V(2, 8);
+    case 5:
+      return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
+                             batches_cap, out_tokens, out_mask, out_capacity, summary, st);
+    default: BS_PACK_V(4, 6);
   }
-  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
-  k_pack<<<blocks, kPackThreads, 0, st>>>(len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens,
-                                          p.l_max,
-                                          p.truncate, p.pad_id, batches, batch_begin, batch_end,
-                                          summary, batches_cap, out_tokens, out_mask, out_capacity,
-                                          summary);
-  ++ctx->launches;
-  return cudaGetLastError();
+#undef BS_PACK_V
 }
 
 }  // namespace bsk
