@@ -443,3 +443,8 @@ int bs_profile_read(bs_ctx* ctx, float* stage_ms, int32_t* steps_out) {
 int64_t bs_launch_count(const bs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 }  // extern "C"
+
+static_assert(sizeof(bs_window_params) == 104, "bs_window_params layout (Python binding)");
+static_assert(sizeof(bs_batch) == 64, "bs_batch layout");
+static_assert(sizeof(bs_summary) == 256, "bs_summary layout");
+static_assert(sizeof(bs_window_io) == 176, "bs_window_io layout");

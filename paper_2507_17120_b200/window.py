@@ -26,6 +26,7 @@ import torch
 from . import _native as N
 from .errors import ConfigError
 from .memory_model import GpuConfig, ModelConfig, safe_memory
+from .sharding import allreduce_histogram
 from .types import (CHANGE_KIND, DispatchPolicy, MemoryAccounting, StructuralChange,
                     accounting_code, policy_code)
 
@@ -296,11 +297,7 @@ class WindowScheduler:
         io.summary = _ptr(self.summary)
         return io
 
-    def schedule(self, lengths, classes, tok_off=None, tokens=None, *, sync: bool = True,
-                 check: bool = True) -> WindowResult:
-        """Schedule one window.  `lengths` int32[n] and `classes` uint8[n] in arrival
-        order (device tensors, or host arrays that are copied); optional CSR token
-        store (`tok_off` int64[n+1], `tokens` int32[...]) enables packing."""
+    def _inputs(self, lengths, classes):
         dev = self.device
         lens = _as_device(lengths, torch.int32, dev)
         cls = _as_device(classes, torch.uint8, dev)
@@ -309,6 +306,33 @@ class WindowScheduler:
             raise ValueError("lengths and classes differ in length")
         if n > self.max_requests:
             raise ValueError(f"window of {n} exceeds max_requests={self.max_requests}")
+        return lens, cls, n
+
+    def histogram(self, lengths, classes, *, sync: bool = True):
+        """K1 only: the window's per-(class, length) counts as an int32 [C, L] tensor
+        (a copy; uint32 bit patterns).  Used to build a global histogram by hand."""
+        lens, cls, n = self._inputs(lengths, classes)
+        with torch.cuda.device(self.device):
+            N.check(N.load().bs_histogram(self.ctx.ptr, _ptr(lens), _ptr(cls), n,
+                                          C.byref(self._params), _ptr(self.hist),
+                                          _ptr(self.summary), _stream_handle(self.device)),
+                    self.ctx.ptr)
+        out = self.hist.view(self.cfg.n_classes, self.cfg.max_seq_len).clone()
+        if sync:
+            torch.cuda.current_stream(self.device).synchronize()
+        return out
+
+    def schedule(self, lengths, classes, tok_off=None, tokens=None, *, sync: bool = True,
+                 check: bool = True, hist_reduce=None) -> WindowResult:
+        """Schedule one window.  `lengths` int32[n] and `classes` uint8[n] in arrival
+        order (device tensors, or host arrays that are copied); optional CSR token
+        store (`tok_off` int64[n+1], `tokens` int32[...]) enables packing.
+
+        Sharded windows: with a process group (constructor) the local histogram is
+        all-reduced over it (C1); `hist_reduce(hist)` may instead transform the
+        local histogram in place into the global one (e.g. in single-GPU tests)."""
+        dev = self.device
+        lens, cls, n = self._inputs(lengths, classes)
         pack = tok_off is not None and tokens is not None
         if pack:
             tok_off = _as_device(tok_off, torch.int64, dev)
@@ -321,17 +345,22 @@ class WindowScheduler:
         if pack and n == 0:
             self._ensure_pack(64)  # nothing to pack; keep the result shape uniform
         two_phase = pack and self.pack_capacity == 0
+        sharded = self.process_group is not None or hist_reduce is not None
+        if sharded and self.hist_global is None:
+            self.hist_global = torch.zeros_like(self.hist)
         io = self._io(lens, cls, n, tok_off, tokens, pack and not two_phase)
         with torch.cuda.device(dev):
-            if self.process_group is None:
+            if not sharded:
                 N.check(lib.bs_window_schedule(self.ctx.ptr, C.byref(io), C.byref(p), st), self.ctx.ptr)
             else:
-                import torch.distributed as dist
                 N.check(lib.bs_histogram(self.ctx.ptr, _ptr(lens), _ptr(cls), n, C.byref(p),
                                          _ptr(self.hist), _ptr(self.summary), st), self.ctx.ptr)
                 self.hist_global.copy_(self.hist)
-                # C1: sum of per-rank length histograms over NCCL (NVLink/NVSwitch)
-                dist.all_reduce(self.hist_global, op=dist.ReduceOp.SUM, group=self.process_group)
+                if hist_reduce is not None:
+                    hist_reduce(self.hist_global)
+                else:  # C1: sum of per-rank histograms over NCCL (NVLink / NVSwitch)
+                    allreduce_histogram(self.hist_global, self.process_group)
+                io.hist_global = _ptr(self.hist_global)
                 N.check(lib.bs_window_from_hist(self.ctx.ptr, C.byref(io), C.byref(p), st),
                         self.ctx.ptr)
             if two_phase:

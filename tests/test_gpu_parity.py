@@ -223,3 +223,52 @@ def test_monitor_bins_match_numpy_histogram():
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_window_on_one_gpu(world):
+    """C1 logic on one GPU: per-shard K1, summed histogram (what the NCCL all-reduce
+    produces), K2 from the global histogram on every shard -> identical edges equal
+    to the single-window edges; each shard's batches equal the reference drain of
+    that shard on the global edges (SURVEY §8e parity definition)."""
+    from paper_2507_17120_b200.sharding import shard_range
+    cfg, lens, cls = W.make_window("c2", n=300_000, seed=31)
+    spec = _cfg_spec(cfg)
+    full = _oracle(spec, lens, cls)
+    dev = torch.device("cuda", 0)
+    scheds, shards, hists = [], [], []
+    for r in range(world):
+        a, b = shard_range(len(lens), r, world)
+        s = _sched(spec, b - a)
+        l, c = lens[a:b], cls[a:b]
+        hists.append(s.histogram(torch.as_tensor(l).to(dev), torch.as_tensor(c).to(dev)))
+        scheds.append(s)
+        shards.append((l, c))
+    glob = torch.stack(hists).sum(0).reshape(-1)
+    for (l, c), s in zip(shards, scheds):
+        tok_off, tokens = W.token_store(l)
+        res = s.schedule(torch.as_tensor(l).to(dev), torch.as_tensor(c).to(dev),
+                         torch.as_tensor(tok_off).to(dev), torch.as_tensor(tokens).to(dev),
+                         hist_reduce=lambda h: h.copy_(glob))
+        h = res.to_host()
+        assert np.array_equal(h["edges"], full.edges)
+        assert h["summary"]["n_max"] == full.summary["n_max"]
+        assert h["summary"]["total_global"] == len(lens)
+        shard_spec = dict(spec, adjust=False, init_edges=tuple(int(e) for e in full.edges))
+        o = _oracle(shard_spec, l, c, tok_off, tokens)
+        assert np.array_equal(h["perm"], o.perm)
+        assert np.array_equal(h["req_batch"], o.req_batch)
+        assert np.array_equal(h["req_row"], o.req_row)
+        m = int(h["summary"]["packed_elems"])
+        assert np.array_equal(h["out_tokens"][:m], o.out_tokens[:m])
+        s.close()
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+def test_pack_variants_bit_exact(variant, monkeypatch):
+    """Every K6 variant (BS_PACK_VARIANT tuning hook) packs the same bytes."""
+    monkeypatch.setenv("BS_PACK_VARIANT", str(variant))
+    cfg, lens, cls = W.make_window("c4", n=3_000, seed=2)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+    cfg, lens, cls = W.make_window("c2", n=50_000, seed=2)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
