@@ -11,7 +11,8 @@
 // n_max = BatchController.current_n_max (batch_controller.py:93-104) evaluated
 // with CPython's float floor division, bit-exact.
 //
-// B200 mapping, three launches:
+// B200 mapping.  l_max <= 16384: one fused CTA (k_bounds_small, below).  Larger
+// l_max (long context), three launches:
 //   K2a  k_prefix_tiles  one CTA per 4096 lengths: tile-local exclusive prefixes of
 //                        the total and per-class histograms, tile totals, sum(len)
 //   K2b  k_boundaries    one 1024-thread CTA: carries over the tiles, n_max, the
@@ -392,6 +393,335 @@ __global__ void __launch_bounds__(256)
     if (sbins[i]) atomicAdd(&bins_cnt[i], sbins[i]);
 }
 
+// ---------------------------------------------------------------------------- small L
+// Single-CTA fused K2 for l_max <= kSmallL: prefix sums live in shared memory and the
+// window fixpoint from the root (no init edges, passes until no split) is computed
+// on the implicit midpoint tree level by level: a node of depth d is a bucket of
+// pass d+1 iff its parent split, so every pass costs one level of work and the
+// change log is one scan over the split flags in heap (= pass-major, left-to-right)
+// order — exactly the reference's emission order.  Other modes run the general
+// pass loop.  Lookup tables and digit counts are built by the same CTA.
+constexpr int kSmallL = 16384;
+constexpr int kMaxDepth = 15;  // ceil(log2(kSmallL)) + 1
+
+__device__ __forceinline__ void node_bounds(int32_t L, int d, int32_t k, int32_t& lo,
+                                            int32_t& up) {
+  lo = 0;
+  up = L;
+  for (int bit = d - 1; bit >= 0; --bit) {
+    const int32_t mid = (lo + up) >> 1;
+    if ((k >> bit) & 1) lo = mid; else up = mid;
+  }
+}
+
+__global__ void __launch_bounds__(kBT, 1)
+    k_bounds_small(const uint32_t* __restrict__ hist_local,
+                   const uint32_t* __restrict__ hist_global, bs_window_params p, int sort_bits,
+                   int sort_passes, const int32_t* __restrict__ init_edges, int32_t k_init,
+                   int32_t* __restrict__ edges_out, int32_t* __restrict__ changes_out,
+                   int32_t changes_cap, int32_t* __restrict__ seg_off_out,
+                   uint32_t* __restrict__ PcL, int32_t* __restrict__ gE,
+                   int32_t* __restrict__ seg_base, int32_t* __restrict__ lut,
+                   uint32_t* __restrict__ slot_lut, uint32_t* __restrict__ bins_cnt,
+                   int32_t* __restrict__ kinfo, bs_summary* sum) {
+  extern __shared__ uint32_t dyn[];
+  __shared__ BoundsShared sh;
+  __shared__ uint32_t sbins[4 * 256];
+  __shared__ int32_t s_flag;
+  const int32_t L = p.l_max, C = p.n_classes;
+  const int W = (L + 1 + 31) / 32;
+  const int tid = threadIdx.x;
+  const int NW = ((1 << kMaxDepth) + 31) / 32;     // node-bitmask words
+  uint32_t* Ps = dyn;                               // [L+1]
+  uint32_t* bm = Ps + (L + 1);                      // [W]
+  uint32_t* split_bits = bm + W;                    // [NW] node split flags (heap order)
+  int32_t* E = reinterpret_cast<int32_t*>(split_bits + NW);  // [L+1]
+  const int chunk = (L + kBT - 1) / kBT;
+  const int x0 = min(L, tid * chunk), x1 = min(L, x0 + chunk);
+
+  // ---- A. prefix sums (global total in smem, local per class in global) ------------
+  {
+    uint32_t s = 0;
+    uint64_t sl = 0;
+    for (int x = x0; x < x1; ++x) {
+      uint32_t h = 0;
+      for (int c = 0; c < C; ++c) h += hist_global[(int64_t)c * L + x];
+      Ps[x] = h;
+      s += h;
+      sl += (uint64_t)h * (uint64_t)x;
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_scan<uint32_t>(s, sh.s32, &tot);
+    for (int x = x0; x < x1; ++x) {
+      const uint32_t h = Ps[x];
+      Ps[x] = run;
+      run += h;
+    }
+    uint64_t sltot;
+    block_excl_scan<uint64_t>(sl, sh.s64, &sltot);
+    for (int c = 0; c < C; ++c) {
+      uint32_t sc = 0;
+      for (int x = x0; x < x1; ++x) sc += hist_local[(int64_t)c * L + x];
+      uint32_t tc;
+      uint32_t rc = block_excl_scan<uint32_t>(sc, sh.s32, &tc);
+      uint32_t* Pc = PcL + (int64_t)c * (L + 1);
+      for (int x = x0; x < x1; ++x) {
+        Pc[x] = rc;
+        rc += hist_local[(int64_t)c * L + x];
+      }
+      if (tid == 0) Pc[L] = tc;
+    }
+    if (tid == 0) {
+      Ps[L] = tot;
+      sh.total = tot;
+      int64_t nm;
+      if (p.n_max > 0) {
+        nm = p.n_max;
+      } else if (tot == 0) {
+        nm = 1;
+      } else {
+        const double mean = __ddiv_rn((double)sltot, (double)tot);
+        if (mean == 0.0) {
+          latch_flags(sum, BS_FLAG_ZERO_MEAN);
+          nm = 1;
+        } else {
+          const int64_t tb = p.current_safe / p.kv_bytes_per_token;
+          nm = (int64_t)py_floordiv((double)tb, mean);
+          if (nm < 1) nm = 1;
+        }
+      }
+      sh.n_max = nm;
+      sum->total_global = tot;
+      sum->sum_len_global = (int64_t)sltot;
+      sum->n_max = nm;
+    }
+  }
+  for (int w = tid; w < W; w += kBT) bm[w] = 0;
+  for (int w = tid; w < NW; w += kBT) split_bits[w] = 0;
+  for (int i = tid; i < 4 * 256; i += kBT) sbins[i] = 0;
+  if (tid == 0) { sh.bad = 0; s_flag = 0; }
+  __syncthreads();
+  const int64_t n_max = sh.n_max;
+  const uint32_t total = sh.total;
+  int64_t nch = 0;
+  int32_t passes = 0;
+  const bool fast = init_edges == nullptr && p.adjust && p.max_passes <= 0;
+
+  if (fast) {
+    // ---- C'. window fixpoint on the midpoint tree, one level per pass ---------------
+    if (tid == 0) { atomicOr(&bm[0], 1u); atomicOr(&bm[L >> 5], 1u << (L & 31)); }
+    int deepest = -1;
+    for (int d = 0; d < kMaxDepth; ++d) {
+      const int32_t nodes = 1 << d;
+      int any = 0;
+      for (int32_t k = tid; k < nodes; k += kBT) {
+        const int32_t id = nodes - 1 + k;
+        bool realized = d == 0;
+        if (d > 0) {
+          const int32_t par = (id - 1) >> 1;
+          realized = (split_bits[par >> 5] >> (par & 31)) & 1u;
+        }
+        if (!realized) continue;
+        int32_t lo, up;
+        node_bounds(L, d, k, lo, up);
+        const int32_t mid = (lo + up) >> 1;
+        const uint32_t c = Ps[up] - Ps[lo], s = Ps[mid] - Ps[lo];
+        if ((int64_t)c > n_max && (double)s > __dmul_rn(p.split_threshold, (double)c)) {
+          if (mid <= lo) {
+            s_flag = 1;  // a skip: leave it to the general loop (never happens on counts)
+          } else {
+            atomicOr(&split_bits[id >> 5], 1u << (id & 31));
+            atomicOr(&bm[mid >> 5], 1u << (mid & 31));
+            any = 1;
+          }
+        }
+      }
+      any = __syncthreads_or(any);
+      if (!any) break;
+      deepest = d;
+    }
+    passes = deepest + 2;
+    __syncthreads();
+    if (s_flag) {  // fall back: reset and run the general loop below
+      for (int w = tid; w < W; w += kBT) bm[w] = 0;
+      __syncthreads();
+    } else {
+      // change log: split nodes in heap order == pass-major, left to right
+      const int32_t nnodes = deepest >= 0 ? (2 << deepest) - 1 : 0;
+      const int per = (nnodes + kBT - 1) / kBT;
+      const int32_t n0 = tid * per, n1 = min(nnodes, n0 + per);
+      int32_t cnt = 0;
+      for (int32_t id = n0; id < n1; ++id) cnt += (split_bits[id >> 5] >> (id & 31)) & 1u;
+      int32_t tot;
+      int32_t off = block_excl_scan<int32_t>(cnt, sh.si, &tot);
+      for (int32_t id = n0; id < n1; ++id) {
+        if ((split_bits[id >> 5] >> (id & 31)) & 1u) {
+          if (off < changes_cap) {
+            const int d = 31 - __clz(id + 1);
+            int32_t lo, up;
+            node_bounds(L, d, id + 1 - (1 << d), lo, up);
+            int32_t* r = changes_out + 4 * off;
+            r[0] = BS_CHANGE_SPLIT; r[1] = lo; r[2] = up; r[3] = (lo + up) >> 1;
+          }
+          ++off;
+        }
+      }
+      nch = tot;
+    }
+  }
+  if (!fast || s_flag) {
+    // ---- B/C. general adjust_buckets passes (init edges / max_passes / skips) -----------
+    nch = 0;
+    passes = 0;
+    if (init_edges) {
+      for (int i = tid; i <= k_init; i += kBT) {
+        const int32_t e = init_edges[i];
+        bool ok = e >= 0 && e <= L;
+        if (i == 0) ok = ok && e == 0;
+        if (i == k_init) ok = ok && e == L;
+        if (i > 0) ok = ok && init_edges[i - 1] < e;
+        if (!ok) sh.bad = 1;
+        else atomicOr(&bm[e >> 5], 1u << (e & 31));
+      }
+      __syncthreads();
+      if (sh.bad || k_init < 1) {
+        if (tid == 0) latch_flags(sum, BS_FLAG_BAD_EDGES);
+        for (int w = tid; w < W; w += kBT) bm[w] = 0;
+        __syncthreads();
+        if (tid == 0) { atomicOr(&bm[0], 1u); atomicOr(&bm[L >> 5], 1u << (L & 31)); }
+      }
+    } else if (tid == 0) {
+      atomicOr(&bm[0], 1u);
+      atomicOr(&bm[L >> 5], 1u << (L & 31));
+    }
+    __syncthreads();
+    if (p.adjust) {
+      for (;;) {
+        const int32_t K = compact_edges(bm, W, E, sh);
+        ++passes;
+        if ((int64_t)total < n_max) {
+          if (K != 1) {
+            for (int w = tid; w < W; w += kBT) bm[w] = 0;
+            __syncthreads();
+            if (tid == 0) {
+              atomicOr(&bm[0], 1u);
+              atomicOr(&bm[L >> 5], 1u << (L & 31));
+              if (nch < changes_cap) {
+                int32_t* r = changes_out + 4 * nch;
+                r[0] = BS_CHANGE_MERGE; r[1] = 0; r[2] = L; r[3] = -1;
+              }
+            }
+            ++nch;
+            __syncthreads();
+          }
+          break;
+        }
+        if ((int64_t)total == n_max) break;
+        int any = 0;
+        for (int base = 0; base < K; base += kBT) {
+          const int k = base + tid;
+          int kind = 0, lo = 0, up = 0, mid = 0;
+          if (k < K) {
+            lo = E[k]; up = E[k + 1]; mid = (lo + up) >> 1;
+            const uint32_t c = Ps[up] - Ps[lo], s = Ps[mid] - Ps[lo];
+            if ((int64_t)c > n_max && (double)s > __dmul_rn(p.split_threshold, (double)c))
+              kind = (mid <= lo) ? BS_CHANGE_SKIP : BS_CHANGE_SPLIT;
+          }
+          int32_t tot;
+          const int32_t off = block_excl_scan<int32_t>(kind != 0, sh.si, &tot);
+          if (kind) {
+            const int64_t idx = nch + off;
+            if (idx < changes_cap) {
+              int32_t* r = changes_out + 4 * idx;
+              r[0] = kind; r[1] = lo; r[2] = up; r[3] = mid;
+            }
+            if (kind == BS_CHANGE_SPLIT) {
+              atomicOr(&bm[mid >> 5], 1u << (mid & 31));
+              any = 1;
+            }
+          }
+          nch += tot;
+        }
+        any = __syncthreads_or(any);
+        if (!any) break;
+        if (p.max_passes > 0 && passes >= p.max_passes) break;
+      }
+    }
+  }
+  __syncthreads();
+  const int32_t K = compact_edges(bm, W, E, sh);
+  for (int i = tid; i <= K; i += kBT) { edges_out[i] = E[i]; gE[i] = E[i]; }
+
+  // ---- E. segment offsets (local per-class counts) and radix slot bases -------------
+  const int32_t S = K * C;
+  // ---- D. per-length bucket LUT (K3): largest b with E[b] <= x ----------------------
+  for (int x = tid; x < L; x += kBT) {
+    // binary search over E (smem): largest b with E[b] <= x
+    int32_t lo = 0, hi = K;
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (E[mid] <= x) lo = mid; else hi = mid;
+    }
+    lut[x] = lo;
+  }
+  __syncthreads();
+  int32_t run_cnt = 0, run_w = 0;
+  for (int base = 0; base < S; base += kBT) {
+    const int s = base + tid;
+    int32_t cnt = 0, width = 0;
+    if (s < S) {
+      const int b = s / C, c = s % C;
+      const int32_t lo = E[b], up = E[b + 1];
+      const uint32_t* Pc = PcL + (int64_t)c * (L + 1);
+      cnt = (int32_t)(Pc[up] - Pc[lo]);
+      width = p.policy[c] == BS_POLICY_FCFS ? 1 : (up - lo);
+    }
+    int32_t tcn, tw;
+    const int32_t oc = block_excl_scan<int32_t>(cnt, sh.si, &tcn);
+    const int32_t ow = block_excl_scan<int32_t>(width, sh.si, &tw);
+    if (s < S) {
+      seg_off_out[s] = run_cnt + oc;
+      seg_base[s] = run_w + ow;
+    }
+    run_cnt += tcn;
+    run_w += tw;
+  }
+  if (tid == 0) seg_off_out[S] = run_cnt;
+  __syncthreads();
+  // ---- F. radix slots per (class, length) + digit counts --------------------------------
+  const uint32_t dmask = (1u << sort_bits) - 1u;
+  for (int64_t idx = tid; idx < (int64_t)C * L; idx += kBT) {
+    const int c = (int)(idx / L), x = (int)(idx % L);
+    const int b = lut[x];
+    const int pol = p.policy[c];
+    uint32_t slot = (uint32_t)seg_base[b * C + c];
+    if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - E[b]);
+    else if (pol == BS_POLICY_LJF) slot += (uint32_t)(E[b + 1] - 1 - x);
+    slot_lut[idx] = slot;
+    const uint32_t h = hist_local[idx];
+    const unsigned act = __ballot_sync(__activemask(), h != 0);
+    if (h) {
+      for (int q = 0; q < sort_passes; ++q) {
+        const uint32_t d = (slot >> (q * sort_bits)) & dmask;
+        const unsigned peers = __match_any_sync(act, d);
+        const uint32_t tot = __reduce_add_sync(peers, h);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sbins[q * 256 + d], tot);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < 4 * 256; i += kBT) bins_cnt[i] = sbins[i];
+  if (tid == 0) {
+    kinfo[0] = K;
+    kinfo[1] = run_w;
+    kinfo[2] = S;
+    sum->k_buckets = K;
+    sum->n_changes = nch;
+    sum->n_passes = passes;
+    if (nch > changes_cap) latch_flags(sum, BS_FLAG_CHANGES_TRUNC);
+  }
+}
+
 SortPlan sort_plan(int32_t l_max, int32_t n_classes) {
   // slots D <= n_classes * l_max; digits of <= 8 bits, split evenly over passes
   uint64_t dmax = (uint64_t)n_classes * (uint64_t)l_max;
@@ -408,6 +738,23 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
                               int32_t* seg_off_out, bs_summary* summary, cudaStream_t st) {
   const SortPlan sp = sort_plan(p.l_max, p.n_classes);
   const int32_t L = p.l_max, C = p.n_classes;
+  if (L <= kSmallL) {
+    const int W = (L + 1 + 31) / 32;
+    const int NW = ((1 << kMaxDepth) + 31) / 32;
+    const size_t smem = sizeof(uint32_t) * ((size_t)(L + 1) + W + NW + (L + 1));
+    static size_t attr_small = 0;
+    if (smem > 48 * 1024 && smem > attr_small) {
+      cudaFuncSetAttribute(k_bounds_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_small = smem;
+    }
+    k_bounds_small<<<1, kBT, smem, st>>>(hist_local, hist_global ? hist_global : hist_local, p,
+                                         sp.bits, sp.passes, init_edges, k_init, edges_out,
+                                         changes_out, changes_cap, seg_off_out, ctx->PcL, ctx->E,
+                                         ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
+                                         ctx->kinfo, summary);
+    ++ctx->launches;
+    return cudaGetLastError();
+  }
   const int ntiles = (L + kTileX - 1) / kTileX;
   const uint32_t* hg = hist_global ? hist_global : hist_local;
   k_prefix_tiles<<<ntiles, 1024, 0, st>>>(hist_local, hg, L, C, ctx->P, ctx->PcL, ctx->tile_tot,

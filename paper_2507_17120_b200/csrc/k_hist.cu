@@ -93,10 +93,10 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
     attr_set = true;
   }
   const int threads = 512;
-  // >= 8 elements per thread; the flush only touches non-zero bins, so its cost
-  // is bounded by the elements each CTA read
-  int64_t blocks = (n + 8LL * threads - 1) / (8LL * threads);
-  blocks = std::min<int64_t>(blocks, 3LL * ctx->num_sms);
+  // >= 16 elements per thread and at most 2 CTAs per SM: the per-CTA zero/flush of the
+  // privatised bins stays well below the elements each CTA reads
+  int64_t blocks = (n + 16LL * threads - 1) / (16LL * threads);
+  blocks = std::min<int64_t>(blocks, 2LL * ctx->num_sms);
   blocks = std::max<int64_t>(blocks, 1);
   const int vec_ok = ((reinterpret_cast<uintptr_t>(len) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(cls) & 3) == 0);

@@ -181,12 +181,13 @@ __global__ void __launch_bounds__(256)
     const int64_t gend = ((g << 5) + 32) < a.n ? ((g << 5) + 32) : a.n;
     const bool nr = valid && ((nrm >> lane) & 1u);
     // suffix max / sum of the admissible lengths at lanes >= lane
+    // (sums of <= 32 lengths < 2^22 and of <= 32 group sums < 2^27 fit int32)
     int32_t vm = nr ? x : 0;
-    int64_t vs = nr ? x : 0;
+    int32_t vs = nr ? x : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t tm = __shfl_down_sync(FULL, vm, o);
-      const int64_t ts = __shfl_down_sync(FULL, vs, o);
+      const int32_t ts = __shfl_down_sync(FULL, vs, o);
       if (lane + o < 32) { vm = tm > vm ? tm : vm; vs += ts; }
     }
     const uint32_t rem = nrm & (FULL << lane);
@@ -213,14 +214,13 @@ __global__ void __launch_bounds__(256)
     int64_t base = g + 1;
     while (__any_sync(FULL, mode == 1)) {
       const int64_t gi = base + lane;
-      int32_t pc = 0, pm = 0;
-      int64_t ps = 0;
+      int32_t pc = 0, pm = 0, ps = 0;
       if (gi < G) { pc = bcnt[gi]; pm = bmax[gi]; ps = bsum[gi]; }
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t tc = __shfl_up_sync(FULL, pc, o);
         const int32_t tm = __shfl_up_sync(FULL, pm, o);
-        const int64_t ts = __shfl_up_sync(FULL, ps, o);
+        const int32_t ts = __shfl_up_sync(FULL, ps, o);
         if (lane >= o) { pc += tc; pm = tm > pm ? tm : pm; ps += ts; }
       }
       int ng = 0;
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256)
         const int src = mid < 31 ? mid : 31;
         const int32_t qc = __shfl_sync(FULL, pc, src);
         const int32_t qm = __shfl_sync(FULL, pm, src);
-        const int64_t qs = __shfl_sync(FULL, ps, src);
+        const int32_t qs = __shfl_sync(FULL, ps, src);
         if (lo < hi) {
           const int64_t nm = qm > st.m ? qm : st.m;
           if (violates(a, nm, st.c + qc, st.s + qs)) hi = mid; else lo = mid + 1;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(256)
       const int src2 = lo - 1 < 0 ? 0 : (lo - 1 > 31 ? 31 : lo - 1);
       const int32_t bc = __shfl_sync(FULL, pc, src2);
       const int32_t bm = __shfl_sync(FULL, pm, src2);
-      const int64_t bs = __shfl_sync(FULL, ps, src2);
+      const int32_t bs = __shfl_sync(FULL, ps, src2);
       if (mode == 1) {
         if (lo > 0) { st.m = bm > st.m ? bm : st.m; st.c += bc; st.s += bs; }
         if (lo < ng) { mode = 3; p = (base + lo) << 5; }        // violation inside that group
