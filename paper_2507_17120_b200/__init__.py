@@ -1,7 +1,9 @@
 """B200-native BucketServe scheduling hot path (arXiv 2507.17120).
 
-Drop-in names of the reference package (bucketsim) for the scheduling path, with
-the window hot path on sm_100a kernels behind a C-ABI (include/bucketserve.h):
+Drop-in names of the reference package (bucketsim) for the scheduling path
+(BucketSet, Bucket, BatchController, order_requests, memory-model functions; see
+compat.py), with the window hot path on sm_100a kernels behind a C-ABI
+(include/bucketserve.h):
 
     from paper_2507_17120_b200 import WindowScheduler, ModelConfig, GpuConfig
     sched = WindowScheduler(model, gpu, max_requests=1 << 20)
@@ -18,6 +20,8 @@ from .memory_model import (MODEL_PRESETS, GpuConfig, ModelConfig, kv_footprint_e
 from .types import (BatchPlan, DispatchPolicy, MemoryAccounting, OversizeRejection,
                     PartitionViolation, Request, StructuralChange, TaskClass)
 from ._native import NativeUnavailable
+from .compat import (Bucket, BucketSet, BatchController, WindowSchedule, order_requests,
+                     schedule_requests)
 
 __version__ = "0.1.0"
 

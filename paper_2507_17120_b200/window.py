@@ -378,6 +378,37 @@ class WindowScheduler:
                 res.check()
         return res
 
+    def boundaries(self, lengths, classes=None, *, init_edges=None, n_max=None,
+                   max_passes=None):
+        """K1 + K2 only: BucketSet.adjust_buckets run `max_passes` times (None: the
+        configured value) from `init_edges` (None: the configured edges) with an
+        explicit split floor `n_max` (None: current_n_max from the histogram).
+        Returns (edges, [StructuralChange], summary)."""
+        if classes is None:
+            classes = np.zeros(len(lengths), np.uint8)
+        lens, cls, n = self._inputs(lengths, classes)
+        p = N.WindowParams.from_buffer_copy(self._params)
+        if n_max is not None:
+            p.n_max = int(n_max)
+        if max_passes is not None:
+            p.max_passes = int(max_passes)
+        ie, k_init = self.init_edges, self.k_init
+        if init_edges is not None:
+            e = np.asarray(init_edges, np.int32)
+            ie, k_init = torch.as_tensor(e).to(self.device), len(e) - 1
+        lib = N.load()
+        st = _stream_handle(self.device)
+        with torch.cuda.device(self.device):
+            N.check(lib.bs_histogram(self.ctx.ptr, _ptr(lens), _ptr(cls), n, C.byref(p),
+                                     _ptr(self.hist), _ptr(self.summary), st), self.ctx.ptr)
+            N.check(lib.bs_boundaries(self.ctx.ptr, _ptr(self.hist), _ptr(self.hist), C.byref(p),
+                                      _ptr(ie), k_init, _ptr(self.edges), _ptr(self.changes),
+                                      self.changes_cap, _ptr(self.summary), st), self.ctx.ptr)
+        torch.cuda.current_stream(self.device).synchronize()
+        res = WindowResult(self, n, False)
+        res.check()
+        return res.edges(), res.changes(), res.summary()
+
     def monitor_bins(self, bins: int = 64) -> np.ndarray:
         """f2: the 64-bin LengthHistogram view of the last window (pd_sim.py:828-833)."""
         out = torch.zeros(bins, dtype=torch.int64, device=self.device)

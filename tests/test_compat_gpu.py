@@ -1,0 +1,177 @@
+"""The reference-shaped drop-in surface (compat.py) on the GPU.
+
+Scenarios restated from the reference's own bucket-manager / batch-controller
+tests (pkg/tests/test_bucket_manager.py, test_batch_controller.py),
+run against the GPU-backed BucketSet / BatchController, plus whole-window
+equivalence with the live-reference golden fixtures via schedule_requests."""
+
+from collections import deque
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from golden_util import fixture_names, load  # noqa: E402
+from paper_2507_17120_b200 import GpuConfig, ModelConfig, safe_memory  # noqa: E402
+from paper_2507_17120_b200.compat import (BatchController, Bucket, BucketSet,  # noqa: E402
+                                          schedule_requests)
+from paper_2507_17120_b200.types import (DispatchPolicy, MemoryAccounting, Request,  # noqa: E402
+                                         TaskClass)
+
+UNIT = ModelConfig(1, 1, 1, 2, 100_000)  # 4 bytes of KV per token
+
+
+def _req(rid, length, arrival=0.0, cls=TaskClass.OFFLINE):
+    return Request(rid, arrival, length, 10, cls)
+
+
+def _gpu_budget(tokens):
+    return GpuConfig(total_mem=tokens * UNIT.kv_bytes_per_token, model_mem=0, reserve_fraction=0.0)
+
+
+def _bucket(low, up, lengths, cls=TaskClass.OFFLINE):
+    return Bucket(low, up, deque(_req(i, s, float(i), cls) for i, s in enumerate(lengths)))
+
+
+# ---- BucketSet (bucket_manager.py) -------------------------------------------------
+def test_assign_half_open_and_counters():
+    bs = BucketSet(4096, buckets=[Bucket(0, 256), Bucket(256, 1024), Bucket(1024, 4096)])
+    assert bs.assign(_req(0, 256)) == 1
+    assert bs.assign(_req(1, 255)) == 0
+    assert bs.assign(_req(2, 1023)) == 1
+    assert bs.last_assign_comparisons == 2
+    with pytest.raises(ValueError):
+        bs.assign(_req(3, 4096))
+
+
+def test_adjust_split_trace_12_8():
+    bs = BucketSet(2048, buckets=[_bucket(0, 2048, [500] * 12 + [1500] * 8)])
+    ch = bs.adjust_buckets(16)
+    assert [c.kind for c in ch] == ["split"] and ch[0].midpoint == 1024
+    assert [(b.low, b.up, len(b)) for b in bs.buckets] == [(0, 1024, 12), (1024, 2048, 8)]
+    assert bs.check_partition() is None
+
+
+def test_adjust_merge_orders_by_arrival():
+    a, b, c = _req(0, 100, 5.0), _req(1, 1500, 1.0), _req(2, 200, 3.0)
+    bs = BucketSet(2048, buckets=[Bucket(0, 1024, deque([a, c])), Bucket(1024, 2048, deque([b]))])
+    ch = bs.adjust_buckets(16)
+    assert [x.kind for x in ch] == ["merge"]
+    assert [r.id for r in bs.buckets[0].requests] == [1, 2, 0]
+
+
+def test_adjust_no_split_below_threshold_and_stable_partition():
+    bs = BucketSet(2048, buckets=[_bucket(0, 2048, [500] * 8 + [1500] * 12)])
+    assert bs.adjust_buckets(16) == [] and not bs.dirty
+    bs = BucketSet(2048, buckets=[_bucket(0, 2048, [100, 1900, 150, 1950, 120, 1980, 130, 1905, 110])])
+    bs.adjust_buckets(8)
+    left, right = bs.buckets
+    assert [r.input_len for r in left.requests] == [100, 150, 120, 130, 110]
+    assert [r.input_len for r in right.requests] == [1900, 1950, 1980, 1905]
+
+
+def test_partition_invariant_random_ops():
+    rng = np.random.default_rng(77)
+    bs = BucketSet(4096)
+    nid = 0
+    for step in range(600):
+        if rng.random() < 0.7:
+            bs.assign(_req(nid, int(rng.integers(0, 4096)), float(step)))
+            nid += 1
+        else:
+            bs.adjust_buckets(int(rng.integers(1, 40)))
+    assert bs.check_partition() is None and bs.total_requests == nid
+
+
+# ---- BatchController (batch_controller.py) ------------------------------------------
+def test_form_batch_exact_prefix_and_remaining_queue():
+    bucket = _bucket(0, 100_000, [100, 200, 300, 400])
+    ctl = BatchController(UNIT, _gpu_budget(600), MemoryAccounting.EXACT)
+    plan = ctl.form_batch(bucket, DispatchPolicy.SJF)
+    assert plan.request_ids == (0, 1, 2) and plan.token_sum == 600
+    assert [r.input_len for r in bucket.requests] == [400]
+
+
+def test_form_batch_padded_charges_batch_max():
+    ctl = BatchController(UNIT, _gpu_budget(1500))
+    assert ctl.form_batch(_bucket(0, 100_000, [1000, 10]), DispatchPolicy.FCFS).request_ids == (0,)
+    ctl2 = BatchController(UNIT, _gpu_budget(2000))
+    plan = ctl2.form_batch(_bucket(0, 100_000, [1000, 10]), DispatchPolicy.FCFS)
+    assert plan.request_ids == (0, 1) and plan.footprint == 2000 * UNIT.kv_bytes_per_token
+
+
+def test_form_batch_oversize_rejected_and_zero_headroom():
+    bucket = _bucket(0, 100_000, [5000, 100])
+    ctl = BatchController(UNIT, _gpu_budget(1000), MemoryAccounting.EXACT)
+    plan = ctl.form_batch(bucket, DispatchPolicy.FCFS)
+    assert plan.request_ids == (1,) and [r.request.id for r in ctl.rejections] == [0]
+    assert len(bucket.requests) == 0
+    b2 = _bucket(0, 100_000, [10])
+    ctl2 = BatchController(UNIT, _gpu_budget(600))
+    assert ctl2.form_batch(b2, DispatchPolicy.SJF, pledged=safe_memory(_gpu_budget(600))) is None
+    assert len(b2.requests) == 1
+
+
+def test_form_batch_class_filter_keeps_other_class_in_place():
+    reqs = deque([_req(0, 100, cls=TaskClass.ONLINE), _req(1, 100, cls=TaskClass.OFFLINE),
+                  _req(2, 100, cls=TaskClass.ONLINE)])
+    bucket = Bucket(0, 100_000, reqs)
+    ctl = BatchController(UNIT, _gpu_budget(10_000))
+    plan = ctl.form_batch(bucket, DispatchPolicy.FCFS, task_class=TaskClass.ONLINE)
+    assert plan.request_ids == (0, 2) and [r.id for r in bucket.requests] == [1]
+
+
+def test_form_batch_tie_break_by_arrival_not_queue_order():
+    reqs = deque([_req(0, 100, arrival=2.0), _req(1, 100, arrival=1.0)])
+    ctl = BatchController(UNIT, _gpu_budget(150))
+    plan = ctl.form_batch(Bucket(0, 100_000, reqs), DispatchPolicy.SJF)
+    assert plan.request_ids == (1,)
+
+
+def test_form_batch_matches_max_safe_batch_oracle():
+    from paper_2507_17120_b200 import max_safe_batch
+    rng = np.random.default_rng(8)
+    for _ in range(40):
+        lengths = rng.integers(1, 2000, size=int(rng.integers(1, 30))).tolist()
+        budget = int(rng.integers(1, 20_000))
+        bucket = _bucket(0, 100_000, lengths)
+        ctl = BatchController(UNIT, _gpu_budget(budget), MemoryAccounting.EXACT)
+        plan = ctl.form_batch(bucket, DispatchPolicy.FCFS)
+        got = 0 if plan is None else len(plan)
+        if not ctl.rejections:
+            assert got == max_safe_batch(lengths, budget)
+
+
+# ---- whole window from reference objects --------------------------------------------
+@pytest.mark.parametrize("name", [n for n in fixture_names()
+                                  if not n.startswith(("four_class", "one_pass"))])
+def test_schedule_requests_matches_reference_fixture(name):
+    spec, lens, cls, ref = load(name)
+    if spec["n_classes"] != 2 or spec["policies"][0] != 0:
+        pytest.skip("schedule_requests drives ONLINE=EARLIEST_ARRIVAL / OFFLINE=policy")
+    if spec["kvpt"] % 2:
+        pytest.skip("needs an even kv_bytes_per_token")
+    model = ModelConfig(spec["kvpt"] // 2, 1, 1, 1, spec["l_max"])
+    gpu = GpuConfig(spec["current_safe"], 0, 0.0)
+    if safe_memory(gpu) != spec["current_safe"]:
+        pytest.skip("safe memory not representable exactly")
+    classes = [TaskClass.ONLINE, TaskClass.OFFLINE]
+    reqs = [Request(i, float(i), int(x), 1, classes[int(c)]) for i, (x, c) in enumerate(zip(lens, cls))]
+    pol = {0: DispatchPolicy.FCFS, 1: DispatchPolicy.SJF, 2: DispatchPolicy.LJF}[spec["policies"][1]]
+    out = schedule_requests(reqs, model, gpu, accounting=[MemoryAccounting.PADDED,
+                                                          MemoryAccounting.EXACT][spec["accounting"]],
+                            offline_policy=pol, split_threshold=spec["theta"],
+                            buckets=spec["init_edges"], adjust=spec["adjust"] and spec["max_passes"] == 0,
+                            pledged=spec["pledged"])
+    if spec["max_passes"]:
+        pytest.skip("one-pass fixtures covered by BucketSet.adjust_buckets")
+    ids = [i for p in out.plans for i in p.request_ids]
+    assert ids == ref["batch_ids"].tolist()
+    assert [(p.max_input_len, p.token_sum, p.footprint) for p in out.plans] == \
+        [tuple(m[2:5]) for m in ref["batch_meta"].tolist()]
+    assert [r.request.id for r in out.rejections] == ref["rejected"].tolist()
+    assert sorted(r.id for r in out.pending) == ref["pending"].tolist()
+    assert out.n_max == int(ref["n_max"])
+    assert out.bucket_set.edges() == ref["edges"].tolist()
