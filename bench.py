@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--requests", type=int, default=None, help="requests per GPU (default: config)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the window kernels "
+                    "individually instead of replaying one CUDA graph per window")
     ap.add_argument("--cpu-sample", type=int, default=131_072)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -228,15 +230,30 @@ def main():
                             current_safe=cfg.current_safe, accounting=cfg.accounting,
                             device=dev, process_group=pg)
     # first window sizes the reusable packed-output buffer
+    l_a = sched.ctx.launches
     res = sched.schedule(lens, cls, tok_off, tokens)
     s0 = res.summary()
-    for _ in range(args.warmup):
+    l_b = sched.ctx.launches
+    res = sched.schedule(lens, cls, tok_off, tokens)
+    kernels_per_window = sched.ctx.launches - l_b
+    use_graph = (not args.no_graph) and pg is None
+    # stage breakdown: a separate profiled pass (events between the kernels of the
+    # eager launch sequence), not part of the timed region
+    for _ in range(2):
         sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False)
+    sched.ctx.profile_enable(args.steps)
+    for _ in range(args.steps):
+        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False)
+    torch.cuda.synchronize(dev)
+    stage_ms, prof_steps = sched.ctx.profile_read()
+    stage_ms = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
+    sched.ctx.profile_enable(0)
+    for _ in range(args.warmup):
+        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False, graph=use_graph)
     torch.cuda.synchronize(dev)
 
     # ---------------- timed region: device-resident windows ----------------------
     sampler = ClockSampler(local)
-    sched.ctx.profile_enable(args.steps)
     l0 = sched.ctx.launches
     if pg is not None:
         dist.barrier()
@@ -247,16 +264,16 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False)
+        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False, graph=use_graph)
     ev1.record()
     torch.cuda.synchronize(dev)
     clocks = sampler.stop()
     if pg is not None:
         dist.barrier()
     launches = sched.ctx.launches - l0
+    if use_graph:  # graph replays do not pass through the host launchers: count per window
+        launches = kernels_per_window * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
-    stage_ms, prof_steps = sched.ctx.profile_read()
-    stage_ms = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
     res = sched.schedule(lens, cls, tok_off, tokens)  # check the steady-state result
     s = res.summary()
     assert s["n_batches"] == s0["n_batches"] and s["packed_elems"] == s0["packed_elems"]
@@ -360,6 +377,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu_base,
         "gpu_launches": launches,
+        "cuda_graph": use_graph,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -77,7 +77,7 @@ void free_all(bs_ctx* c) {
                   c->tile_tot, c->tile_slen, c->tile_carry, c->bmw, c->wp, c->kinfo,
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
                   c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
-                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->task_base,
+                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->task_base, c->segw,
                   c->misc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -169,6 +169,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(listA, N + 1); A(listB, N + 1);
   A(node_batch, N + 1);
   A(node_j0, N + 1);
+  A(segw, 5 * (L * C + 1));
   A(rowpos, N + 1);
   A(task_base, N + 2);
   A(misc, 128);

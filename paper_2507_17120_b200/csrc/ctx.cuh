@@ -56,7 +56,8 @@ struct bs_ctx {
   int32_t* rowpos = nullptr;     // [max_n] admitted window row -> drain position (K6)
   int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
                                  //   <= kPiece tokens; exclusive prefix, K5f)
-  int32_t* node_j0 = nullptr;    // [max_n + 1] first admissible position at/after each chain node
+  int32_t* node_j0 = nullptr;
+  int32_t* segw = nullptr;       // [5][l_cap*c_max+1] per-segment chain length / tail / bases    // [max_n + 1] first admissible position at/after each chain node
   int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
   uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
   int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)
@@ -74,6 +75,8 @@ constexpr int kPiece = 2048;  // K6 work unit: at most this many tokens of one r
 // records boundary event `stage` (0..BS_STAGES) of the current profiled step
 inline void prof_mark(bs_ctx* ctx, int stage, cudaStream_t st) {
   if (!ctx->prof_in_window || ctx->prof_steps <= 0 || ctx->prof_recorded >= ctx->prof_steps) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
   cudaEventRecord(ctx->prof_events[(size_t)ctx->prof_recorded * (BS_STAGES + 1) + stage], st);
   if (stage == BS_STAGES) ++ctx->prof_recorded;
 }

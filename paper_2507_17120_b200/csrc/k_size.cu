@@ -22,9 +22,11 @@
 //                  O(1 + span/1024) warp steps instead of O(span/32) serial loads.
 //   K5c  chain     one cooperative kernel: group-count prefix scan, pointer
 //                  doubling J[r] = next^(2^r) (grid.sync per level, stops when
-//                  every segment's chain is covered), then a top-down expansion
-//                  from the segment starts emitting every batch start in
-//                  emission order — O(N log B) work, O(log B) depth.
+//                  every segment's chain is covered), per-segment chain length
+//                  by binary lifting, then every chain node (= batch start) is
+//                  materialised in emission order in parallel (node k of segment s
+//                  is next^k(start_s), composed from the set bits of k) —
+//                  O(N log B) work, O(log B) depth.
 //   K5d  describe  one warp per batch: n / sum / max / min from group summaries
 //   K5f  offsets   one CTA: packed-buffer offsets (scan of n*pitch), row bases, totals
 //   K5e  outcome   one warp per 32 positions: batch id / row / rejected / pending,
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(512)
             int32_t* listA, int32_t* listB, int32_t* node_batch, int32_t* node_j0, int32_t* misc,
             const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
             const int32_t* __restrict__ bcnt, int32_t* __restrict__ Rg, int32_t* btot,
-            int32_t batches_cap, bs_summary* sum) {
+            int32_t* segw, int32_t batches_cap, bs_summary* sum) {
   cg::grid_group grid = cg::this_grid();
   __shared__ ChainShared sh;
   const int64_t n = a.n;
@@ -335,68 +337,79 @@ __global__ void __launch_bounds__(512)
     grid.sync();
     ++r;
   }
-  if (blockIdx.x != 0) return;
-  if (tid == 0) sh.flag = (r + 1 >= r_cap && ld_rel_i32(alive + r)) ? 1 : 0;
-  // ---- phase 2 (block 0): expansion from the segment starts, emission order ----------
-  int32_t cnt = 0;
-  for (int base = 0; base < n_segs; base += bt) {
-    const int s = base + tid;
-    int32_t st = 0, en = 0;
-    if (s < n_segs) { st = seg_off[s]; en = seg_off[s + 1]; }
-    const int f = (s < n_segs) && (st < en);
-    int32_t tot;
-    const int32_t off = block_excl_scan<int32_t>(f, sh.si, &tot);
-    if (f) listA[cnt + off] = st;
-    cnt += tot;
-  }
-  int32_t* cur = listA;
-  int32_t* nxt = listB;
-  for (int lvl = r - 1; lvl >= 0; --lvl) {
-    const int32_t* Jl = J + (int64_t)lvl * n;
-    int32_t run = 0;
-    for (int base = 0; base < cnt; base += bt) {
-      const int i = base + tid;
-      int32_t x = 0, y = kEnd;
-      if (i < cnt) { x = cur[i]; y = Jl[x]; }
-      const int32_t emit = i < cnt ? 1 + (y != kEnd) : 0;
-      int32_t tot;
-      const int32_t off = block_excl_scan<int32_t>(emit, sh.si, &tot);
-      if (i < cnt) {
-        nxt[run + off] = x;
-        if (y != kEnd) nxt[run + off + 1] = y;
+  // ---- phase 2: per segment, chain length and its last node (binary lifting) -------
+  // len = number of chain nodes (form_batch calls); the last one may be an empty tail
+  // (everything left is oversize, or the drain blocks on a request that does not fit)
+  int32_t* seg_len = segw;
+  int32_t* seg_empty = segw + (n_segs + 1);
+  int32_t* seg_tailj0 = segw + 2 * (n_segs + 1);
+  int32_t* seg_nbase = segw + 3 * (n_segs + 1);
+  int32_t* seg_ebase = segw + 4 * (n_segs + 1);
+  for (int64_t sg = (int64_t)blockIdx.x * bt + tid; sg < n_segs; sg += (int64_t)gridDim.x * bt) {
+    const int64_t st = seg_off[sg], en = seg_off[sg + 1];
+    int32_t len = 0, empty = 0, tj0 = 0;
+    if (st < en) {
+      int64_t pos = st;
+      int32_t cnt = 0;
+      for (int lv = r - 1; lv >= 0; --lv) {
+        const int32_t y = J[(int64_t)lv * n + pos];
+        if (y != kEnd) { pos = y; cnt += 1 << lv; }
       }
-      run += tot;
+      len = cnt + 1;
+      const int64_t j0 = first_nonrej(pos, en, bmask);
+      empty = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
+      tj0 = (int32_t)j0;
     }
-    int32_t* t = cur; cur = nxt; nxt = t;
-    cnt = run;
-    __syncthreads();
+    seg_len[sg] = len;
+    seg_empty[sg] = empty;
+    seg_tailj0[sg] = tj0;
   }
-  // ---- batch ids: a chain node is a batch unless it is its segment's empty tail -----------
-  int32_t nb = 0;
-  for (int base = 0; base < cnt; base += bt) {
-    const int i = base + tid;
-    int f = 0;
-    if (i < cnt) {
-      const int64_t c = cur[i];
-      const int64_t s = seg_of(seg_off, n_segs, c);
-      const int64_t end = seg_off[s + 1];
-      const int64_t j0 = first_nonrej(c, end, bmask);
-      f = (j0 < end) && ((int64_t)slen[j0] <= a.T);
-      node_j0[i] = (int32_t)j0;
+  grid.sync();
+  // ---- phase 3 (block 0): node / batch bases per segment ---------------------------------
+  if (blockIdx.x == 0) {
+    if (tid == 0) sh.flag = (r + 1 >= r_cap && ld_rel_i32(alive + r)) ? 1 : 0;
+    int32_t run_n = 0, run_e = 0;
+    for (int base = 0; base < n_segs; base += bt) {
+      const int sg = base + tid;
+      const int32_t ln = sg < n_segs ? ld_rel_i32(seg_len + sg) : 0;
+      const int32_t em = sg < n_segs ? ld_rel_i32(seg_empty + sg) : 0;
+      int32_t tn, te;
+      const int32_t on = block_excl_scan<int32_t>(ln, sh.si, &tn);
+      const int32_t oe = block_excl_scan<int32_t>(em, sh.si, &te);
+      if (sg < n_segs) { seg_nbase[sg] = run_n + on; seg_ebase[sg] = run_e + oe; }
+      run_n += tn;
+      run_e += te;
     }
-    int32_t tot;
-    const int32_t off = block_excl_scan<int32_t>(f, sh.si, &tot);
-    if (i < cnt) node_batch[i] = f ? nb + off : -1;
-    nb += tot;
+    if (tid == 0) {
+      seg_nbase[n_segs] = run_n;
+      seg_ebase[n_segs] = run_e;
+      const int32_t nb = run_n - run_e;
+      misc[64] = run_n;
+      misc[65] = r;
+      misc[66] = nb;
+      misc[68] = 0;
+      sum->n_batches = nb;
+      if (nb > batches_cap) latch_flags(sum, BS_FLAG_BATCH_CAP);
+      if (sh.flag) latch_flags(sum, BS_FLAG_BATCH_CAP);  // doubling table exhausted
+    }
   }
-  if (tid == 0) {
-    misc[64] = cnt;
-    misc[65] = r;
-    misc[66] = nb;
-    misc[68] = cur == listA ? 0 : 1;
-    sum->n_batches = nb;
-    if (nb > batches_cap) latch_flags(sum, BS_FLAG_BATCH_CAP);
-    if (sh.flag) latch_flags(sum, BS_FLAG_BATCH_CAP);  // doubling table exhausted
+  grid.sync();
+  // ---- phase 4: materialise every chain node in emission order (fully parallel) -------
+  const int32_t M = ld_rel_i32(seg_nbase + n_segs);
+  for (int64_t i = (int64_t)blockIdx.x * bt + tid; i < M; i += (int64_t)gridDim.x * bt) {
+    int32_t lo = 0, hi = n_segs;  // last segment with seg_nbase <= i (non-empty ones win ties)
+    while (hi - lo > 1) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (ld_rel_i32(seg_nbase + mid) <= i) lo = mid; else hi = mid;
+    }
+    const int32_t k = (int32_t)(i - ld_rel_i32(seg_nbase + lo));
+    int64_t pos = seg_off[lo];
+    for (int lv = 0; lv < r; ++lv)
+      if ((k >> lv) & 1) pos = J[(int64_t)lv * n + pos];
+    listA[i] = (int32_t)pos;
+    const bool tail_empty = (k == ld_rel_i32(seg_len + lo) - 1) && ld_rel_i32(seg_empty + lo);
+    node_batch[i] = tail_empty ? -1 : (int32_t)(i - ld_rel_i32(seg_ebase + lo));
+    node_j0[i] = tail_empty ? ld_rel_i32(seg_tailj0 + lo) : (int32_t)pos;
   }
 }
 
@@ -658,11 +671,12 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     const int32_t* bc = ctx->bcnt;
     int32_t* rg = ctx->Rg;
     int32_t* bt = ctx->btot;
+    int32_t* sw = ctx->segw;
     int32_t bcap = batches_cap;
     bs_summary* sm = summary;
     void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
                     &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
-                    (void*)&bc, &rg,   &bt,        &bcap, &sm};
+                    (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm};
     e = cudaLaunchCooperativeKernel((void*)k_chain, dim3(ctx->chain_blocks), dim3(512), args, 0,
                                     st);
     if (e != cudaSuccess) return e;

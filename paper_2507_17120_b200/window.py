@@ -260,6 +260,8 @@ class WindowScheduler:
             self.init_edges = torch.as_tensor(e).to(dev)
             self.k_init = len(e) - 1
         self.with_mask = with_mask
+        self._graph = None
+        self._graph_key = None
         self.out_tokens = None
         self.out_mask = None
         self.pack_capacity = 0
@@ -323,14 +325,18 @@ class WindowScheduler:
         return out
 
     def schedule(self, lengths, classes, tok_off=None, tokens=None, *, sync: bool = True,
-                 check: bool = True, hist_reduce=None) -> WindowResult:
+                 check: bool = True, hist_reduce=None, graph: bool = False) -> WindowResult:
         """Schedule one window.  `lengths` int32[n] and `classes` uint8[n] in arrival
         order (device tensors, or host arrays that are copied); optional CSR token
         store (`tok_off` int64[n+1], `tokens` int32[...]) enables packing.
 
         Sharded windows: with a process group (constructor) the local histogram is
         all-reduced over it (C1); `hist_reduce(hist)` may instead transform the
-        local histogram in place into the global one (e.g. in single-GPU tests)."""
+        local histogram in place into the global one (e.g. in single-GPU tests).
+
+        graph=True replays the whole fused window (16-20 kernels) as one CUDA graph,
+        captured on the first call for these input buffers (serving loops reuse
+        their input buffers); launch gaps between the stages disappear."""
         dev = self.device
         lens, cls, n = self._inputs(lengths, classes)
         pack = tok_off is not None and tokens is not None
@@ -346,6 +352,26 @@ class WindowScheduler:
             self._ensure_pack(64)  # nothing to pack; keep the result shape uniform
         two_phase = pack and self.pack_capacity == 0
         sharded = self.process_group is not None or hist_reduce is not None
+        if graph and not sharded and not two_phase:
+            key = (lens.data_ptr(), cls.data_ptr(), n,
+                   tok_off.data_ptr() if pack else 0, tokens.data_ptr() if pack else 0,
+                   self.pack_capacity)
+            if self._graph is None or self._graph_key != key:
+                self._graph = None
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    io_g = self._io(lens, cls, n, tok_off, tokens, pack)
+                    N.check(lib.bs_window_schedule(self.ctx.ptr, C.byref(io_g), C.byref(p),
+                                                   _stream_handle(dev)), self.ctx.ptr)
+                self._graph, self._graph_key = g, key
+            self._graph.replay()
+            res = WindowResult(self, n, pack)
+            if sync:
+                torch.cuda.current_stream(dev).synchronize()
+                if check:
+                    res.check()
+            return res
         if sharded and self.hist_global is None:
             self.hist_global = torch.zeros_like(self.hist)
         io = self._io(lens, cls, n, tok_off, tokens, pack and not two_phase)
@@ -374,6 +400,19 @@ class WindowScheduler:
         res = WindowResult(self, n, pack)
         if sync:
             torch.cuda.current_stream(dev).synchronize()
+            s = res.summary()
+            if pack and (s["flags"] & N.FLAG_PACK_CAPACITY):
+                # the packed extent outgrew the reusable buffer: grow it and re-pack
+                self._ensure_pack(int(s["packed_elems"]))
+                keep = int(s["flags"]) & ~N.FLAG_PACK_CAPACITY  # flags word at byte 128
+                self.summary[128:136].copy_(torch.tensor([keep], dtype=torch.int64).view(torch.uint8))
+                with torch.cuda.device(dev):
+                    N.check(lib.bs_pack(self.ctx.ptr, _ptr(lens), _ptr(self.perm), _ptr(tok_off),
+                                        _ptr(tokens), C.byref(p), _ptr(self.batches_raw), 0, -1,
+                                        _ptr(self.out_tokens), _ptr(self.out_mask),
+                                        self.pack_capacity, _ptr(self.summary), st), self.ctx.ptr)
+                torch.cuda.current_stream(dev).synchronize()
+                res = WindowResult(self, n, pack)
             if check:
                 res.check()
         return res

@@ -272,3 +272,43 @@ def test_pack_variants_bit_exact(variant, monkeypatch):
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
     cfg, lens, cls = W.make_window("c2", n=50_000, seed=2)
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+
+
+def test_cuda_graph_replay_matches_eager():
+    """graph=True (one CUDA graph per window, replayed) gives the eager result."""
+    cfg, lens, cls = W.make_window("c2", n=120_000, seed=44)
+    spec = _cfg_spec(cfg)
+    dev = torch.device("cuda", 0)
+    tok_off, tokens = W.token_store(lens)
+    t = [torch.as_tensor(x).to(dev) for x in (lens, cls, tok_off, tokens)]
+    s = _sched(spec, len(lens))
+    eager = s.schedule(*t).to_host()
+    for _ in range(3):
+        g = s.schedule(*t, graph=True).to_host()
+    for k in ("perm", "req_batch", "req_row", "edges", "bucket", "out_tokens", "out_mask"):
+        assert np.array_equal(g[k], eager[k]), k
+    assert np.array_equal(g["batches"], eager["batches"])
+    # new inputs in the same buffers (no larger packed extent): the replay sees them
+    lens2 = np.maximum(lens - 1, 1).astype(np.int32)
+    t[0].copy_(torch.as_tensor(lens2).to(dev))
+    g2 = s.schedule(*t, graph=True).to_host()
+    o = _oracle(spec, lens2, cls)
+    assert np.array_equal(g2["perm"], o.perm) and np.array_equal(g2["req_batch"], o.req_batch)
+    s.close()
+
+
+def test_packed_buffer_grows_when_window_needs_more():
+    cfg, lens, cls = W.make_window("c2", n=50_000, seed=12)
+    spec = _cfg_spec(cfg)
+    s = _sched(spec, len(lens))
+    tok_off, tokens = W.token_store(lens)
+    s.schedule(lens, cls, tok_off, tokens)
+    cap0 = s.pack_capacity
+    lens2 = np.minimum(lens * 2, cfg.l_max - 1).astype(np.int32)
+    tok_off2, tokens2 = W.token_store(lens2)
+    h = s.schedule(lens2, cls, tok_off2, tokens2).to_host()
+    assert s.pack_capacity > cap0
+    o = _oracle(spec, lens2, cls, tok_off2, tokens2)
+    m = int(h["summary"]["packed_elems"])
+    assert np.array_equal(h["out_tokens"][:m], o.out_tokens[:m])
+    s.close()
