@@ -175,10 +175,15 @@ __global__ void __launch_bounds__(256)
     const int32_t x = valid ? slen[j] : 0;
     int64_t e = 0;
     bool start = false;
-    if (valid) {
-      const int64_t s = seg_of(seg_off, n_segs, j);
-      e = seg_off[s + 1];
-      start = seg_off[s] == j;
+    {  // segment of j: one binary search per warp, then a short walk per lane
+      int64_t s0 = 0;
+      if (lane == 0) s0 = seg_of(seg_off, n_segs, g << 5);
+      int64_t s = __shfl_sync(FULL, s0, 0);
+      if (valid) {
+        while (seg_off[s + 1] <= j) ++s;
+        e = seg_off[s + 1];
+        start = seg_off[s] == j;
+      }
     }
     const int64_t gend = ((g << 5) + 32) < a.n ? ((g << 5) + 32) : a.n;
     const bool nr = valid && ((nrm >> lane) & 1u);
@@ -249,10 +254,62 @@ __global__ void __launch_bounds__(256)
       const int32_t bs = __shfl_sync(FULL, ps, src2);
       if (mode == 1) {
         if (lo > 0) { st.m = bm > st.m ? bm : st.m; st.c += bc; st.s += bs; }
-        if (lo < ng) { mode = 3; p = (base + lo) << 5; }        // violation inside that group
-        else if (ng < 32) { mode = 3; p = (base + ng) << 5; }   // segment tail (< 32 elements)
+        if (lo < ng) { mode = 4; p = (base + lo) << 5; }        // violation inside that group
+        else if (ng < 32) { mode = 4; p = (base + ng) << 5; }   // segment tail (< 32 elements)
       }
       base += 32;
+    }
+    // warp-cooperative resolution inside the target group: the warp loads the group
+    // once, builds inclusive prefixes by shuffles, and every lane aiming at that group
+    // binary-searches its first violating element (first violation is admissible:
+    // an inadmissible element leaves the prefix unchanged)
+    unsigned pend = __ballot_sync(FULL, mode == 4);
+    while (pend) {
+      const int leader = __ffs(pend) - 1;
+      const int64_t tp = __shfl_sync(FULL, p, leader);
+      const int64_t te = __shfl_sync(FULL, e, leader);
+      const int lim = (te - tp) < 32 ? (int)(te - tp) : 32;
+      const int32_t xx = lane < lim ? slen[tp + lane] : 0;
+      const bool ad = lane < lim && (int64_t)xx <= a.S;
+      int32_t qc = ad ? 1 : 0, qm = ad ? xx : 0, qs = ad ? xx : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t tc = __shfl_up_sync(FULL, qc, o);
+        const int32_t tm = __shfl_up_sync(FULL, qm, o);
+        const int32_t ts = __shfl_up_sync(FULL, qs, o);
+        if (lane >= o) { qc += tc; qm = tm > qm ? tm : qm; qs += ts; }
+      }
+      const bool serve = mode == 4 && p == tp && e == te;
+      int lo = 0, hi = lim;
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const int src = mid < 31 ? mid : 31;
+        const int32_t c_ = __shfl_sync(FULL, qc, src);
+        const int32_t m_ = __shfl_sync(FULL, qm, src);
+        const int32_t s_ = __shfl_sync(FULL, qs, src);
+        if (serve && lo < hi) {
+          const int64_t nm = m_ > st.m ? m_ : st.m;
+          if (violates(a, nm, st.c + c_, st.s + s_)) hi = mid; else lo = mid + 1;
+        }
+      }
+      const int32_t c31 = __shfl_sync(FULL, qc, 31);
+      const int32_t m31 = __shfl_sync(FULL, qm, 31);
+      const int32_t s31 = __shfl_sync(FULL, qs, 31);
+      if (serve) {
+        if (lo < lim) {
+          nx = (int32_t)(tp + lo);
+          mode = 0;
+        } else if (tp + lim >= e) {
+          nx = kEnd;  // reached the segment end
+          mode = 0;
+        } else {      // (not expected) no violation in a full group: continue serially
+          st.m = m31 > st.m ? m31 : st.m; st.c += c31; st.s += s31;
+          mode = 3;
+          p = tp + 32;
+        }
+      }
+      pend &= ~__ballot_sync(FULL, serve);
     }
     if (mode == 3) {
       const int64_t k = extend_elems(p, e, st, a, slen);
@@ -511,14 +568,20 @@ __global__ void __launch_bounds__(256)
   int64_t rej = 0, pend = 0;
   for (int64_t g = wg; g < G; g += wstride) {
     const int64_t j = (g << 5) + lane;
-    if (j >= a.n) continue;
     // chain node covering j: last node position <= j (nodes ascend and every segment
-    // start is a node, so the node lies in j's segment)
-    int lo = 0, hi = M;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (list[mid] <= j) lo = mid; else hi = mid;
+    // start is a node, so the node lies in j's segment); one binary search per warp
+    int lo0 = 0;
+    if (lane == 0) {
+      int lo = 0, hi = M;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (list[mid] <= (g << 5)) lo = mid; else hi = mid;
+      }
+      lo0 = lo;
     }
+    int lo = __shfl_sync(0xffffffffu, lo0, 0);
+    if (j >= a.n) continue;
+    while (lo + 1 < M && list[lo + 1] <= j) ++lo;
     const int64_t c = list[lo];
     const int32_t b = node_batch[lo];
     const uint32_t m = bmask[g];
