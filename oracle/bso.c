@@ -441,3 +441,93 @@ int bso_window(const int32_t* len, const uint8_t* cls, int64_t n, const int64_t*
   }
   return 0;
 }
+
+/* f3. Global batch emission order: Simulator._next_plan (pd_sim.py:448-462) repeated
+ * while it makes progress.  Each call tries the classes in priority order; for a
+ * class, BatchController.select_bucket (batch_controller.py:106-134) picks the
+ * bucket — class 0 (ONLINE): the one holding the globally oldest request of the
+ * class (:114-123); other classes (OFFLINE): the largest queued token mass of the
+ * class, strict > from 0, so ties go to the lower index (:124-134) — and form_batch
+ * runs on it; the first plan ends the call.  A call that forms no plan but rejects
+ * requests still counts as progress (the simulator marks the set dirty, :457-459).
+ * Generalisation: classes >= 2 use the mass rule of their own class.
+ *
+ * The form_batch calls of one (bucket, class) segment do not depend on the others
+ * (fixed current_safe and pledged), so each call's outcome is read from the drain
+ * of bso_size (the batch starting at the segment's cursor, or the segment's null
+ * tail call); this function restates only the selection loop.  Outputs:
+ * emit_order[t] = batch of the t-th plan; batch_emit[b] = t or -1 (never formed);
+ * req_batch / req_row are rewritten to the dispatch outcome (requests of calls the
+ * loop never reaches stay queued: BS_REQ_PENDING).  Returns the number of plans. */
+int64_t bso_dispatch(const int32_t* len, const int32_t* perm, const int32_t* seg_off,
+                     int64_t n_segs, int64_t n, const bso_params* p, const bso_batch* batches,
+                     int64_t nb, int32_t* req_batch, int32_t* req_row, int32_t* emit_order,
+                     int32_t* batch_emit, bso_summary* sum) {
+  const int64_t C = p->n_classes;
+  int64_t fl = 0;
+  for (int64_t b = 0; b < nb; ++b) batch_emit[b] = -1;
+  int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_segs + 1));
+  int64_t* nextb = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_segs + 1));
+  int32_t* sufmin = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int64_t* pre = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  pre[0] = 0;
+  for (int64_t j = 0; j < n; ++j) pre[j + 1] = pre[j] + eff_len(len[perm[j]], p, &fl);
+  for (int64_t s = 0; s < n_segs; ++s) {
+    cur[s] = seg_off[s];
+    int32_t m = INT32_MAX;
+    for (int64_t j = seg_off[s + 1] - 1; j >= seg_off[s]; --j) {
+      if (perm[j] < m) m = perm[j];
+      sufmin[j] = m;
+    }
+  }
+  for (int64_t s = 0, b = 0; s < n_segs; ++s) { /* first batch of each segment */
+    while (b < nb && batches[b].segment < s) ++b;
+    nextb[s] = b;
+  }
+  const int64_t H = p->current_safe - p->pledged;
+  int64_t t = 0;
+  for (;;) {
+    int formed = 0, progress = 0;
+    for (int64_t c = 0; c < C && !formed; ++c) {
+      int64_t best = -1;
+      if (c == 0) { /* oldest queued request of the class */
+        int32_t best_key = INT32_MAX;
+        for (int64_t s = c; s < n_segs; s += C)
+          if (cur[s] < seg_off[s + 1] && sufmin[cur[s]] < best_key) { best_key = sufmin[cur[s]]; best = s; }
+      } else { /* largest queued token mass, strict > from 0 */
+        int64_t best_mass = 0;
+        for (int64_t s = c; s < n_segs; s += C) {
+          const int64_t mass = pre[seg_off[s + 1]] - pre[cur[s]];
+          if (mass > best_mass) { best_mass = mass; best = s; }
+        }
+      }
+      if (best < 0) continue;
+      if (H <= 0) continue; /* form_batch returns None before touching the queue (:150-152) */
+      const int64_t s = best, end = seg_off[s + 1];
+      const int64_t b = nextb[s];
+      if (b < nb && batches[b].segment == s && batches[b].start == cur[s]) {
+        batch_emit[b] = (int32_t)t;
+        emit_order[t++] = (int32_t)b;
+        cur[s] = batches[b].end;
+        nextb[s] = b + 1;
+        formed = 1;
+      } else { /* the segment's null call: rejects up to the first admissible request */
+        int64_t j = cur[s];
+        while (j < end && req_batch[perm[j]] == REQ_REJECTED) ++j;
+        if (j > cur[s]) progress = 1;
+        cur[s] = j;
+      }
+    }
+    if (!formed && !progress) break;
+  }
+  int64_t nrej = 0, npend = 0;
+  for (int64_t s = 0; s < n_segs; ++s)
+    for (int64_t j = cur[s]; j < seg_off[s + 1]; ++j) { req_batch[perm[j]] = REQ_PENDING; req_row[perm[j]] = -1; }
+  for (int64_t i = 0; i < n; ++i) { nrej += req_batch[i] == REQ_REJECTED; npend += req_batch[i] == REQ_PENDING; }
+  sum->n_rejected = nrej;
+  sum->n_pending = npend;
+  sum->reserved[0] = t; /* n_emitted */
+  sum->flags |= fl;
+  free(cur); free(nextb); free(sufmin); free(pre);
+  return t;
+}

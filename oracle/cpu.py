@@ -194,3 +194,37 @@ def monitor_bins(hist: np.ndarray, l_max: int, bins: int = 64) -> np.ndarray:
     out = np.zeros(bins, np.uint64)
     lib().bso_monitor_bins(_ptr(h), C.byref(p), C.c_int32(bins), _ptr(out))
     return out
+
+
+@dataclass
+class DispatchResult:
+    emit_order: np.ndarray   # batch index of the t-th plan
+    batch_emit: np.ndarray   # t of batch b, or -1
+    req_batch: np.ndarray    # dispatch outcome per request
+    req_row: np.ndarray
+    n_emitted: int
+    n_rejected: int
+    n_pending: int
+
+
+def dispatch(spec: WindowSpec, lens, res: WindowResult) -> DispatchResult:
+    """f3: the simulator's global dispatch sequence over a window result
+    (bso_dispatch; Simulator._next_plan repeated, pd_sim.py:448-462)."""
+    L = lib()
+    L.bso_dispatch.restype = C.c_int64
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    n = len(lens)
+    p = spec.params()
+    nb = len(res.batches)
+    batches = np.ascontiguousarray(res.batches)
+    rb = res.req_batch.copy()
+    rr = res.req_row.copy()
+    emit = np.full(max(nb, 1), -1, np.int32)
+    bemit = np.full(max(nb, 1), -1, np.int32)
+    s = Summary()
+    t = L.bso_dispatch(_ptr(lens), _ptr(res.perm), _ptr(res.seg_off),
+                       C.c_int64(len(res.seg_off) - 1), C.c_int64(n), C.byref(p), _ptr(batches),
+                       C.c_int64(nb), _ptr(rb), _ptr(rr), _ptr(emit), _ptr(bemit), C.byref(s))
+    return DispatchResult(emit_order=emit[:t].copy(), batch_emit=bemit[:nb].copy(), req_batch=rb,
+                          req_row=rr, n_emitted=int(t), n_rejected=int(s.n_rejected),
+                          n_pending=int(s.n_pending))

@@ -104,6 +104,22 @@ def cases():
     out.append(_case("fixed_edges_no_adjust", l[:4000], c[:4000], l_max=4096, n_classes=2,
                      policies=(0, 1), init_edges=(0, 256, 1024, 4096), adjust=False, kvpt=2,
                      current_safe=2 * 20000))
+    # f3 dispatch-order stress: whole buckets of oversize ONLINE requests (null calls
+    # that cascade to OFFLINE inside one _next_plan), equal offline masses (ties to
+    # the lower bucket), and a blocked ONLINE drain under pledged memory
+    ld = rng.integers(1, 4096, size=6000)
+    cd = (rng.random(6000) < 0.3).astype(np.uint8)
+    out.append(_case("dispatch_online_rejects", ld, cd, l_max=4096, n_classes=2, policies=(0, 1),
+                     init_edges=(0, 512, 1024, 2048, 3072, 4096), adjust=False, kvpt=2,
+                     current_safe=2 * 1800))
+    lt = np.repeat(np.array([100, 700, 1500, 2500], np.int32), 50)
+    ct = np.ones(len(lt), np.uint8)
+    ct[::7] = 0
+    out.append(_case("dispatch_mass_ties", lt, ct, l_max=4096, n_classes=2, policies=(0, 2),
+                     init_edges=(0, 512, 1024, 2048, 4096), adjust=False, kvpt=2,
+                     current_safe=2 * 2600, accounting=1))
+    out.append(_case("dispatch_pledged_block", ld[:2500], cd[:2500], l_max=4096, n_classes=2,
+                     policies=(0, 1), kvpt=2, current_safe=2 * 4000, pledged=2 * 1200 + 1))
     return out
 
 
@@ -113,7 +129,8 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     for name, lens, cls, spec in cases():
         spec = dict(spec)
-        ref = reference_window(lens, cls, **spec)
+        # the simulator's global dispatch sequence (f3) where the reference defines it
+        ref = reference_window(lens, cls, dispatch=spec.get("n_classes", 2) == 2, **spec)
         init = spec.get("init_edges")
         np.savez_compressed(
             os.path.join(OUT, f"{name}.npz"), lens=lens, cls=cls,

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import os
 import sys
+import copy
 from collections import deque
 
 import numpy as np
@@ -52,7 +53,8 @@ class _Cls:
 
 def reference_window(lens, cls, *, l_max, n_classes=2, policies=(0, 1), theta=0.5,
                      adjust=True, max_passes=0, init_edges=None, model=None, gpu=None,
-                     kvpt=None, current_safe=None, accounting=0, pledged=0, truncate=True):
+                     kvpt=None, current_safe=None, accounting=0, pledged=0, truncate=True,
+                     dispatch=False):
     """Returns a dict of numpy arrays describing the reference's window result.
 
     Memory can be given as (model, gpu) reference objects, or as raw
@@ -106,6 +108,14 @@ def reference_window(lens, cls, *, l_max, n_classes=2, policies=(0, 1), theta=0.
         for r in b.requests:
             bucket_of[r.id] = bi
 
+    dispatch_bs = dispatch_ctl = None
+    if dispatch:
+        # the simulator's dispatch loop runs on its own copy of the adjusted buckets
+        dispatch_bs = copy.deepcopy(bs)
+        dispatch_ctl = bc.BatchController(model, gpu, acc)
+        if current_safe is not None and current_safe != dispatch_ctl.current_safe:
+            dispatch_ctl.on_memory_change(current_safe)
+
     kind_code = {"split": 1, "merge": 2, "skip": 3}
     ch_arr = np.array([[kind_code[c.kind], c.parent_low, c.parent_up,
                         -1 if c.midpoint is None else c.midpoint] for c in changes],
@@ -128,7 +138,13 @@ def reference_window(lens, cls, *, l_max, n_classes=2, policies=(0, 1), theta=0.
                     waste.append(np.nan)
     rejected = [rej.request.id for rej in ctl.rejections]
     pending = sorted(r.id for r in bs.iter_requests())
+    if dispatch_bs is not None:
+        extra = _dispatch_loop(dispatch_bs, dispatch_ctl, class_objs, pol_map, policies, pledged,
+                               TaskClass)
+    else:
+        extra = {}
     return dict(
+        **extra,
         n_max=np.int64(n_max), edges=np.array(edges, np.int64), changes=ch_arr,
         n_passes=np.int64(passes), bucket=bucket_of,
         batch_ids=np.array(batch_ids, np.int64), batch_off=np.array(batch_off, np.int64),
@@ -137,3 +153,36 @@ def reference_window(lens, cls, *, l_max, n_classes=2, policies=(0, 1), theta=0.
         rejected=np.array(rejected, np.int64), pending=np.array(pending, np.int64),
         current_safe=np.int64(ctl.current_safe), kvpt=np.int64(ctl.kv_per_token),
     )
+
+
+def _dispatch_loop(bs, ctl, class_objs, pol_map, policies, pledged, TaskClass):
+    """Simulator._next_plan (pd_sim.py:448-462) repeated while it makes progress:
+    for each class in priority order, select_bucket (batch_controller.py:106-134)
+    then form_batch on that bucket; the first plan ends the call.  Progress = a plan
+    or new rejections (the simulator marks the set dirty and would call again,
+    pd_sim.py:457-459).  Two classes only: select_bucket knows ONLINE / OFFLINE."""
+    assert len(class_objs) == 2, "the reference's select_bucket has two classes"
+    seq, off, rejected = [], [0], []
+    while True:
+        plan, progressed = None, False
+        for ci, cobj in enumerate(class_objs):
+            idx = ctl.select_bucket(bs, cobj)
+            if idx is None:
+                continue
+            plan = ctl.form_batch(bs.buckets[idx], pol_map[policies[ci]], pledged=pledged,
+                                  task_class=cobj)
+            if ctl.rejections:
+                progressed = True
+                rejected.extend(rej.request.id for rej in ctl.rejections)
+                ctl.rejections.clear()
+            if plan is not None:
+                break
+        if plan is not None:
+            seq.extend(plan.request_ids)
+            off.append(len(seq))
+            continue
+        if not progressed:
+            break
+    return dict(disp_ids=np.array(seq, np.int64), disp_off=np.array(off, np.int64),
+                disp_rejected=np.array(sorted(rejected), np.int64),
+                disp_pending=np.array(sorted(r.id for r in bs.iter_requests()), np.int64))
