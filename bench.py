@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the window kernels "
                     "individually instead of replaying one CUDA graph per window")
     ap.add_argument("--cpu-sample", type=int, default=131_072)
+    ap.add_argument("--dispatch", action="store_true", help="also compute the simulator's "
+                    "global dispatch order (K7, SURVEY f3) inside every window")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -228,7 +230,7 @@ def main():
                             policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
                             buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
                             current_safe=cfg.current_safe, accounting=cfg.accounting,
-                            device=dev, process_group=pg)
+                            device=dev, process_group=pg, dispatch=args.dispatch)
     # first window sizes the reusable packed-output buffer
     l_a = sched.ctx.launches
     res = sched.schedule(lens, cls, tok_off, tokens)

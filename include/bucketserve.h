@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BS_ABI_VERSION 1
+#define BS_ABI_VERSION 2
 
 /* ---- status codes (mapped by the Python shim to the reference exceptions) -- */
 #define BS_OK                 0
@@ -62,6 +62,7 @@ extern "C" {
 #define BS_FLAG_NONPOS_LEN    0x20 /* a batch holds a length < 1: waste_ratio raises, memory_model.py:96  */
 #define BS_FLAG_BATCH_CAP     0x40 /* more batches than batches_cap                                       */
 #define BS_FLAG_BAD_EDGES     0x80 /* init_edges not strictly increasing from 0 to l_max: ValueError      */
+#define BS_FLAG_DISPATCH_RANGE 0x100 /* dispatch keys out of range (token mass >= 2^43 or > 2^17 buckets) */
 
 /* ---- enums ------------------------------------------------------------------ */
 /* Dispatch order inside one (bucket, class) segment, batch_controller.py:33-41.
@@ -95,7 +96,8 @@ typedef struct bs_window_params {
   int32_t accounting;        /* bs_accounting                                              */
   int32_t truncate;          /* 1: len >= l_max -> l_max-1 (pd_sim.py:382-383); 0: flag    */
   int32_t pad_id;            /* token id written into padding                              */
-  int32_t reserved;
+  int32_t dispatch;          /* 1: also compute the simulator's global dispatch order (f3,
+                                bs_dispatch) inside bs_window_schedule / _from_hist        */
 } bs_window_params;
 
 /* ---- one batch descriptor (device memory), BatchPlan, batch_controller.py:44-56 */
@@ -132,7 +134,8 @@ typedef struct bs_summary {
   double  waste_sum;      /* sum of per-batch waste_ratio                             */
   int64_t sort_passes;    /* radix passes run by K4                                   */
   int64_t flags;          /* BS_FLAG_* bits                                           */
-  int64_t reserved[15];
+  int64_t n_dispatched;   /* plans in the dispatch sequence (bs_dispatch; else 0)     */
+  int64_t reserved[14];
 } bs_summary;             /* 256 bytes */
 
 typedef struct bs_ctx bs_ctx;
@@ -214,6 +217,24 @@ int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int64_t*
             int64_t batch_begin, int64_t batch_end, int32_t* out_tokens, uint8_t* out_mask,
             int64_t out_capacity, bs_summary* summary, void* stream);
 
+/* ---- K7: dispatch order ----------------------------------------
+ * The order in which the simulator would hand the window's batches to prefill:
+ * Simulator._next_plan (pd_sim.py:448-462) repeated while it makes progress — per
+ * call, classes in priority order, BatchController.select_bucket
+ * (batch_controller.py:106-134: class 0 the bucket holding the oldest queued request
+ * of the class, other classes the largest queued token mass of the class, ties to the
+ * lower bucket, zero mass never) then form_batch on it; the first plan ends the call.
+ * emit_order[t] = batch of the t-th plan (t < summary->n_dispatched); batch_emit[b] =
+ * t, or -1 for a batch the loop never forms (its bucket is never selected again: a
+ * blocked drain under pledged memory, or zero token mass).  Requests of calls the
+ * loop never reaches are rewritten to BS_REQ_PENDING in req_batch / req_row and the
+ * summary's n_rejected / n_pending follow.  Uses the drain of the last bs_size call
+ * on ctx (same perm / seg_off / batches). */
+int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_t n,
+                const bs_window_params* p, const bs_batch* batches, int32_t batches_cap,
+                int32_t* req_batch, int32_t* req_row, int32_t* emit_order, int32_t* batch_emit,
+                bs_summary* summary, void* stream);
+
 /* ---- fused window ------------------------------------------------------------------
  * K1..K6 in one call on one stream (single-GPU window).  For a sharded window
  * call bs_histogram, all-reduce the histogram across ranks, then
@@ -245,6 +266,8 @@ typedef struct bs_window_io {
   int32_t*       out_tokens;  /* [out_capacity]                */
   uint8_t*       out_mask;    /* [out_capacity]                */
   bs_summary*    summary;     /* required */
+  int32_t*       emit_order;  /* [batches_cap] dispatch sequence (p->dispatch)  */
+  int32_t*       batch_emit;  /* [batches_cap] rank in it or -1 (p->dispatch)   */
 } bs_window_io;
 
 int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p, void* stream);
@@ -265,8 +288,9 @@ int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p
  * sets (0 disarms); bs_profile_read synchronises the recorded events, writes the
  * summed milliseconds per stage (BS_STAGES floats) and the number of recorded
  * steps, and resets the ring.  bs_launch_count: kernels launched by ctx so far. */
-#define BS_STAGES 9   /* 0 histogram, 1 boundaries, 2 order, 3 size.prep, 4 size.next,
-                         5 size.chain, 6 size.describe(+offsets), 7 size.outcome, 8 pack */
+#define BS_STAGES 10  /* 0 histogram, 1 boundaries, 2 order, 3 size.prep, 4 size.next,
+                         5 size.chain, 6 size.describe(+offsets), 7 size.outcome,
+                         8 dispatch (when p->dispatch), 9 pack */
 int bs_profile_enable(bs_ctx* ctx, int32_t max_steps);
 int bs_profile_read(bs_ctx* ctx, float* stage_ms, int32_t* steps_out);
 int64_t bs_launch_count(const bs_ctx* ctx);

@@ -32,6 +32,7 @@ FLAG_PACK_CAPACITY = 0x10
 FLAG_NONPOS_LEN = 0x20
 FLAG_BATCH_CAP = 0x40
 FLAG_BAD_EDGES = 0x80
+FLAG_DISPATCH_RANGE = 0x100
 
 POLICY_FCFS, POLICY_SJF, POLICY_LJF = 0, 1, 2
 ACCOUNTING_PADDED, ACCOUNTING_EXACT = 0, 1
@@ -43,9 +44,9 @@ PACK_ALIGN = 4
 EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "bs_destroy",
            "bs_histogram", "bs_boundaries", "bs_assign", "bs_order", "bs_size", "bs_pack",
            "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_profile_enable",
-           "bs_profile_read", "bs_launch_count")
+           "bs_profile_read", "bs_launch_count", "bs_dispatch")
 STAGES = ("histogram", "boundaries", "order", "size.prep", "size.next", "size.chain",
-          "size.describe", "size.outcome", "pack")
+          "size.describe", "size.outcome", "dispatch", "pack")
 
 
 class NativeUnavailable(RuntimeError):
@@ -57,7 +58,7 @@ class WindowParams(C.Structure):
                 ("split_threshold", C.c_double), ("adjust", C.c_int32), ("max_passes", C.c_int32),
                 ("n_max", C.c_int64), ("kv_bytes_per_token", C.c_int64),
                 ("current_safe", C.c_int64), ("pledged", C.c_int64), ("accounting", C.c_int32),
-                ("truncate", C.c_int32), ("pad_id", C.c_int32), ("reserved", C.c_int32)]
+                ("truncate", C.c_int32), ("pad_id", C.c_int32), ("dispatch", C.c_int32)]
 
 
 class WindowIO(C.Structure):
@@ -68,7 +69,8 @@ class WindowIO(C.Structure):
                 ("hist_global", C.c_void_p), ("edges", C.c_void_p), ("changes", C.c_void_p),
                 ("bucket", C.c_void_p), ("perm", C.c_void_p), ("seg_off", C.c_void_p),
                 ("batches", C.c_void_p), ("req_batch", C.c_void_p), ("req_row", C.c_void_p),
-                ("out_tokens", C.c_void_p), ("out_mask", C.c_void_p), ("summary", C.c_void_p)]
+                ("out_tokens", C.c_void_p), ("out_mask", C.c_void_p), ("summary", C.c_void_p),
+                ("emit_order", C.c_void_p), ("batch_emit", C.c_void_p)]
 
 
 BATCH_DTYPE = np.dtype([("segment", "<i4"), ("start", "<i4"), ("end", "<i4"), ("n", "<i4"),
@@ -78,9 +80,9 @@ BATCH_DTYPE = np.dtype([("segment", "<i4"), ("start", "<i4"), ("end", "<i4"), ("
 SUMMARY_FIELDS = ("n_requests", "total_global", "sum_len_global", "n_max", "k_buckets",
                   "n_changes", "n_passes", "n_batches", "n_rejected", "n_pending",
                   "admitted_tokens", "padded_tokens", "packed_elems", "peak_footprint",
-                  "waste_sum", "sort_passes", "flags")
+                  "waste_sum", "sort_passes", "flags", "n_dispatched")
 SUMMARY_DTYPE = np.dtype([(f, "<f8" if f == "waste_sum" else "<i8") for f in SUMMARY_FIELDS] +
-                         [("reserved", "<i8", (15,))])
+                         [("reserved", "<i8", (14,))])
 assert BATCH_DTYPE.itemsize == 64 and SUMMARY_DTYPE.itemsize == 256
 
 _lib = None
@@ -120,6 +122,7 @@ def load():
         "bs_profile_enable": (C.c_int, [vp, i32]),
         "bs_profile_read": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(i32)]),
         "bs_launch_count": (i64, [vp]),
+        "bs_dispatch": (C.c_int, [vp, vp, vp, i64, P, vp, i32, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -157,10 +160,13 @@ def raise_for_flags(flags: int, l_max: int | None = None):
         raise SimulationError("batch descriptor capacity exceeded")
     if flags & FLAG_PACK_CAPACITY:
         raise ValueError("packed output buffer too small")
+    if flags & FLAG_DISPATCH_RANGE:
+        raise ValueError("dispatch order: queued token mass or bucket count out of range")
 
 
 def make_params(*, l_max, n_classes, policies, split_threshold, adjust, max_passes, n_max,
-                kv_bytes_per_token, current_safe, pledged, accounting, truncate, pad_id):
+                kv_bytes_per_token, current_safe, pledged, accounting, truncate, pad_id,
+                dispatch=False):
     p = WindowParams()
     p.l_max, p.n_classes = int(l_max), int(n_classes)
     for i, v in enumerate(policies):
@@ -171,6 +177,7 @@ def make_params(*, l_max, n_classes, policies, split_threshold, adjust, max_pass
     p.kv_bytes_per_token = int(kv_bytes_per_token)
     p.current_safe, p.pledged = int(current_safe), int(pledged)
     p.accounting, p.truncate, p.pad_id = int(accounting), int(bool(truncate)), int(pad_id)
+    p.dispatch = int(bool(dispatch))
     return p
 
 

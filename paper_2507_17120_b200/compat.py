@@ -349,12 +349,18 @@ def schedule_requests(requests: Sequence[Request], model: ModelConfig, gpu: GpuC
                       offline_policy: DispatchPolicy = DispatchPolicy.SJF,
                       split_threshold: float = 0.5, buckets: Sequence[int] | None = None,
                       adjust: bool = True, pledged: int = 0, truncate: bool = True,
-                      now: float = 0.0, tok_off=None, tokens=None) -> WindowSchedule:
+                      now: float = 0.0, tok_off=None, tokens=None,
+                      dispatch: bool = False) -> WindowSchedule:
     """The reference window composition on the GPU: assign every request,
     adjust_buckets(current_n_max) to the fixpoint, then for every bucket and class
     (ONLINE first) drain form_batch.  Requests may come in any order; the arrival
     rank is (arrival_time, id) as in order_requests.  Over-long inputs are scheduled
-    at max_seq_len - 1 (pd_sim.py:382-383) without mutating the caller's objects."""
+    at max_seq_len - 1 (pd_sim.py:382-383) without mutating the caller's objects.
+
+    dispatch=True returns the plans in the order the simulator would start them
+    instead — Simulator._next_plan repeated while it makes progress (pd_sim.py:448-462,
+    select_bucket batch_controller.py:106-134) — computed by the K7 kernels; requests
+    the loop never reaches stay pending."""
     L = model.max_seq_len
     reqs = sorted(requests, key=_ARRIVAL_ORDER)
     classes = [TaskClass.ONLINE, TaskClass.OFFLINE]
@@ -366,7 +372,7 @@ def schedule_requests(requests: Sequence[Request], model: ModelConfig, gpu: GpuC
                        buckets=None if buckets is None else tuple(buckets),
                        kv_bytes_per_token=model.kv_bytes_per_token,
                        current_safe=safe_memory(gpu), pledged=pledged,
-                       accounting=accounting, truncate=truncate)
+                       accounting=accounting, truncate=truncate, dispatch=dispatch)
     res = sched.schedule(lens, cls, tok_off, tokens)
     h = res.to_host()
     edges = [int(e) for e in h["edges"]]
@@ -383,10 +389,12 @@ def schedule_requests(requests: Sequence[Request], model: ModelConfig, gpu: GpuC
             rejections.append(OversizeRejection(reqs[i], model.kv_bytes_per_token * reqs[i].input_len,
                                                 safe))
     C = 2
-    for k, x in enumerate(b):
+    order = h["emit_order"] if dispatch else range(len(b))
+    for k in order:
+        x = b[int(k)]
         bk = int(x["segment"]) // C
-        plans.append(BatchPlan(request_ids=tuple(r.id for r in members[k]),
-                               requests=tuple(members[k]), max_input_len=int(x["max_input_len"]),
+        plans.append(BatchPlan(request_ids=tuple(r.id for r in members[int(k)]),
+                               requests=tuple(members[int(k)]), max_input_len=int(x["max_input_len"]),
                                token_sum=int(x["token_sum"]), footprint=int(x["footprint"]),
                                created_at=now, source_bucket=(edges[bk], edges[bk + 1])))
     bs = BucketSet(L, split_threshold,

@@ -10,7 +10,8 @@
 
 #include "ctx.cuh"
 
-void* bs_chain_kernel_ptr();  // k_size.cu
+void* bs_chain_kernel_ptr();     // k_size.cu
+void* bs_dispatch_kernel_ptr();  // k_dispatch.cu
 
 namespace {
 
@@ -78,6 +79,8 @@ void free_all(bs_ctx* c) {
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
                   c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
                   c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->task_base, c->segw,
+                  c->disp_cseg, c->disp_cmin, c->disp_csum, c->disp_keys0, c->disp_keys1,
+                  c->disp_vals0, c->disp_vals1, c->disp_hist8, c->disp_agg, c->disp_status, c->disp_tctr, c->disp_nulls, c->disp_runs, c->disp_misc,
                   c->misc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -173,6 +176,18 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(rowpos, N + 1);
   A(task_base, N + 2);
   A(misc, 128);
+  // K7 dispatch order
+  A(disp_cseg, N + 1); A(disp_cmin, N + 1); A(disp_csum, N + 1);
+  A(disp_keys0, N + 1); A(disp_keys1, N + 1); A(disp_vals0, N + 1); A(disp_vals1, N + 1);
+  A(disp_hist8, 8 * 256);
+  A(disp_status, 8 * ((N + 7167) / 7168 * 256 + 256)); A(disp_tctr, 8);
+  A(disp_nulls, L * C + 1); A(disp_runs, 4 * (2 * L * C + 32)); A(disp_misc, 32);
+  if ((e = cudaMemset(ctx->disp_hist8, 0, sizeof(uint32_t) * 8 * 256)) != cudaSuccess) {
+    int rc = cuda_fail(ctx, e, "cudaMemset disp_hist8");
+    free_all(ctx);
+    delete ctx;
+    return rc;
+  }
   // co-resident blocks for the cooperative chain kernel (512 threads)
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(), 512, 0);
@@ -185,6 +200,23 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   }
   ctx->chain_blocks = per_sm * ctx->num_sms;
   A(btot, ctx->chain_blocks);
+  // the cooperative K7 dispatch kernel: one 1024-thread CTA per SM, ~211 KB of shared memory
+  e = cudaFuncSetAttribute(bs_dispatch_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           bsk::dispatch_smem_bytes());
+  per_sm = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_dispatch_kernel_ptr(),
+                                                      bsk::dispatch_threads(),
+                                                      bsk::dispatch_smem_bytes());
+  if (e != cudaSuccess || per_sm < 1) {
+    int rc = e != cudaSuccess ? cuda_fail(ctx, e, "occupancy(k_dispatch)")
+                              : fail(ctx, BS_ERR_NOT_BUILT, "k_dispatch cannot be resident");
+    free_all(ctx);
+    delete ctx;
+    return rc;
+  }
+  ctx->disp_blocks = per_sm * ctx->num_sms;
+  A(disp_agg, 2 * ctx->disp_blocks);
 #undef A
   *out = ctx;
   return BS_OK;
@@ -315,6 +347,23 @@ int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int64_t*
   return BS_OK;
 }
 
+int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_t n,
+                const bs_window_params* p, const bs_batch* batches, int32_t batches_cap,
+                int32_t* req_batch, int32_t* req_row, int32_t* emit_order, int32_t* batch_emit,
+                bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK || (rc = check_n(ctx, n)) != BS_OK) return rc;
+  if (!summary || !batches || batches_cap < 0 || !emit_order || !batch_emit ||
+      (n > 0 && (!perm || !seg_off || !req_batch || !req_row)))
+    return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_dispatch(ctx, perm, seg_off, n, *p, batches, batches_cap, req_batch, req_row,
+                               emit_order, batch_emit, summary, static_cast<cudaStream_t>(stream)),
+          "k_dispatch");
+  return BS_OK;
+}
+
 static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
                                  cudaStream_t st) {
   int rc;
@@ -330,6 +379,15 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                            io->batches_cap, io->req_batch, io->req_row, io->summary, st),
           "k_size");
   bsk::prof_mark(ctx, 8, st);
+  if (p->dispatch) {
+    if (!io->emit_order || !io->batch_emit)
+      return fail(ctx, BS_ERR_INVALID_ARG, "dispatch needs emit_order and batch_emit");
+    BS_CUDA(bsk::launch_dispatch(ctx, io->perm, io->seg_off, io->n, *p, io->batches,
+                                 io->batches_cap, io->req_batch, io->req_row, io->emit_order,
+                                 io->batch_emit, io->summary, st),
+            "k_dispatch");
+  }
+  bsk::prof_mark(ctx, 9, st);
   if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
     if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
       return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
@@ -340,7 +398,7 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                              io->out_capacity, io->summary, st),
             "k_pack");
   }
-  bsk::prof_mark(ctx, 9, st);
+  bsk::prof_mark(ctx, 10, st);
   return BS_OK;
 }
 
@@ -448,4 +506,4 @@ int64_t bs_launch_count(const bs_ctx* ctx) { return ctx ? ctx->launches : 0; }
 static_assert(sizeof(bs_window_params) == 104, "bs_window_params layout (Python binding)");
 static_assert(sizeof(bs_batch) == 64, "bs_batch layout");
 static_assert(sizeof(bs_summary) == 256, "bs_summary layout");
-static_assert(sizeof(bs_window_io) == 176, "bs_window_io layout");
+static_assert(sizeof(bs_window_io) == 192, "bs_window_io layout");

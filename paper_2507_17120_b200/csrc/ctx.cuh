@@ -63,6 +63,20 @@ struct bs_ctx {
   int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)
   int32_t* listB = nullptr;
   int32_t* node_batch = nullptr; // [max_n + 1] batch id of each chain node (-1: empty tail)
+  // K7 dispatch order (f3)
+  int disp_blocks = 0;           // co-resident CTAs of the cooperative K7 kernel
+  int32_t* disp_cseg = nullptr;  // [max_n+1] segment of each call
+  int32_t* disp_cmin = nullptr;  // [max_n+1] min arrival rank over the call's range
+  int64_t* disp_csum = nullptr;  // [max_n+1] length sum over the call's range
+  uint64_t *disp_keys0 = nullptr, *disp_keys1 = nullptr;  // [max_n+1] sort keys (ping-pong)
+  uint32_t *disp_vals0 = nullptr, *disp_vals1 = nullptr;  // [max_n+1] call ids
+  uint32_t* disp_hist8 = nullptr;    // [8][256] key-byte histograms (zero between windows)
+  int64_t* disp_agg = nullptr;       // [2*disp_blocks] chunk aggregates of the key scan
+  uint32_t* disp_status = nullptr;   // [8][max_n/7168+2][256] look-back words
+  uint32_t* disp_tctr = nullptr;     // [8] tile counters
+  int32_t* disp_nulls = nullptr;     // [l_cap*c_max+1] sorted positions of null calls
+  int32_t* disp_runs = nullptr;      // [2*l_cap*c_max+32][4] runs of consecutive plans
+  int64_t* disp_misc = nullptr;      // [32]
   int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
                                  //        [66] n_batches, [67] pack rows cursor
 };
@@ -109,6 +123,13 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const bs_batch* batches, int64_t batch_begin, int64_t batch_end,
                         int32_t batches_cap, int32_t* out_tokens, uint8_t* out_mask,
                         int64_t out_capacity, bs_summary* summary, cudaStream_t st);
+cudaError_t launch_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_t n,
+                            const bs_window_params& p, const bs_batch* batches,
+                            int32_t batches_cap, int32_t* req_batch, int32_t* req_row,
+                            int32_t* emit_order, int32_t* batch_emit, bs_summary* summary,
+                            cudaStream_t st);
+int dispatch_smem_bytes();
+int dispatch_threads();
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);

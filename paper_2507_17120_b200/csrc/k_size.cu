@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(512)
             int32_t* listA, int32_t* listB, int32_t* node_batch, int32_t* node_j0, int32_t* misc,
             const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
             const int32_t* __restrict__ bcnt, int32_t* __restrict__ Rg, int32_t* btot,
-            int32_t* segw, int32_t batches_cap, bs_summary* sum) {
+            int32_t* segw, int32_t batches_cap, bs_summary* sum, int32_t* dseg, int32_t* dmin,
+            int64_t* dsum) {
   cg::grid_group grid = cg::this_grid();
   __shared__ ChainShared sh;
   const int64_t n = a.n;
@@ -467,6 +468,11 @@ __global__ void __launch_bounds__(512)
     const bool tail_empty = (k == ld_rel_i32(seg_len + lo) - 1) && ld_rel_i32(seg_empty + lo);
     node_batch[i] = tail_empty ? -1 : (int32_t)(i - ld_rel_i32(seg_ebase + lo));
     node_j0[i] = tail_empty ? ld_rel_i32(seg_tailj0 + lo) : (int32_t)pos;
+    if (dseg) {  // K7 per-call accumulators (filled by K5e)
+      dseg[i] = lo;
+      dmin[i] = INT32_MAX;
+      dsum[i] = 0;
+    }
   }
 }
 
@@ -558,7 +564,9 @@ __global__ void __launch_bounds__(256)
                    const int32_t* __restrict__ node_j0, const int32_t* __restrict__ misc,
                    const bs_batch* __restrict__ batches, int32_t batches_cap,
                    int32_t* __restrict__ req_batch, int32_t* __restrict__ req_row,
-                   int32_t* __restrict__ rowpos, bs_summary* sum) {
+                   int32_t* __restrict__ rowpos, bs_summary* sum,
+                   const int32_t* __restrict__ slen, int32_t* __restrict__ dmin,
+                   int64_t* __restrict__ dsum) {
   const int M = misc[64];
   const int32_t* list = misc[68] ? listB : listA;
   const int lane = threadIdx.x & 31;
@@ -580,8 +588,23 @@ __global__ void __launch_bounds__(256)
       lo0 = lo;
     }
     int lo = __shfl_sync(0xffffffffu, lo0, 0);
-    if (j >= a.n) continue;
-    while (lo + 1 < M && list[lo + 1] <= j) ++lo;
+    const bool in = j < a.n;
+    if (in)
+      while (lo + 1 < M && list[lo + 1] <= j) ++lo;
+    if (dmin) {
+      // K7 per-call accumulators: min arrival rank and length sum over the call's range
+      // (lanes of one call are contiguous: one atomic per call and warp)
+      const unsigned peers = __match_any_sync(0xffffffffu, in ? lo : -1);
+      const unsigned pr = in ? (unsigned)perm[j] : 0xffffffffu;
+      const unsigned ln = in ? (unsigned)slen[j] : 0u;
+      const unsigned mn = __reduce_min_sync(peers, pr);
+      const unsigned sm = __reduce_add_sync(peers, ln);
+      if (in && lane == __ffs(peers) - 1) {
+        atomicMin(dmin + lo, (int)mn);
+        atomicAdd(reinterpret_cast<unsigned long long*>(dsum + lo), (unsigned long long)sm);
+      }
+    }
+    if (!in) continue;
     const int64_t c = list[lo];
     const int32_t b = node_batch[lo];
     const uint32_t m = bmask[g];
@@ -737,9 +760,12 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     int32_t* sw = ctx->segw;
     int32_t bcap = batches_cap;
     bs_summary* sm = summary;
+    int32_t* dseg = p.dispatch ? ctx->disp_cseg : nullptr;
+    int32_t* dmin = p.dispatch ? ctx->disp_cmin : nullptr;
+    int64_t* dsum = p.dispatch ? ctx->disp_csum : nullptr;
     void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
                     &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
-                    (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm};
+                    (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
     e = cudaLaunchCooperativeKernel((void*)k_chain, dim3(ctx->chain_blocks), dim3(512), args, 0,
                                     st);
     if (e != cudaSuccess) return e;
@@ -755,7 +781,9 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   prof_mark(ctx, 7, st);
   k_size_outcome<<<wblocks, 256, 0, st>>>(a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB,
                                           ctx->node_batch, ctx->node_j0, misc, batches,
-                                          batches_cap, req_batch, req_row, ctx->rowpos, summary);
+                                          batches_cap, req_batch, req_row, ctx->rowpos, summary,
+                                          ctx->sorted_len, p.dispatch ? ctx->disp_cmin : nullptr,
+                                          p.dispatch ? ctx->disp_csum : nullptr);
   ctx->launches += 6;
   return cudaGetLastError();
 }

@@ -63,6 +63,7 @@ class WindowConfig:
     accounting: MemoryAccounting = MemoryAccounting.PADDED
     truncate: bool = True
     pad_id: int = 0
+    dispatch: bool = False
 
     def params(self) -> N.WindowParams:
         if len(self.policies) != self.n_classes:
@@ -78,7 +79,7 @@ class WindowConfig:
             n_max=self.n_max, kv_bytes_per_token=self.kv_bytes_per_token,
             current_safe=self.current_safe, pledged=self.pledged,
             accounting=accounting_code(self.accounting), truncate=self.truncate,
-            pad_id=self.pad_id)
+            pad_id=self.pad_id, dispatch=self.dispatch)
 
 
 class WindowResult:
@@ -161,6 +162,20 @@ class WindowResult:
         raw = self._s.batches_raw[:nb * 64].cpu().numpy()
         return raw.view(N.BATCH_DTYPE).copy()
 
+    def emit_order(self) -> np.ndarray:
+        """f3: batch indices in the simulator's dispatch order (Simulator._next_plan
+        repeated, pd_sim.py:448-462); needs dispatch=True."""
+        if not self._s.cfg.dispatch:
+            raise ValueError("the scheduler was built without dispatch=True")
+        t = min(self.summary()["n_dispatched"], self._s.batches_cap)
+        return self._s.emit_order[:t].cpu().numpy()
+
+    def batch_emit(self) -> np.ndarray:
+        """f3: dispatch rank of every batch, -1 for batches the loop never forms."""
+        if not self._s.cfg.dispatch:
+            raise ValueError("the scheduler was built without dispatch=True")
+        return self._s.batch_emit[:self.n_batches].cpu().numpy()
+
     def mean_batch_waste(self):
         """pd_sim.py:898-899: mean of per-batch waste_ratio in emission order."""
         b = self.batches()
@@ -184,6 +199,9 @@ class WindowResult:
                    perm=self.perm.cpu().numpy(), bucket=self.bucket.cpu().numpy(),
                    req_batch=self.req_batch.cpu().numpy(), req_row=self.req_row.cpu().numpy(),
                    hist=self.hist.cpu().numpy().view(np.uint32))
+        if self._s.cfg.dispatch:
+            out["emit_order"] = self.emit_order()
+            out["batch_emit"] = self.batch_emit()
         if self.packed:
             m = int(s["packed_elems"])
             out["out_tokens"] = self._s.out_tokens[:m].cpu().numpy()
@@ -209,7 +227,7 @@ class WindowScheduler:
                  current_safe: int | None = None, n_max: int | None = None, device=None,
                  pack_capacity: int | None = None, with_mask: bool = True,
                  changes_cap: int | None = None, batches_cap: int | None = None,
-                 process_group=None):
+                 process_group=None, dispatch: bool = False):
         if not torch.cuda.is_available():
             raise N.NativeUnavailable("no CUDA device: the window scheduler runs only on a B200")
         if max_seq_len is None:
@@ -230,7 +248,8 @@ class WindowScheduler:
                                 policies=tuple(policies), split_threshold=split_threshold,
                                 adjust=adjust, max_passes=max_passes, n_max=n_max,
                                 kv_bytes_per_token=kvpt, current_safe=safe, pledged=pledged,
-                                accounting=accounting, truncate=truncate, pad_id=pad_id)
+                                accounting=accounting, truncate=truncate, pad_id=pad_id,
+                                dispatch=dispatch)
         self._params = self.cfg.params()
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    torch.device(device).index or 0)
@@ -253,6 +272,8 @@ class WindowScheduler:
         self.req_batch = torch.zeros(max(Nmax, 1), **i32)
         self.req_row = torch.zeros(max(Nmax, 1), **i32)
         self.summary = torch.zeros(256, dtype=torch.uint8, device=dev)
+        self.emit_order = torch.zeros(self.batches_cap, **i32) if dispatch else None
+        self.batch_emit = torch.zeros(self.batches_cap, **i32) if dispatch else None
         self.init_edges = None
         self.k_init = 0
         if buckets is not None:
@@ -297,6 +318,8 @@ class WindowScheduler:
         io.out_tokens = _ptr(self.out_tokens) if pack else None
         io.out_mask = _ptr(self.out_mask) if (pack and self.out_mask is not None) else None
         io.summary = _ptr(self.summary)
+        io.emit_order = _ptr(self.emit_order)
+        io.batch_emit = _ptr(self.batch_emit)
         return io
 
     def _inputs(self, lengths, classes):

@@ -33,20 +33,23 @@ def test_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert N.load().bs_abi_version() == 1
+    assert N.load().bs_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
     assert C.sizeof(N.WindowParams) == 104
+    assert C.sizeof(N.WindowIO) == 192
     assert N.BATCH_DTYPE.itemsize == 64
     assert N.SUMMARY_DTYPE.itemsize == 256
     src = open(HEADER).read()
     for f in ("l_max", "n_classes", "policy", "split_threshold", "adjust", "max_passes", "n_max",
-              "kv_bytes_per_token", "current_safe", "pledged", "accounting", "truncate", "pad_id"):
+              "kv_bytes_per_token", "current_safe", "pledged", "accounting", "truncate", "pad_id", "dispatch"):
         assert re.search(rf"\b{f}\b", src), f
     for f in N.BATCH_DTYPE.names:
         assert re.search(rf"\b{f}\b", src), f
     for f in N.SUMMARY_FIELDS:
+        assert re.search(rf"\b{f}\b", src), f
+    for f, _ in N.WindowIO._fields_:
         assert re.search(rf"\b{f}\b", src), f
 
 

@@ -147,8 +147,11 @@ def test_form_batch_matches_max_safe_batch_oracle():
 # ---- whole window from reference objects --------------------------------------------
 @pytest.mark.parametrize("name", [n for n in fixture_names()
                                   if not n.startswith(("four_class", "one_pass"))])
-def test_schedule_requests_matches_reference_fixture(name):
+@pytest.mark.parametrize("dispatch", [False, True])
+def test_schedule_requests_matches_reference_fixture(name, dispatch):
     spec, lens, cls, ref = load(name)
+    if dispatch and "disp_ids" not in ref:
+        pytest.skip("no reference dispatch sequence for this fixture")
     if spec["n_classes"] != 2 or spec["policies"][0] != 0:
         pytest.skip("schedule_requests drives ONLINE=EARLIEST_ARRIVAL / OFFLINE=policy")
     if spec["kvpt"] % 2:
@@ -164,10 +167,16 @@ def test_schedule_requests_matches_reference_fixture(name):
                                                           MemoryAccounting.EXACT][spec["accounting"]],
                             offline_policy=pol, split_threshold=spec["theta"],
                             buckets=spec["init_edges"], adjust=spec["adjust"] and spec["max_passes"] == 0,
-                            pledged=spec["pledged"])
+                            pledged=spec["pledged"], dispatch=dispatch)
     if spec["max_passes"]:
         pytest.skip("one-pass fixtures covered by BucketSet.adjust_buckets")
     ids = [i for p in out.plans for i in p.request_ids]
+    if dispatch:  # Simulator._next_plan order (pd_sim.py:448-462)
+        assert ids == ref["disp_ids"].tolist()
+        assert np.diff(ref["disp_off"]).tolist() == [len(p) for p in out.plans]
+        assert sorted(r.id for r in out.pending) == ref["disp_pending"].tolist()
+        assert sorted(r.request.id for r in out.rejections) == ref["disp_rejected"].tolist()
+        return
     assert ids == ref["batch_ids"].tolist()
     assert [(p.max_input_len, p.token_sum, p.footprint) for p in out.plans] == \
         [tuple(m[2:5]) for m in ref["batch_meta"].tolist()]

@@ -45,3 +45,48 @@ def test_fixture_set_is_nontrivial():
     assert len(names) >= 25
     total_batches = sum(len(load(n)[3]["batch_meta"]) for n in names)
     assert total_batches > 5000
+
+
+def dispatch_sequence(req_batch, req_row, emit_order):
+    """Plans in dispatch order as (flat request ids, offsets) — the reference shape."""
+    req_batch = np.asarray(req_batch, np.int64)
+    adm = np.nonzero(req_batch >= 0)[0]
+    order = adm[np.lexsort((np.asarray(req_row)[adm], req_batch[adm]))]
+    starts = np.searchsorted(req_batch[order], np.arange(int(req_batch.max(initial=-1)) + 2))
+    seq, off = [], [0]
+    for b in np.asarray(emit_order, np.int64):
+        seq.extend(order[starts[b]:starts[b + 1]].tolist())
+        off.append(len(seq))
+    return np.array(seq, np.int64), np.array(off, np.int64)
+
+
+DISPATCH_FIXTURES = [n for n in fixture_names() if "disp_ids" in load(n)[3]]
+
+
+@pytest.mark.parametrize("name", DISPATCH_FIXTURES)
+def test_oracle_dispatch_matches_reference(name):
+    """f3: Simulator._next_plan repeated (pd_sim.py:448-462) — the plan sequence,
+    rejections and still-queued requests equal the live reference's."""
+    spec, lens, cls, ref = load(name)
+    res, _ = run_oracle(spec, lens, cls)
+    ws = cpu.WindowSpec(l_max=spec["l_max"], n_classes=spec["n_classes"],
+                        policies=spec["policies"], theta=spec["theta"], adjust=spec["adjust"],
+                        max_passes=spec["max_passes"], kvpt=spec["kvpt"],
+                        current_safe=spec["current_safe"], pledged=spec["pledged"],
+                        accounting=spec["accounting"], truncate=spec["truncate"],
+                        init_edges=spec["init_edges"])
+    d = cpu.dispatch(ws, lens, res)
+    seq, off = dispatch_sequence(d.req_batch, d.req_row, d.emit_order)
+    assert np.array_equal(seq, ref["disp_ids"]) and np.array_equal(off, ref["disp_off"])
+    assert np.array_equal(np.nonzero(d.req_batch == cpu.REQ_REJECTED)[0], ref["disp_rejected"])
+    assert np.array_equal(np.nonzero(d.req_batch == cpu.REQ_PENDING)[0], ref["disp_pending"])
+
+
+def test_dispatch_fixtures_cover_the_hazards():
+    assert len(DISPATCH_FIXTURES) >= 28
+    reordered = pending_differs = 0
+    for n in DISPATCH_FIXTURES:
+        ref = load(n)[3]
+        reordered += not np.array_equal(ref["disp_ids"], ref["batch_ids"])
+        pending_differs += len(ref["disp_pending"]) != len(ref["pending"])
+    assert reordered >= 10 and pending_differs >= 3
