@@ -29,11 +29,13 @@
 // (one 1024-thread CTA per SM):
 //   keys    reverse segmented scan over the calls (suffix min / suffix sum per
 //           segment) -> 64-bit keys
-//   sort    stable LSD radix sort on the key bytes that vary
+//   sort    <= 8192 calls: bitonic sort of (key, call) in CTA 0 (registers, lane
+//           shuffles and shared memory); more: stable onesweep LSD radix sort on the
+//           key bytes that vary
 //   walk    class ranges, null-call list, single-thread walk -> runs of plans
 //   emit    emit_order[t] / batch_emit[b] from the runs; requests of calls the loop
 //           never reaches go back to PENDING
-// Windows with <= kSmall calls (C2: 1,911; C4: 4,591) run entirely in CTA 0's shared
+// Windows with <= kSmallCap calls (C2: 1,911; C4: 4,591) run entirely in CTA 0's shared
 // memory with no grid barrier; larger ones (C3: 24,998) use every CTA, onesweep
 // radix passes with decoupled look-back, and a grid barrier between phases.
 #include <cooperative_groups.h>
@@ -49,7 +51,8 @@ namespace {
 constexpr int kKT = 1024;                  // threads per CTA
 constexpr int kKW = kKT / 32;              // warps
 constexpr int kKItems = 7;
-constexpr int kSmall = kKT * kKItems;      // 7168: shared-memory path / radix tile size
+constexpr int kSmall = kKT * kKItems;      // 7168: radix tile of the multi-CTA path
+constexpr int kSmallCap = 8192;            // calls sorted in CTA 0's shared memory (bitonic)
 constexpr int kBucketBits = 17;
 constexpr uint64_t kMassMax = (1ull << (60 - kBucketBits)) - 1;
 constexpr uint64_t kUnreach = ~0ull;
@@ -249,6 +252,90 @@ __device__ __forceinline__ void tile_rank(const uint64_t (&key)[kKItems], int tb
   __syncthreads();
 }
 
+__device__ __forceinline__ bool pair_gt(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+  return ka > kb || (ka == kb && va > vb);
+}
+
+// Bitonic sort of P (power of two, 64 <= P <= 1024*E) (key, val) pairs in shared memory by
+// one 1024-thread CTA.  Warp w holds elements [w*32E, (w+1)*32E) in registers (element
+// e*32+lane of its span); compare distances < 32 are lane shuffles, < 32E register
+// swaps, and only the longer ones go through shared memory.
+template <int E>
+__device__ void block_bitonic(uint64_t* K, uint32_t* V, int P) {
+  constexpr int kSpan = 32 * E;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int base = w * kSpan;
+  const bool active = base < P;
+  uint64_t k[E];
+  uint32_t v[E];
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) { k[e] = K[base + e * 32 + lane]; v[e] = V[base + e * 32 + lane]; }
+  }
+  for (int kk = 2; kk <= P; kk <<= 1) {
+    if ((kk >> 1) >= kSpan) {  // long distances through shared memory
+      if (active) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) { K[base + e * 32 + lane] = k[e]; V[base + e * 32 + lane] = v[e]; }
+      }
+      __syncthreads();
+      for (int j = kk >> 1; j >= kSpan; j >>= 1) {
+        for (int i = tid; i < (P >> 1); i += kKT) {
+          const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+          const uint64_t ka = K[lo], kb = K[hi];
+          const uint32_t va = V[lo], vb = V[hi];
+          if (pair_gt(ka, va, kb, vb) == ((lo & kk) == 0)) {
+            K[lo] = kb; K[hi] = ka;
+            V[lo] = vb; V[hi] = va;
+          }
+        }
+        __syncthreads();
+      }
+      if (active) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) { k[e] = K[base + e * 32 + lane]; v[e] = V[base + e * 32 + lane]; }
+      }
+      __syncthreads();
+    }
+    if (!active) continue;
+#pragma unroll
+    for (int jb = E / 2; jb >= 1; jb >>= 1) {  // distances 32*jb: register pairs
+      if ((jb << 5) <= (kk >> 1)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int pe = e ^ jb;
+          if (pe > e) {
+            const bool up = ((base + e * 32 + lane) & kk) == 0;
+            if (pair_gt(k[e], v[e], k[pe], v[pe]) == up) {
+              const uint64_t tk = k[e]; k[e] = k[pe]; k[pe] = tk;
+              const uint32_t tv = v[e]; v[e] = v[pe]; v[pe] = tv;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 16; jj >= 1; jj >>= 1) {  // distances < 32: lane shuffles
+      if (jj <= (kk >> 1)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[e], jj);
+          const uint32_t ov = __shfl_xor_sync(0xffffffffu, v[e], jj);
+          const bool lower = (lane & jj) == 0;
+          const bool up = ((base + e * 32 + lane) & kk) == 0;
+          const bool gt = pair_gt(k[e], v[e], ok, ov);
+          if ((lower == up) ? gt : !gt) { k[e] = ok; v[e] = ov; }
+        }
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) { K[base + e * 32 + lane] = k[e]; V[base + e * 32 + lane] = v[e]; }
+  }
+  __syncthreads();
+}
+
 // null calls in sorted order -> a.nulls (block-wide compaction by one CTA); returns count
 __device__ int compact_nulls(const DispArgs& a, const uint32_t* V, int M) {
   __shared__ int32_t s_scan[33];
@@ -425,7 +512,6 @@ __global__ void __launch_bounds__(kKT, 1) k_dispatch(DispArgs a) {
   uint32_t* s_bin = reinterpret_cast<uint32_t*>(smem + kOffBin);
   uint32_t* s_dst = reinterpret_cast<uint32_t*>(smem + kOffDst);
   int64_t* s_gb = reinterpret_cast<int64_t*>(smem + kOffGb);
-  __shared__ unsigned long long s_or, s_and;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_sc[33];
 
@@ -434,53 +520,24 @@ __global__ void __launch_bounds__(kKT, 1) k_dispatch(DispArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   unsigned fl = 0;
 
-  if (M <= kSmall) {
+  if (M <= kSmallCap) {
     // ================= one CTA, everything in shared memory ==========================
     if (blockIdx.x != 0) return;
     for (int b = tid; b < nb; b += kKT) a.batch_emit[b] = -1;
-    scan_calls(a, M, 0, M, seg_id(), sk0, sv0, fl);
-    // key bytes that vary
-    if (tid == 0) { s_or = 0ull; s_and = ~0ull; }
+    uint64_t* K = reinterpret_cast<uint64_t*>(smem + kOffK0);  // [kSmallCap], in place
+    uint32_t* V = reinterpret_cast<uint32_t*>(smem + kOffV0);
+    scan_calls(a, M, 0, M, seg_id(), K, V, fl);
+    // bitonic sort of (key, call) pairs: (key, call) is unique, so the order is the
+    // stable order by key; pad to a power of two with keys that sort last
+    int P = 64;
+    while (P < M) P <<= 1;
+    for (int i = M + tid; i < P; i += kKT) { K[i] = kUnreach; V[i] = 0xffffffffu; }
     __syncthreads();
-    unsigned long long o = 0ull, an = ~0ull;
-    for (int i = tid; i < M; i += kKT) { o |= sk0[i]; an &= sk0[i]; }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      o |= __shfl_xor_sync(0xffffffffu, o, d);
-      an &= __shfl_xor_sync(0xffffffffu, an, d);
-    }
-    if (lane == 0) { atomicOr(&s_or, o); atomicAnd(&s_and, an); }
-    __syncthreads();
-    const uint64_t diff = s_or ^ s_and;
-    uint64_t* kin = sk0;
-    uint64_t* kout = sk1;
-    uint32_t* vin = sv0;
-    uint32_t* vout = sv1;
-    for (int d = 0; d < 8; ++d) {
-      if (!((diff >> (8 * d)) & 255u)) continue;
-      const int shift = 8 * d;
-      uint64_t key[kKItems];
-      uint32_t rank[kKItems], tc;
-#pragma unroll
-      for (int k = 0; k < kKItems; ++k) {
-        const int e = w * 32 * kKItems + k * 32 + lane;
-        key[k] = e < M ? kin[e] : kUnreach;
-      }
-      tile_rank(key, 0, M, shift, s_cnt, s_dst, rank, &tc);
-#pragma unroll
-      for (int k = 0; k < kKItems; ++k) {
-        const int e = w * 32 * kKItems + k * 32 + lane;
-        if (e < M) {
-          const uint32_t dg = (uint32_t)((key[k] >> shift) & 255u);
-          const uint32_t lp = s_dst[dg] + s_cnt[w * 256 + dg] + rank[k];
-          kout[lp] = key[k];
-          vout[lp] = vin[e];
-        }
-      }
-      __syncthreads();
-      uint64_t* tk = kin; kin = kout; kout = tk;
-      uint32_t* tv = vin; vin = vout; vout = tv;
-    }
+    if (P <= 2048) block_bitonic<2>(K, V, P);
+    else if (P == 4096) block_bitonic<4>(K, V, P);
+    else block_bitonic<8>(K, V, P);
+    uint64_t* kin = K;
+    uint32_t* vin = V;
     walk(a, kin, vin, M);
     __syncthreads();
     emit(a, vin, tid, kKT);

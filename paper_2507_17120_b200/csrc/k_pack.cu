@@ -347,6 +347,188 @@ static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------
+// Ring variant: the warp streams its 32 pieces as a flat sequence of chunks (one
+// chunk = 32 lanes x kU 16-byte vectors of one piece).  Loads are cp.async (16 B per
+// lane, L1 bypass) into a per-warp shared-memory ring of kNS chunks, so kNS-1 chunks
+// stay in flight while the oldest is written out — bytes in flight are bounded by
+// shared memory instead of registers.  Each lane reads back only the vectors it
+// fetched itself, so cp.async.wait_group is the only synchronisation.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int kU, int kNS, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_pack_ring(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
+                const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
+                const int64_t* __restrict__ tok_off, const int32_t* __restrict__ tokens,
+                int32_t L, int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
+                int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
+                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
+                bs_summary* sum) {
+  constexpr int kChunkV = 32 * kU;  // vectors per chunk
+  extern __shared__ __align__(128) uint8_t ring_smem[];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int4* ring = reinterpret_cast<int4*>(ring_smem) + (size_t)wib * kNS * kChunkV;
+  int64_t b_end = b_end_arg;
+  if (b_end < 0) {
+    b_end = sum_in->n_batches;
+    if (b_end > batches_cap) b_end = batches_cap;
+  }
+  if (b_begin >= b_end) return;
+  const int64_t base_off = batches[b_begin].out_offset;
+  const bs_batch last = batches[b_end - 1];
+  if (last.out_offset + (int64_t)last.n * last.pitch - base_off > out_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
+    return;
+  }
+  const int64_t t0 = task_base[b_begin], t1 = task_base[b_end];
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int4 pad4 = make_int4(pad_id, pad_id, pad_id, pad_id);
+  unsigned fl = 0;
+  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
+    const int64_t t = gt + lane;
+    PieceMeta my{nullptr, nullptr, nullptr, 0, 0, 0};
+    int32_t my_chunks = 0;
+    if (t < t1) {
+      int64_t lo = b_begin, hi = b_end;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (task_base[mid] <= t) lo = mid; else hi = mid;
+      }
+      const bs_batch B = batches[lo];
+      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int64_t local = t - task_base[lo];
+      const int64_t row = local / pieces;
+      const int32_t piece = (int32_t)(local - row * pieces);
+      const int64_t rstart = (B.out_offset - base_off) + row * (int64_t)B.pitch;
+      const int32_t r = perm[rowpos[B.row_base + row]];
+      my.x = eff_len(len[r], L, truncate, fl);
+      my.src = tokens + tok_off[r];
+      my.dst = out_tokens + rstart;
+      my.mdst = out_mask ? out_mask + rstart : nullptr;
+      my.vb = piece * (kPiece / 4);
+      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      my.ve = c1 >> 2;
+      my_chunks = (my.ve - my.vb + kChunkV - 1) / kChunkV;
+      if (((reinterpret_cast<uintptr_t>(my.src) | reinterpret_cast<uintptr_t>(my.dst)) & 15) != 0)
+        my_chunks = -my_chunks;  // unaligned row: scalar copy, no ring traffic
+    }
+    // flat chunk sequence over the group's pieces: chunk k of piece i
+    const int32_t ch_abs = my_chunks < 0 ? -my_chunks : my_chunks;
+    const int32_t ch_incl = warp_incl_scan(ch_abs);
+    const int32_t total = __shfl_sync(FULL, ch_incl, 31);
+    const int32_t ch_excl = ch_incl - ch_abs;
+    auto get = [&](int i) {
+      PieceMeta m;
+      m.src = reinterpret_cast<const int32_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.src), i));
+      m.dst = reinterpret_cast<int32_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.dst), i));
+      m.mdst = reinterpret_cast<uint8_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.mdst), i));
+      m.x = __shfl_sync(FULL, my.x, i);
+      m.vb = __shfl_sync(FULL, my.vb, i);
+      m.ve = __shfl_sync(FULL, my.ve, i);
+      return m;
+    };
+    // piece owning flat chunk c (lanes hold inclusive chunk prefixes)
+    auto owner = [&](int32_t c) { return __popc(__ballot_sync(FULL, ch_incl <= c)); };
+    auto issue = [&](int32_t c) {
+      if (c < total) {
+        const int i = owner(c);
+        const PieceMeta m = get(i);
+        const int32_t ci = c - __shfl_sync(FULL, ch_excl, i);
+        const bool al = __shfl_sync(FULL, my_chunks, i) > 0;
+        if (al) {
+          const int32_t full = m.x >> 2;
+          const int32_t hi = full < m.ve ? full : m.ve;
+          int4* slot = ring + (c % kNS) * kChunkV;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int32_t v = m.vb + ci * kChunkV + u * 32 + lane;
+            if (v < hi) cp_async16(slot + u * 32 + lane, m.src + 4 * v);
+          }
+        }
+      }
+      cp_async_commit();  // one group per chunk slot, empty past the end
+    };
+#pragma unroll
+    for (int c = 0; c < kNS - 1; ++c) issue(c);
+    for (int32_t c = 0; c < total; ++c) {
+      issue(c + kNS - 1);
+      cp_async_wait<kNS - 1>();  // chunk c has landed (groups complete in order)
+      const int i = owner(c);
+      const PieceMeta m = get(i);
+      const int32_t ci = c - __shfl_sync(FULL, ch_excl, i);
+      const bool al = __shfl_sync(FULL, my_chunks, i) > 0;
+      const int32_t cb = m.vb + ci * kChunkV;
+      const int32_t ce = cb + kChunkV < m.ve ? cb + kChunkV : m.ve;
+      if (al) {
+        const int32_t full = m.x >> 2, rem = m.x & 3;
+        const int4* slot = ring + (c % kNS) * kChunkV;
+        int4* d4 = reinterpret_cast<int4*>(m.dst);
+        uint32_t* m4 = reinterpret_cast<uint32_t*>(m.mdst);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int32_t v = cb + u * 32 + lane;
+          if (v < ce) {
+            int4 val = v < full ? slot[u * 32 + lane] : pad4;
+            if (v == full && rem) {
+              val.x = m.src[4 * v];
+              if (rem > 1) val.y = m.src[4 * v + 1];
+              if (rem > 2) val.z = m.src[4 * v + 2];
+            }
+            st_stream_v4(d4 + v, val);
+            if (m4) st_stream_u32(m4 + v, mask_word(m.x - 4 * v));
+          }
+        }
+      } else {
+        for (int32_t tt = 4 * cb + lane; tt < 4 * ce; tt += 32) {
+          m.dst[tt] = tt < m.x ? m.src[tt] : pad_id;
+          if (m.mdst) m.mdst[tt] = tt < m.x ? 1 : 0;
+        }
+      }
+    }
+    cp_async_wait<0>();
+  }
+  if (fl) latch_flags(sum, fl);
+}
+
+template <int kU, int kNS, int kWarps>
+static cudaError_t launch_pack_ring(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                                    const int64_t* tok_off, const int32_t* tokens,
+                                    const bs_window_params& p, const bs_batch* batches,
+                                    int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                                    bs_summary* summary, cudaStream_t st) {
+  const size_t smem = (size_t)kWarps * kNS * 32 * kU * 16;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k_pack_ring<kU, kNS, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_ring<kU, kNS, kWarps>,
+                                                  kWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
+  k_pack_ring<kU, kNS, kWarps><<<blocks, kWarps * 32, smem, st>>>(
+      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
+      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
+      summary);
+  ++ctx->launches;
+  return cudaGetLastError();
+}
+
 template <int kU, int kMinB>
 static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                  const int64_t* tok_off, const int32_t* tokens,
@@ -386,6 +568,16 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     case 2: BS_PACK_V(8, 4);
     case 3: BS_PACK_V(8, 3);
     case 4: BS_PACK_V(2, 8);
+#define BS_PACK_R(U, NS, W)                                                              \
+  return launch_pack_ring<U, NS, W>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, \
+                                    batch_end, batches_cap, out_tokens, out_mask,             \
+                                    out_capacity, summary, st)
+    case 6: BS_PACK_R(4, 4, 8);
+    case 7: BS_PACK_R(2, 8, 8);
+    case 8: BS_PACK_R(2, 6, 8);
+    case 9: BS_PACK_R(4, 6, 4);
+    case 10: BS_PACK_R(1, 16, 8);
+#undef BS_PACK_R
     case 5:
       return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
                              batches_cap, out_tokens, out_mask, out_capacity, summary, st);
