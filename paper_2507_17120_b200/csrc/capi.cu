@@ -11,6 +11,7 @@
 #include "ctx.cuh"
 
 void* bs_chain_kernel_ptr();     // k_size.cu
+int bs_chain_threads();
 void* bs_dispatch_kernel_ptr();  // k_dispatch.cu
 
 namespace {
@@ -172,7 +173,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(listA, N + 1); A(listB, N + 1);
   A(node_batch, N + 1);
   A(node_j0, N + 1);
-  A(segw, 5 * (L * C + 1));
+  A(segw, 6 * (L * C + 1));
   A(rowpos, N + 1);
   A(task_base, N + 2);
   A(misc, 128);
@@ -188,9 +189,10 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
     delete ctx;
     return rc;
   }
-  // co-resident blocks for the cooperative chain kernel (512 threads)
+  // co-resident blocks for the cooperative chain kernel
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(), 512, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(),
+                                                    bs_chain_threads(), 0);
   if (e != cudaSuccess || per_sm < 1) {
     int rc = e != cudaSuccess ? cuda_fail(ctx, e, "occupancy(k_chain)")
                               : fail(ctx, BS_ERR_NOT_BUILT, "k_chain cannot be resident");

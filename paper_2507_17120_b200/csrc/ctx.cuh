@@ -57,7 +57,7 @@ struct bs_ctx {
   int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
                                  //   <= kPiece tokens; exclusive prefix, K5f)
   int32_t* node_j0 = nullptr;
-  int32_t* segw = nullptr;       // [5][l_cap*c_max+1] per-segment chain length / tail / bases    // [max_n + 1] first admissible position at/after each chain node
+  int32_t* segw = nullptr;       // [6][l_cap*c_max+1] per-segment chain length / tail / bases    // [max_n + 1] first admissible position at/after each chain node
   int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
   uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
   int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)
@@ -78,7 +78,7 @@ struct bs_ctx {
   int32_t* disp_runs = nullptr;      // [2*l_cap*c_max+32][4] runs of consecutive plans
   int64_t* disp_misc = nullptr;      // [32]
   int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
-                                 //        [66] n_batches, [67] pack rows cursor
+                                 //        [66] n_batches, [67] pack rows cursor, [69] long chains
 };
 
 namespace bsk {

@@ -20,13 +20,13 @@
 //                  32 group summaries per step (shuffle scans + per-lane binary
 //                  search), then <= 32 element steps per lane.  Work per start is
 //                  O(1 + span/1024) warp steps instead of O(span/32) serial loads.
-//   K5c  chain     one cooperative kernel: group-count prefix scan, pointer
-//                  doubling J[r] = next^(2^r) (grid.sync per level, stops when
-//                  every segment's chain is covered), per-segment chain length
-//                  by binary lifting, then every chain node (= batch start) is
-//                  materialised in emission order in parallel (node k of segment s
-//                  is next^k(start_s), composed from the set bits of k) —
-//                  O(N log B) work, O(log B) depth.
+//   K5c  chain     one cooperative kernel (one 1024-thread CTA per SM): group-count
+//                  prefix scan; every segment's chain next(next(...)) followed serially
+//                  by one thread for up to kWalk calls (dependent L2 hits, C2's longest
+//                  chain is 75 calls); only when some chain is longer: pointer doubling
+//                  J[r] = next^(2^r) (grid.sync per level) and binary lifting for those
+//                  segments; then every chain node (= batch start) is materialised in
+//                  emission order in parallel.
 //   K5d  describe  one warp per batch: n / sum / max / min from group summaries
 //   K5f  offsets   one CTA: packed-buffer offsets (scan of n*pitch), row bases, totals
 //   K5e  outcome   one warp per 32 positions: batch id / row / rejected / pending,
@@ -330,6 +330,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------- K5c
+constexpr int kChainThreads = 1024;  // one CTA per SM: fewer CTAs per grid barrier
+constexpr int kWalk = 128;           // chain calls followed serially before doubling is used
+
 struct ChainShared {
   int32_t si[33];
   int32_t flag;
@@ -339,7 +342,7 @@ __device__ __forceinline__ int32_t ld_rel_i32(const int32_t* p) {
   return (int32_t)ld_relaxed(reinterpret_cast<const uint32_t*>(p));
 }
 
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(kChainThreads, 1)
     k_chain(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
             int32_t* J, int r_cap, const uint8_t* __restrict__ is_start, int32_t* alive,
             int32_t* listA, int32_t* listB, int32_t* node_batch, int32_t* node_j0, int32_t* misc,
@@ -352,18 +355,60 @@ __global__ void __launch_bounds__(512)
   const int64_t n = a.n;
   const int32_t n_segs = kinfo[2];
   const int tid = threadIdx.x, bt = blockDim.x;
+  int32_t* seg_len = segw;
+  int32_t* seg_empty = segw + (n_segs + 1);
+  int32_t* seg_tailj0 = segw + 2 * (n_segs + 1);
+  int32_t* seg_nbase = segw + 3 * (n_segs + 1);
+  int32_t* seg_ebase = segw + 4 * (n_segs + 1);
+  int32_t* seg_long = segw + 5 * (n_segs + 1);
   // ---- phase 0: Rg = exclusive prefix of admissible counts per 32-position group ----
+  const int64_t G = (n + 31) >> 5;
+  const int64_t per = (G + gridDim.x - 1) / gridDim.x;
+  const int64_t g0 = (int64_t)blockIdx.x * per;
+  const int64_t g1 = g0 + per < G ? g0 + per : G;
   {
-    const int64_t G = (n + 31) >> 5;
-    const int64_t per = (G + gridDim.x - 1) / gridDim.x;
-    const int64_t g0 = (int64_t)blockIdx.x * per;
-    const int64_t g1 = g0 + per < G ? g0 + per : G;
     int32_t loc = 0;
     for (int64_t g = g0 + tid; g < g1; g += bt) loc += bcnt[g];
     int32_t tot;
     block_excl_scan<int32_t>(loc, sh.si, &tot);
     if (tid == 0) btot[blockIdx.x] = tot;
-    grid.sync();
+  }
+  // ---- phase W: follow every segment's chain next(next(...)) for up to kWalk calls,
+  // one thread per segment (dependent L2 hits: ~kWalk x 130 ns); nodes land in listB
+  // at seg_off[s] + k.  Only segments with longer chains need pointer doubling.
+  {
+    bool any_long = false;
+    for (int64_t sg = (int64_t)blockIdx.x * bt + tid; sg < n_segs; sg += (int64_t)gridDim.x * bt) {
+      const int64_t st = seg_off[sg], en = seg_off[sg + 1];
+      int32_t len = 0, empty = 0, tj0 = 0, lng = 0;
+      if (st < en) {
+        int64_t pos = st;
+        int32_t k = 0;
+        listB[st] = (int32_t)st;
+        for (;;) {
+          const int32_t y = J[pos];
+          if (y == kEnd) break;
+          if (++k >= kWalk) { lng = 1; break; }
+          listB[st + k] = y;
+          pos = y;
+        }
+        if (!lng) {
+          len = k + 1;
+          const int64_t j0 = first_nonrej(pos, en, bmask);
+          empty = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
+          tj0 = (int32_t)j0;
+        }
+      }
+      seg_len[sg] = len;
+      seg_empty[sg] = empty;
+      seg_tailj0[sg] = tj0;
+      seg_long[sg] = lng;
+      any_long |= lng != 0;
+    }
+    if (any_long) misc[69] = 1;
+  }
+  grid.sync();
+  {
     int32_t pre = 0;
     for (int b = tid; b < (int)blockIdx.x; b += bt) pre += ld_rel_i32(btot + b);
     int32_t off;
@@ -379,53 +424,61 @@ __global__ void __launch_bounds__(512)
     }
   }
   int r = 0;
-  // ---- phase 1: pointer doubling ---------------------------------------------------------
-  while (r + 1 < r_cap && ld_rel_i32(alive + r)) {
-    const int32_t* Jr = J + (int64_t)r * n;
-    int32_t* Jn = J + (int64_t)(r + 1) * n;
-    bool any = false;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
-         x += (int64_t)gridDim.x * blockDim.x) {
-      const int32_t v = Jr[x];
-      const int32_t w = v == kEnd ? kEnd : Jr[v];
-      Jn[x] = w;
-      if (w != kEnd && is_start[x]) any = true;
+  const bool need_doubling = ld_rel_i32(misc + 69) != 0;
+  if (need_doubling) {
+    // ---- phase 1: pointer doubling -------------------------------------------------------
+    while (r + 1 < r_cap && ld_rel_i32(alive + r)) {
+      const int32_t* Jr = J + (int64_t)r * n;
+      int32_t* Jn = J + (int64_t)(r + 1) * n;
+      bool any = false;
+      // four independent positions per thread in flight (the second load is a gather)
+      const int64_t S = (int64_t)gridDim.x * blockDim.x;
+      for (int64_t x0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < n; x0 += 4 * S) {
+        int32_t v[4], w[4];
+        uint8_t st[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t x = x0 + k * S;
+          v[k] = x < n ? Jr[x] : kEnd;
+          st[k] = x < n ? is_start[x] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = v[k] == kEnd ? kEnd : Jr[v[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t x = x0 + k * S;
+          if (x < n) {
+            Jn[x] = w[k];
+            if (w[k] != kEnd && st[k]) any = true;
+          }
+        }
+      }
+      if (any) alive[r + 1] = 1;
+      grid.sync();
+      ++r;
     }
-    if (any) alive[r + 1] = 1;
-    grid.sync();
-    ++r;
-  }
-  // ---- phase 2: per segment, chain length and its last node (binary lifting) -------
-  // len = number of chain nodes (form_batch calls); the last one may be an empty tail
-  // (everything left is oversize, or the drain blocks on a request that does not fit)
-  int32_t* seg_len = segw;
-  int32_t* seg_empty = segw + (n_segs + 1);
-  int32_t* seg_tailj0 = segw + 2 * (n_segs + 1);
-  int32_t* seg_nbase = segw + 3 * (n_segs + 1);
-  int32_t* seg_ebase = segw + 4 * (n_segs + 1);
-  for (int64_t sg = (int64_t)blockIdx.x * bt + tid; sg < n_segs; sg += (int64_t)gridDim.x * bt) {
-    const int64_t st = seg_off[sg], en = seg_off[sg + 1];
-    int32_t len = 0, empty = 0, tj0 = 0;
-    if (st < en) {
+    // ---- phase 2: long segments: chain length and last node by binary lifting ------------
+    // len = number of chain nodes (form_batch calls); the last one may be an empty tail
+    // (everything left is oversize, or the drain blocks on a request that does not fit)
+    for (int64_t sg = (int64_t)blockIdx.x * bt + tid; sg < n_segs; sg += (int64_t)gridDim.x * bt) {
+      if (!seg_long[sg]) continue;
+      const int64_t st = seg_off[sg], en = seg_off[sg + 1];
       int64_t pos = st;
       int32_t cnt = 0;
       for (int lv = r - 1; lv >= 0; --lv) {
         const int32_t y = J[(int64_t)lv * n + pos];
         if (y != kEnd) { pos = y; cnt += 1 << lv; }
       }
-      len = cnt + 1;
       const int64_t j0 = first_nonrej(pos, en, bmask);
-      empty = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
-      tj0 = (int32_t)j0;
+      seg_len[sg] = cnt + 1;
+      seg_empty[sg] = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
+      seg_tailj0[sg] = (int32_t)j0;
     }
-    seg_len[sg] = len;
-    seg_empty[sg] = empty;
-    seg_tailj0[sg] = tj0;
+    grid.sync();
   }
-  grid.sync();
   // ---- phase 3 (block 0): node / batch bases per segment ---------------------------------
   if (blockIdx.x == 0) {
-    if (tid == 0) sh.flag = (r + 1 >= r_cap && ld_rel_i32(alive + r)) ? 1 : 0;
+    if (tid == 0) sh.flag = (need_doubling && r + 1 >= r_cap && ld_rel_i32(alive + r)) ? 1 : 0;
     int32_t run_n = 0, run_e = 0;
     for (int base = 0; base < n_segs; base += bt) {
       const int sg = base + tid;
@@ -462,8 +515,12 @@ __global__ void __launch_bounds__(512)
     }
     const int32_t k = (int32_t)(i - ld_rel_i32(seg_nbase + lo));
     int64_t pos = seg_off[lo];
-    for (int lv = 0; lv < r; ++lv)
-      if ((k >> lv) & 1) pos = J[(int64_t)lv * n + pos];
+    if (ld_rel_i32(seg_long + lo)) {
+      for (int lv = 0; lv < r; ++lv)
+        if ((k >> lv) & 1) pos = J[(int64_t)lv * n + pos];
+    } else {
+      pos = ld_rel_i32(listB + pos + k);  // walked in phase W
+    }
     listA[i] = (int32_t)pos;
     const bool tail_empty = (k == ld_rel_i32(seg_len + lo) - 1) && ld_rel_i32(seg_empty + lo);
     node_batch[i] = tail_empty ? -1 : (int32_t)(i - ld_rel_i32(seg_ebase + lo));
@@ -766,7 +823,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
                     &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
                     (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
-    e = cudaLaunchCooperativeKernel((void*)k_chain, dim3(ctx->chain_blocks), dim3(512), args, 0,
+    e = cudaLaunchCooperativeKernel((void*)k_chain, dim3(ctx->chain_blocks), dim3(kChainThreads), args, 0,
                                     st);
     if (e != cudaSuccess) return e;
   }
@@ -791,3 +848,4 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
 }  // namespace bsk
 
 void* bs_chain_kernel_ptr() { return reinterpret_cast<void*>(&bsk::k_chain); }
+int bs_chain_threads() { return bsk::kChainThreads; }

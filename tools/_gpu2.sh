@@ -1,7 +1,6 @@
 set -u
-OUT=gpurun_out/r1s2d; mkdir -p $OUT
+OUT=gpurun_out/r1s2g; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_dispatch.py -x -q > $OUT/disp.log 2>&1; echo "rc=$?" >> $OUT/disp.log
 timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log
 for c in c2 c3 c4; do timeout 300 python tools/stage_profile.py --config $c --dispatch > $OUT/stages_$c.json 2>&1; done
-tail -5 $OUT/disp.log; tail -3 $OUT/pytest_gpu.log; cat $OUT/stages_*.json | cut -c1-400
+tail -3 $OUT/pytest_gpu.log; cat $OUT/stages_*.json | cut -c1-330
