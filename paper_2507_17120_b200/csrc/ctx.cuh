@@ -18,6 +18,7 @@ struct bs_ctx {
   int64_t scratch_bytes = 0;
   int64_t launches = 0;     // kernels launched through this ctx
   int pack_variant = 0;     // K6 tuning variant (env BS_PACK_VARIANT)
+  int hist_agg = 0;         // K1: 1 = warp-aggregated shared atomics (env BS_HIST_AGG)
   std::string err;
   // stage profiler: ring of (BS_STAGES+1) events per recorded step
   std::vector<cudaEvent_t> prof_events;
@@ -33,6 +34,8 @@ struct bs_ctx {
   int32_t* seg_base = nullptr;   // [l_cap*c_max] first radix slot of each segment
   int32_t* seg_off = nullptr;    // [l_cap*c_max+1] segment offsets of the last bs_boundaries
   uint32_t* slot_lut = nullptr;  // [c_max*l_cap] radix slot per (class, length)
+  int32_t* slot_seg = nullptr;   // [c_max*l_cap] segment of each radix slot
+  const uint32_t* sorted_keys = nullptr;  // drain-order slots of the last bs_order (K4)
   uint32_t* bins_cnt = nullptr;  // [4][256] per-pass radix digit counts (K2c -> K4)
   uint32_t* tile_tot = nullptr;  // [ntiles][C+1] K2a tile totals (per class, then total)
   uint64_t* tile_slen = nullptr; // [ntiles] K2a tile sum of x*h[x]

@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(256)
              int sort_passes, const int32_t* __restrict__ gE, const uint32_t* __restrict__ gbm,
              const uint32_t* __restrict__ gwp, const int32_t* __restrict__ seg_base,
              int32_t* __restrict__ lut, uint32_t* __restrict__ slot_lut,
-             uint32_t* __restrict__ bins_cnt) {
+             uint32_t* __restrict__ bins_cnt, int32_t* __restrict__ slot_seg) {
   __shared__ uint32_t sbins[4 * 256];
   const int32_t L = p.l_max, C = p.n_classes;
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) sbins[i] = 0;
@@ -377,16 +377,11 @@ __global__ void __launch_bounds__(256)
     if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - gE[b]);
     else if (pol == BS_POLICY_LJF) slot += (uint32_t)(gE[b + 1] - 1 - x);
     slot_lut[idx] = slot;
+    slot_seg[slot] = b * C + c;
     const uint32_t h = hist_local[idx];
-    const unsigned act = __ballot_sync(__activemask(), h != 0);
-    if (h) {
-      for (int q = 0; q < sort_passes; ++q) {
-        const uint32_t d = (slot >> (q * sort_bits)) & dmask;
-        const unsigned peers = __match_any_sync(act, d);
-        const uint32_t tot = __reduce_add_sync(peers, h);
-        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sbins[q * 256 + d], tot);
-      }
-    }
+    if (h)  // consecutive lengths hit distinct low digits: plain shared atomics
+      for (int q = 0; q < sort_passes; ++q)
+        atomicAdd(&sbins[q * 256 + ((slot >> (q * sort_bits)) & dmask)], h);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < sort_passes * 256; i += blockDim.x)
@@ -423,7 +418,7 @@ __global__ void __launch_bounds__(kBT, 1)
                    uint32_t* __restrict__ PcL, int32_t* __restrict__ gE,
                    int32_t* __restrict__ seg_base, int32_t* __restrict__ lut,
                    uint32_t* __restrict__ slot_lut, uint32_t* __restrict__ bins_cnt,
-                   int32_t* __restrict__ kinfo, bs_summary* sum) {
+                   int32_t* __restrict__ kinfo, bs_summary* sum, int32_t* __restrict__ slot_seg) {
   extern __shared__ uint32_t dyn[];
   __shared__ BoundsShared sh;
   __shared__ uint32_t sbins[4 * 256];
@@ -698,16 +693,11 @@ __global__ void __launch_bounds__(kBT, 1)
     if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - E[b]);
     else if (pol == BS_POLICY_LJF) slot += (uint32_t)(E[b + 1] - 1 - x);
     slot_lut[idx] = slot;
+    slot_seg[slot] = b * C + c;
     const uint32_t h = hist_local[idx];
-    const unsigned act = __ballot_sync(__activemask(), h != 0);
-    if (h) {
-      for (int q = 0; q < sort_passes; ++q) {
-        const uint32_t d = (slot >> (q * sort_bits)) & dmask;
-        const unsigned peers = __match_any_sync(act, d);
-        const uint32_t tot = __reduce_add_sync(peers, h);
-        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sbins[q * 256 + d], tot);
-      }
-    }
+    if (h)  // consecutive lengths hit distinct low digits: plain shared atomics
+      for (int q = 0; q < sort_passes; ++q)
+        atomicAdd(&sbins[q * 256 + ((slot >> (q * sort_bits)) & dmask)], h);
   }
   __syncthreads();
   for (int i = tid; i < 4 * 256; i += kBT) bins_cnt[i] = sbins[i];
@@ -751,7 +741,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
                                          sp.bits, sp.passes, init_edges, k_init, edges_out,
                                          changes_out, changes_cap, seg_off_out, ctx->PcL, ctx->E,
                                          ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
-                                         ctx->kinfo, summary);
+                                         ctx->kinfo, summary, ctx->slot_seg);
     ++ctx->launches;
     return cudaGetLastError();
   }
@@ -779,7 +769,8 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
   const unsigned tb = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((cells + 1023) / 1024, 4LL * ctx->num_sms));
   k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
-                               ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt);
+                               ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
+                               ctx->slot_seg);
   ctx->launches += 3;
   return cudaGetLastError();
 }

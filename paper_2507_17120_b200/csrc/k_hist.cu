@@ -7,16 +7,27 @@
 //
 // B200 mapping: HBM-bound read of len (int32) + cls (u8) with 128-bit / 32-bit
 // vector loads; counts privatised per CTA in shared memory for the dense head
-// bins (lengths < H), warp-aggregated with __match_any_sync so lanes holding the
-// same (class, length) key issue one shared atomic; tail bins (long-context
-// lengths >= H) go straight to L2 atomics.  Grid is sized so the per-CTA
-// flush of C*H bins stays small relative to the elements each CTA reads.
+// bins (lengths < H); tail bins (long-context lengths >= H) go straight to L2
+// atomics; non-zero shared bins are flushed with one L2 atomic each.  Two forms of
+// the shared-memory update: plain per-lane atomics (default) and warp-aggregated
+// (__match_any_sync: lanes holding the same (class, length) key issue one atomic,
+// BS_HIST_AGG=1).  On the BASELINE length distributions the keys inside a warp are
+// mostly distinct, so aggregation only adds the MATCH latency: measured on B200,
+// plain 18.5 us vs aggregated 26.5 us at C2 (1M), 50 vs 152 us at C3 (16M).
+#include <cstdlib>
+
 #include "ctx.cuh"
 
 namespace bsk {
 
+template <bool kAgg>
 __device__ __forceinline__ void hist_add(int32_t x, int32_t c, int32_t L, int32_t H,
                                          uint32_t* sh, uint32_t* __restrict__ hist) {
+  if (!kAgg) {
+    if (x < H) atomicAdd(&sh[(unsigned)c * (unsigned)H + (unsigned)x], 1u);
+    else atomicAdd(&hist[(unsigned)c * (unsigned)L + (unsigned)x], 1u);
+    return;
+  }
   if (x < H) {
     const unsigned key = (unsigned)c * (unsigned)H + (unsigned)x;
     const unsigned peers = __match_any_sync(__activemask(), key);
@@ -28,6 +39,7 @@ __device__ __forceinline__ void hist_add(int32_t x, int32_t c, int32_t L, int32_
   }
 }
 
+template <bool kAgg>
 __global__ void __launch_bounds__(512) k_histogram(const int32_t* __restrict__ len,
                                                    const uint8_t* __restrict__ cls, int64_t n,
                                                    int32_t L, int32_t C, int32_t truncate,
@@ -47,15 +59,15 @@ __global__ void __launch_bounds__(512) k_histogram(const int32_t* __restrict__ l
     for (int64_t v = tid; v < nv; v += stride) {
       const int4 l = __ldg(len4 + v);
       const uchar4 c = __ldg(cls4 + v);
-      hist_add(eff_len(l.x, L, truncate, fl), eff_cls(c.x, C, fl), L, H, sh, hist);
-      hist_add(eff_len(l.y, L, truncate, fl), eff_cls(c.y, C, fl), L, H, sh, hist);
-      hist_add(eff_len(l.z, L, truncate, fl), eff_cls(c.z, C, fl), L, H, sh, hist);
-      hist_add(eff_len(l.w, L, truncate, fl), eff_cls(c.w, C, fl), L, H, sh, hist);
+      hist_add<kAgg>(eff_len(l.x, L, truncate, fl), eff_cls(c.x, C, fl), L, H, sh, hist);
+      hist_add<kAgg>(eff_len(l.y, L, truncate, fl), eff_cls(c.y, C, fl), L, H, sh, hist);
+      hist_add<kAgg>(eff_len(l.z, L, truncate, fl), eff_cls(c.z, C, fl), L, H, sh, hist);
+      hist_add<kAgg>(eff_len(l.w, L, truncate, fl), eff_cls(c.w, C, fl), L, H, sh, hist);
     }
     done = nv << 2;
   }
   for (int64_t i = done + tid; i < n; i += stride)
-    hist_add(eff_len(__ldg(len + i), L, truncate, fl), eff_cls(__ldg(cls + i), C, fl), L, H, sh,
+    hist_add<kAgg>(eff_len(__ldg(len + i), L, truncate, fl), eff_cls(__ldg(cls + i), C, fl), L, H, sh,
              hist);
   __syncthreads();
   for (int i = threadIdx.x; i < C * H; i += blockDim.x) {
@@ -89,19 +101,32 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
   const size_t smem = sizeof(uint32_t) * (size_t)C * H;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_histogram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_histogram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr_set = true;
   }
   const int threads = 512;
-  // >= 16 elements per thread and at most 2 CTAs per SM: the per-CTA zero/flush of the
+  // >= ept elements per thread and at most 2 CTAs per SM: the per-CTA zero/flush of the
   // privatised bins stays well below the elements each CTA reads
-  int64_t blocks = (n + 16LL * threads - 1) / (16LL * threads);
-  blocks = std::min<int64_t>(blocks, 2LL * ctx->num_sms);
+  const int agg = ctx->hist_agg;
+  static int ept = 0, maxb = 0;
+  if (ept == 0) {  // tuning hooks
+    const char* v = getenv("BS_HIST_EPT");
+    ept = v ? atoi(v) : 4;
+    const char* m = getenv("BS_HIST_MAXB");
+    maxb = m ? atoi(m) : 2 * ctx->num_sms;
+  }
+  int64_t blocks = (n + (int64_t)ept * threads - 1) / ((int64_t)ept * threads);
+  blocks = std::min<int64_t>(blocks, maxb);
   blocks = std::max<int64_t>(blocks, 1);
   const int vec_ok = ((reinterpret_cast<uintptr_t>(len) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(cls) & 3) == 0);
-  k_histogram<<<(unsigned)blocks, threads, smem, st>>>(len, cls, n, L, C, p.truncate, H, vec_ok,
-                                                       hist, summary);
+  if (agg)
+    k_histogram<true><<<(unsigned)blocks, threads, smem, st>>>(len, cls, n, L, C, p.truncate, H,
+                                                             vec_ok, hist, summary);
+  else
+    k_histogram<false><<<(unsigned)blocks, threads, smem, st>>>(len, cls, n, L, C, p.truncate, H,
+                                                              vec_ok, hist, summary);
   ++ctx->launches;
   return cudaGetLastError();
 }

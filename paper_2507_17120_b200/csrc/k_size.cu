@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(256)
                 const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
                 const int32_t* __restrict__ bmax, const int32_t* __restrict__ bcnt,
                 const int32_t* __restrict__ bsum, int32_t* __restrict__ J0,
-                uint8_t* __restrict__ is_start, int32_t* __restrict__ alive) {
+                uint8_t* __restrict__ is_start, int32_t* __restrict__ alive,
+                const uint32_t* __restrict__ skeys, const int32_t* __restrict__ slot_seg) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int32_t n_segs = kinfo[2];
@@ -177,7 +178,8 @@ __global__ void __launch_bounds__(256)
     bool start = false;
     {  // segment of j: one binary search per warp, then a short walk per lane
       int64_t s0 = 0;
-      if (lane == 0) s0 = seg_of(seg_off, n_segs, g << 5);
+      // the sorted radix slot names the segment (K2 slot_seg LUT); binary search otherwise
+      if (lane == 0) s0 = skeys ? slot_seg[skeys[g << 5]] : seg_of(seg_off, n_segs, g << 5);
       int64_t s = __shfl_sync(FULL, s0, 0);
       if (valid) {
         while (seg_off[s + 1] <= j) ++s;
@@ -542,7 +544,8 @@ __global__ void __launch_bounds__(256)
                     const int32_t* __restrict__ J0, const int32_t* __restrict__ listA,
                     const int32_t* __restrict__ listB, const int32_t* __restrict__ node_batch,
                     const int32_t* __restrict__ misc, bs_batch* __restrict__ batches,
-                    int32_t batches_cap, bs_summary* sum) {
+                    int32_t batches_cap, bs_summary* sum, const uint32_t* __restrict__ skeys,
+                    const int32_t* __restrict__ slot_seg) {
   const int M = misc[64];
   const int32_t n_segs = kinfo[2];
   const int32_t* list = misc[68] ? listB : listA;
@@ -554,7 +557,7 @@ __global__ void __launch_bounds__(256)
     const int32_t b = node_batch[i];
     if (b < 0 || b >= batches_cap) continue;
     const int64_t c = list[i];
-    const int64_t s = seg_of(seg_off, n_segs, c);
+    const int64_t s = skeys ? slot_seg[skeys[c]] : seg_of(seg_off, n_segs, c);
     const int32_t nx = J0[c];
     const int64_t e = nx == kEnd ? (int64_t)seg_off[s + 1] : (int64_t)nx;
     int64_t cnt = 0, tsum = 0;
@@ -798,7 +801,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   prof_mark(ctx, 4, st);
   k_size_next<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmask,
                                        ctx->bmax, ctx->bcnt, ctx->bsum, ctx->J, ctx->is_start,
-                                       misc);
+                                       misc, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 5, st);
   {
@@ -831,7 +834,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   k_size_describe<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax,
                                            ctx->bmin, ctx->bcnt, ctx->bsum, ctx->J, ctx->listA,
                                            ctx->listB, ctx->node_batch, misc, batches,
-                                           batches_cap, summary);
+                                           batches_cap, summary, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

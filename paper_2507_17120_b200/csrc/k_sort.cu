@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kSortThreads)
     const uint32_t kk = s_keys[i];
     const uint32_t d = (kk >> shift) & dmask;
     const int64_t g = s_gbase[d] + i;
-    if (!kLast) keys_out[g] = kk;
+    keys_out[g] = kk;  // the last pass too: K5 maps sorted slots to segments
     vals_out[g] = s_vals[i];
   }
   (void)fl;  // range errors on the same inputs are latched by K1
@@ -215,6 +215,7 @@ static cudaError_t order_passes(bs_ctx* ctx, const int32_t* len, const uint8_t* 
     kin = kout;
     vin = vout;
   }
+  ctx->sorted_keys = kin;
   return cudaSuccess;
 }
 

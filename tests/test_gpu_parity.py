@@ -274,6 +274,21 @@ def test_pack_variants_bit_exact(variant, monkeypatch):
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
 
 
+@pytest.mark.parametrize("agg", ["0", "1"])
+def test_histogram_forms_bit_exact(agg, monkeypatch):
+    """K1 plain and warp-aggregated (BS_HIST_AGG) shared-memory atomics give the
+    oracle's histogram, including heavy key duplication inside a warp."""
+    monkeypatch.setenv("BS_HIST_AGG", agg)
+    cfg, lens, cls = W.make_window("c2", n=200_000, seed=9)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=False)
+    spec, lens, cls, ref = load("equal_lengths")
+    s = _sched(spec, len(lens))
+    h = s.schedule(lens, cls).to_host()
+    o = _oracle(spec, lens, cls)
+    assert np.array_equal(h["hist"].reshape(-1), o.hist.reshape(-1))
+    s.close()
+
+
 def test_cuda_graph_replay_matches_eager():
     """graph=True (one CUDA graph per window, replayed) gives the eager result."""
     cfg, lens, cls = W.make_window("c2", n=120_000, seed=44)

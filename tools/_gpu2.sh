@@ -1,6 +1,4 @@
-set -u
-OUT=gpurun_out/r1s2g; mkdir -p $OUT
-python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log
-for c in c2 c3 c4; do timeout 300 python tools/stage_profile.py --config $c --dispatch > $OUT/stages_$c.json 2>&1; done
-tail -3 $OUT/pytest_gpu.log; cat $OUT/stages_*.json | cut -c1-330
+python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
+for agg in 1 0; do for e in 2 4 8 16; do echo -n "agg $agg ept $e: "; BS_HIST_AGG=$agg BS_HIST_EPT=$e python tools/stage_profile.py --config c2 | python -c "import json,sys; print(json.loads(sys.stdin.read())['stage_us']['histogram'])"; done; done
+for agg in 1 0; do for e in 4 16; do echo -n "c3 agg $agg ept $e: "; BS_HIST_AGG=$agg BS_HIST_EPT=$e python tools/stage_profile.py --config c3 | python -c "import json,sys; print(json.loads(sys.stdin.read())['stage_us']['histogram'])"; done; done
+for agg in 1 0; do echo -n "c4 agg $agg: "; BS_HIST_AGG=$agg BS_HIST_EPT=4 python tools/stage_profile.py --config c4 | python -c "import json,sys; print(json.loads(sys.stdin.read())['stage_us']['histogram'])"; done
