@@ -281,6 +281,33 @@ int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_par
 int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
                     uint64_t* out, void* stream);
 
+/* ---- trace ingestion (host side) ---------------------------------
+ * Parses the reference's trace files (workload.py:343-437: `_load_csv`, `_load_jsonl`,
+ * `load_trace`) into structure-of-arrays host memory: records in arrival order
+ * (stable sort, ids = file order), the reference's validation, and on the first
+ * malformed record BS_ERR_CONFIG with err_line / err_msg set to the reference's
+ * TraceFormatError text ("line N: ...", errors.py:8-13).  `threads` <= 0: all host
+ * threads (inputs under 1 MiB parse on one thread).  Arrays are malloc'ed by the
+ * library; release them with bs_trace_free.  No GPU needed.
+ * The .bst binary format stores the same arrays (64-byte header, then id, arrival,
+ * input_len, output_len, cls, each padded to 64 bytes) for direct reloads. */
+#define BS_TRACE_CSV   0
+#define BS_TRACE_JSONL 1
+typedef struct bs_trace {
+  int64_t  n;
+  int64_t* id;          /* [n] file-order id (Request.id)                       */
+  double*  arrival;     /* [n] arrival_s, non-decreasing                        */
+  int64_t* input_len;   /* [n] input_tokens (>= 1)                              */
+  int64_t* output_len;  /* [n] output_tokens, -1 where the record omits it      */
+  uint8_t* cls;         /* [n] 0 = online, 1 = offline                          */
+  int64_t  err_line;    /* 1-based line of the first malformed record, else -1  */
+  char     err_msg[256];
+} bs_trace;
+int  bs_trace_parse(const char* text, int64_t len, int32_t format, int32_t threads, bs_trace* out);
+void bs_trace_free(bs_trace* t);
+int  bs_trace_write_bst(const char* path, const bs_trace* t);
+int  bs_trace_read_bst(const char* path, bs_trace* out);
+
 /* ---- instrumentation ---------------------------------------------------------------
  * Stage timing of the fused window call, recorded with CUDA events on the call's
  * stream at the K1|K2|K4|K5|K6 boundaries (no host synchronisation while

@@ -44,7 +44,8 @@ PACK_ALIGN = 4
 EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "bs_destroy",
            "bs_histogram", "bs_boundaries", "bs_assign", "bs_order", "bs_size", "bs_pack",
            "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_profile_enable",
-           "bs_profile_read", "bs_launch_count", "bs_dispatch")
+           "bs_profile_read", "bs_launch_count", "bs_dispatch", "bs_trace_parse",
+           "bs_trace_write_bst", "bs_trace_read_bst")
 STAGES = ("histogram", "boundaries", "order", "size.prep", "size.next", "size.chain",
           "size.describe", "size.outcome", "dispatch", "pack")
 

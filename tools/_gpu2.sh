@@ -1,4 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
-for agg in 1 0; do for e in 2 4 8 16; do echo -n "agg $agg ept $e: "; BS_HIST_AGG=$agg BS_HIST_EPT=$e python tools/stage_profile.py --config c2 | python -c "import json,sys; print(json.loads(sys.stdin.read())['stage_us']['histogram'])"; done; done
-for agg in 1 0; do for e in 4 16; do echo -n "c3 agg $agg ept $e: "; BS_HIST_AGG=$agg BS_HIST_EPT=$e python tools/stage_profile.py --config c3 | python -c "import json,sys; print(json.loads(sys.stdin.read())['stage_us']['histogram'])"; done; done
-for agg in 1 0; do echo -n "c4 agg $agg: "; BS_HIST_AGG=$agg BS_HIST_EPT=4 python tools/stage_profile.py --config c4 | python -c "import json,sys; print(json.loads(sys.stdin.read())['stage_us']['histogram'])"; done
+for v in 1 14; do for c in c2 c3 c4; do echo -n "$c variant $v: "; BS_PACK_VARIANT=$v python tools/stage_profile.py --config $c | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['stage_us']['pack'])"; done; done
+BS_PACK_VARIANT=14 python -m pytest tests/test_gpu_parity.py -q -x -k "fixture or c2 or c4" 2>&1 | tail -1

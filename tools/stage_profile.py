@@ -17,6 +17,7 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--no-pack", action="store_true")
 ap.add_argument("--dispatch", action="store_true")
+ap.add_argument("--no-mask", action="store_true")
 a = ap.parse_args()
 cfg, lens_np, cls_np = W.make_window(a.config, n=a.n, seed=1234)
 dev = torch.device("cuda", 0)
@@ -29,7 +30,7 @@ s = WindowScheduler(max_requests=len(lens_np), max_seq_len=cfg.l_max, n_classes=
                     policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
                     buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
                     current_safe=cfg.current_safe, accounting=cfg.accounting, device=dev,
-                    dispatch=a.dispatch)
+                    dispatch=a.dispatch, with_mask=not a.no_mask)
 r = s.schedule(lens, cls, tok_off, tokens)
 for _ in range(3):
     s.schedule(lens, cls, tok_off, tokens, sync=False)
