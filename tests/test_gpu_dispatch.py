@@ -134,3 +134,23 @@ def test_gpu_dispatch_graph_replay_and_reuse():
     assert np.array_equal(seq, ref2["disp_ids"])
     sched.close()
     sched2.close()
+
+
+@pytest.mark.parametrize("classes,pledged", [(2, 0), (3, 0), (2, 1)])
+def test_gpu_dispatch_multi_cta_path(classes, pledged):
+    """More than 8,192 form_batch calls: the cooperative multi-CTA path (chunked key
+    scan, onesweep radix passes, grid barriers) against the oracle."""
+    rng = np.random.default_rng(40 + classes + pledged)
+    n = 120_000
+    lens = np.clip(np.rint(rng.lognormal(4.0, 1.0, n)), 1, 1023).astype(np.int32)
+    cls = rng.integers(0, classes, size=n).astype(np.uint8)
+    kvpt = 2
+    spec = dict(l_max=1024, n_classes=classes, policies=(0,) + (1,) * (classes - 1),
+                theta=0.5, adjust=True, max_passes=0, init_edges=None, kvpt=kvpt,
+                current_safe=kvpt * 1200, pledged=kvpt * 200 * pledged, accounting=0,
+                truncate=True)
+    sched = _sched(spec, n)
+    h = sched.schedule(lens, cls).to_host()
+    assert len(h["batches"]) > 8192
+    _check_vs_oracle(spec, lens, cls, h)
+    sched.close()
