@@ -3,7 +3,7 @@
 // No reference counterpart (bucketsim never holds token ids); the layout is the
 // one the memory model charges: a batch is padded to its max_input_len
 // (batch_controller.py:136-139, the PADDED footprint), stored with row pitch
-// round_up(max_input_len, 4) so every row is 16-byte aligned; padding carries
+// round_up(max_input_len, 32) so every row starts on a 128-byte line; padding carries
 // pad_id and mask 0, so the padding fraction of [n, max_input_len] equals the
 // batch's waste_ratio (memory_model.py:92-100).
 //
@@ -26,6 +26,26 @@ constexpr int kPackThreads = 256;
 __device__ __forceinline__ uint32_t mask_word(int32_t k) {
   // bytes 0..3 = 1 for the first k (0..4) entries
   return k >= 4 ? 0x01010101u : (k <= 0 ? 0u : (0x01010101u >> (8 * (4 - k))));
+}
+
+// mask bytes of 4-token words [vb, ve) of a row with x real tokens: 16-byte stores on
+// the 16-byte-aligned part (rows start 4-byte aligned), 4-byte stores on the ends
+__device__ __forceinline__ void store_mask_range(uint8_t* mrow, int32_t x, int32_t vb, int32_t ve,
+                                                 int lane) {
+  uint32_t* m4 = reinterpret_cast<uint32_t*>(mrow);
+  const int32_t head = (int32_t)((4 - (((reinterpret_cast<uintptr_t>(mrow) >> 2) + vb) & 3)) & 3);
+  const int32_t a = vb + head < ve ? vb + head : ve;  // first 16-byte-aligned word
+  const int32_t nbody = (ve - a) >> 2;
+  const int32_t t0 = a + 4 * nbody;                   // tail words [t0, ve)
+  if (lane < a - vb) st_stream_u32(m4 + vb + lane, mask_word(x - 4 * (vb + lane)));
+  for (int32_t c = lane; c < nbody; c += 32) {
+    const int32_t w = a + 4 * c;
+    const int32_t k = x - 4 * w;
+    st_stream_v4(reinterpret_cast<int4*>(m4 + w),
+                 make_int4((int)mask_word(k), (int)mask_word(k - 4), (int)mask_word(k - 8),
+                           (int)mask_word(k - 12)));
+  }
+  if (lane < ve - t0) st_stream_u32(m4 + t0 + lane, mask_word(x - 4 * (t0 + lane)));
 }
 
 // copy columns [4*vb, 4*ve) of one row (x real tokens, pad beyond); kU vectors of
@@ -58,10 +78,10 @@ __device__ __forceinline__ void copy_row_range(const int32_t* src, int32_t* dst,
             if (rem > 2) val.z = src[4 * v + 2];
           }
           st_stream_v4(d4 + v, val);
-          if (m4) st_stream_u32(m4 + v, mask_word(x - 4 * v));
         }
       }
     }
+    if (m4) store_mask_range(mdst, x, vb, ve, lane);
   } else {  // token row not 16-byte aligned: scalar path
     for (int32_t t = 4 * vb + lane; t < 4 * ve; t += 32) {
       dst[t] = t < x ? src[t] : pad_id;
