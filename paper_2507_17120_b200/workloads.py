@@ -112,9 +112,11 @@ _HASH_MUL = 2654435761
 
 
 def token_store(lens: np.ndarray, rng: np.random.Generator | None = None, vocab: int = 32000,
-                align: int = 4, seed: int = 0):
-    """CSR token store: row i starts at tok_off[i] (multiple of `align` tokens so
-    rows are 16-byte aligned for 128-bit loads) and holds lens[i] synthetic ids.
+                align: int = 32, seed: int = 0):
+    """CSR token store: row i starts at tok_off[i] (multiple of `align` tokens: with the
+    default 32 every row starts on a 128-byte line, the TMA-friendly layout SURVEY §8f
+    recommends; measured 790 vs 798 us for C2's pack against 16-byte alignment) and
+    holds lens[i] synthetic ids.
     Token at global slot p is ((p * 2654435761 + seed) mod 2^32) mod vocab."""
     lens = np.asarray(lens, np.int64)
     pitch = (lens + align - 1) // align * align
@@ -128,7 +130,7 @@ def token_store(lens: np.ndarray, rng: np.random.Generator | None = None, vocab:
     return tok_off, pos.view(np.int32)
 
 
-def token_store_device(lens, vocab: int = 32000, align: int = 4, seed: int = 0):
+def token_store_device(lens, vocab: int = 32000, align: int = 32, seed: int = 0):
     """Same store as token_store(), generated on the GPU (torch tensors)."""
     import torch
     lens = lens.to(torch.int64)
