@@ -196,6 +196,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=131_072)
     ap.add_argument("--dispatch", action="store_true", help="also compute the simulator's "
                     "global dispatch order (K7, SURVEY f3) inside every window")
+    ap.add_argument("--inflight", type=int, default=2, help="windows in flight: consecutive "
+                    "windows alternate over this many schedulers (own scratch, outputs and CUDA "
+                    "stream), so the latency-bound scheduling of one window overlaps the "
+                    "HBM-bound pack of the previous one")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -250,13 +254,50 @@ def main():
     stage_ms, prof_steps = sched.ctx.profile_read()
     stage_ms = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
     sched.ctx.profile_enable(0)
-    for _ in range(args.warmup):
-        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False, graph=use_graph)
+    # windows in flight: scheduler k (own context, outputs, stream) takes windows k, k+I, ...
+    inflight = max(1, args.inflight)
+    scheds = [sched] + [
+        WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
+                        policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
+                        buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
+                        current_safe=cfg.current_safe, accounting=cfg.accounting, device=dev,
+                        process_group=pg, dispatch=args.dispatch, pack_capacity=sched.pack_capacity)
+        for _ in range(inflight - 1)]
+    streams = [torch.cuda.Stream(dev) for _ in range(inflight)]
+
+    def run_windows(k_steps, n_inflight):
+        cur = torch.cuda.current_stream(dev)
+        for st in streams:
+            st.wait_stream(cur)
+        for i in range(k_steps):
+            q = i % n_inflight
+            with torch.cuda.stream(streams[q]):
+                scheds[q].schedule(lens, cls, tok_off, tokens, sync=False, check=False,
+                                   graph=use_graph)
+        for st in streams:
+            cur.wait_stream(st)
+
+    for q in range(inflight):
+        with torch.cuda.stream(streams[q]):
+            for _ in range(args.warmup):
+                scheds[q].schedule(lens, cls, tok_off, tokens, sync=False, check=False,
+                                   graph=use_graph)
     torch.cuda.synchronize(dev)
+    # one window at a time (latency per window, reported beside the throughput)
+    lat0 = torch.cuda.Event(enable_timing=True)
+    lat1 = torch.cuda.Event(enable_timing=True)
+    lat_steps = max(3, min(args.steps, 50))
+    if pg is not None:
+        dist.barrier()
+    lat0.record()
+    run_windows(lat_steps, 1)
+    lat1.record()
+    torch.cuda.synchronize(dev)
+    window_latency_ms = lat0.elapsed_time(lat1) / lat_steps
 
     # ---------------- timed region: device-resident windows ----------------------
     sampler = ClockSampler(local)
-    l0 = sched.ctx.launches
+    l0 = sum(x.ctx.launches for x in scheds)
     if pg is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -265,20 +306,19 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
-    for _ in range(args.steps):
-        sched.schedule(lens, cls, tok_off, tokens, sync=False, check=False, graph=use_graph)
+    run_windows(args.steps, inflight)
     ev1.record()
     torch.cuda.synchronize(dev)
     clocks = sampler.stop()
     if pg is not None:
         dist.barrier()
-    launches = sched.ctx.launches - l0
+    launches = sum(x.ctx.launches for x in scheds) - l0
     if use_graph:  # graph replays do not pass through the host launchers: count per window
         launches = kernels_per_window * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
-    res = sched.schedule(lens, cls, tok_off, tokens)  # check the steady-state result
-    s = res.summary()
-    assert s["n_batches"] == s0["n_batches"] and s["packed_elems"] == s0["packed_elems"]
+    for x in scheds:  # check the steady-state result of every scheduler
+        s = x.schedule(lens, cls, tok_off, tokens).summary()
+        assert s["n_batches"] == s0["n_batches"] and s["packed_elems"] == s0["packed_elems"]
 
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if pg is not None:
@@ -363,6 +403,8 @@ def main():
             "kv_bytes_per_token": cfg.kvpt, "safe_memory_bytes": cfg.current_safe,
             "accounting": "padded" if cfg.accounting == 0 else "exact",
             "parallelism": f"dp{world} (request shards, NCCL histogram all-reduce)",
+            "pipeline": f"{inflight} windows in flight (one scheduler context + CUDA stream each); "
+                        "ms_per_step = timed region / steps",
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
                   % (tokens.numel() * 4 / 1e9, int(s["packed_elems"]) * 5 / 1e9),
         },
@@ -380,6 +422,8 @@ def main():
         "cpu_baseline": cpu_base,
         "gpu_launches": launches,
         "cuda_graph": use_graph,
+        "inflight": inflight,
+        "window_latency_ms": window_latency_ms,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -559,6 +559,7 @@ static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t*
   static int per_sm = 0;
   if (per_sm == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack<kU, kMinB>, kPackThreads, 0);
+    if (per_sm > kMinB) per_sm = kMinB;  // kMinB CTAs per SM: the rest of the SM stays free
     if (per_sm < 1) per_sm = 1;
   }
   const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
@@ -597,6 +598,8 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     case 8: BS_PACK_R(2, 6, 8);
     case 9: BS_PACK_R(4, 6, 4);
     case 10: BS_PACK_R(1, 16, 8);
+    case 15: BS_PACK_V(4, 4);
+    case 16: BS_PACK_V(4, 3);
 #undef BS_PACK_R
     case 5:
       return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
