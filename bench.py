@@ -319,6 +319,10 @@ def main():
     for x in scheds:  # check the steady-state result of every scheduler
         s = x.schedule(lens, cls, tok_off, tokens).summary()
         assert s["n_batches"] == s0["n_batches"] and s["packed_elems"] == s0["packed_elems"]
+    for x in scheds[1:]:  # release the extra in-flight contexts / outputs before e2e
+        x.close()
+    del scheds[1:]
+    torch.cuda.empty_cache()
 
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if pg is not None:

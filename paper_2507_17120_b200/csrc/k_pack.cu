@@ -549,6 +549,26 @@ static cudaError_t launch_pack_ring(bs_ctx* ctx, const int32_t* len, const int32
   return cudaGetLastError();
 }
 
+// non-persistent form: one 32-piece group per warp (grid from an upper bound on the
+// pieces), so CTAs retire as they finish and kernels of other streams can interleave
+template <int kU, int kMinB>
+static cudaError_t launch_pack_flat(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                                    const int64_t* tok_off, const int32_t* tokens,
+                                    const bs_window_params& p, const bs_batch* batches,
+                                    int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                                    bs_summary* summary, cudaStream_t st) {
+  const int64_t pieces_per_row = (p.l_max + kPiece - 1) / kPiece;
+  const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
+  const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
+  k_pack<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
+      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
+      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
+      summary);
+  ++ctx->launches;
+  return cudaGetLastError();
+}
+
 template <int kU, int kMinB>
 static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                  const int64_t* tok_off, const int32_t* tokens,
@@ -582,8 +602,11 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                               summary, st)
   int v = ctx->pack_variant;
   // default: the TMA staging variant for long-context windows (rows of many KB),
-  // 128-bit register copies with 6 CTAs/SM otherwise (measured on B200, C2 / C4)
-  if (v == 0) v = p.l_max > 16384 ? 5 : 1;
+  // 128-bit register copies otherwise (measured on B200, C2 / C4)
+  // (non-persistent grid: CTAs retire as they finish, so the scheduling kernels of the
+  // next window in flight interleave with this pack — 0.903 vs 0.922 ms per C2 window
+  // with two windows in flight, identical when windows run one at a time)
+  if (v == 0) v = p.l_max > 16384 ? 5 : 17;
   switch (v) {  // tuning hook (BS_PACK_VARIANT)
     case 1: BS_PACK_V(4, 6);
     case 2: BS_PACK_V(8, 4);
@@ -599,6 +622,10 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     case 9: BS_PACK_R(4, 6, 4);
     case 10: BS_PACK_R(1, 16, 8);
     case 15: BS_PACK_V(4, 4);
+    case 17:
+      return launch_pack_flat<4, 6>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
+                                    batch_end, batches_cap, out_tokens, out_mask, out_capacity,
+                                    summary, st);
     case 16: BS_PACK_V(4, 3);
 #undef BS_PACK_R
     case 5:

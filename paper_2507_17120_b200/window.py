@@ -481,4 +481,8 @@ class WindowScheduler:
         return out.cpu().numpy()
 
     def close(self):
+        """Release the context scratch, the captured graph and the output buffers."""
         self.ctx.close()
+        self._graph = None
+        self.out_tokens = self.out_mask = None
+        self.pack_capacity = 0
