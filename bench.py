@@ -217,11 +217,18 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; ranks beyond the visible GPUs share them round-robin (lets the
+    # distributed path run on a one-GPU box with BS_DIST_BACKEND=gloo)
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist.group.WORLD
     from paper_2507_17120_b200.window import WindowScheduler
 
@@ -296,7 +303,7 @@ def main():
     window_latency_ms = lat0.elapsed_time(lat1) / lat_steps
 
     # ---------------- timed region: device-resident windows ----------------------
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local_dev)
     l0 = sum(x.ctx.launches for x in scheds)
     if pg is not None:
         dist.barrier()
@@ -406,7 +413,8 @@ def main():
             "l_max": cfg.l_max, "classes": cfg.n_classes,
             "kv_bytes_per_token": cfg.kvpt, "safe_memory_bytes": cfg.current_safe,
             "accounting": "padded" if cfg.accounting == 0 else "exact",
-            "parallelism": f"dp{world} (request shards, NCCL histogram all-reduce)",
+            "parallelism": f"dp{world} (request shards, "
+                           f"{os.environ.get('BS_DIST_BACKEND', 'nccl').upper()} histogram all-reduce)",
             "pipeline": f"{inflight} windows in flight (one scheduler context + CUDA stream each); "
                         "ms_per_step = timed region / steps",
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
