@@ -230,7 +230,8 @@ int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int64_t*
  * blocked drain under pledged memory, or zero token mass).  Requests of calls the
  * loop never reaches are rewritten to BS_REQ_PENDING in req_batch / req_row and the
  * summary's n_rejected / n_pending follow.  Uses the drain of the last bs_size call
- * on ctx (same perm / seg_off / batches). */
+ * on ctx (same perm / seg_off / batches), which must have been made with
+ * p->dispatch = 1 (it then also records the per-call keys K7 sorts). */
 int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_t n,
                 const bs_window_params* p, const bs_batch* batches, int32_t batches_cap,
                 int32_t* req_batch, int32_t* req_row, int32_t* emit_order, int32_t* batch_emit,

@@ -361,6 +361,9 @@ int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_
   if (!summary || !batches || batches_cap < 0 || !emit_order || !batch_emit ||
       (n > 0 && (!perm || !seg_off || !req_batch || !req_row)))
     return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  if (!p->dispatch)
+    return fail(ctx, BS_ERR_INVALID_ARG,
+                "bs_dispatch needs the bs_size call before it made with params.dispatch = 1");
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   BS_CUDA(bsk::launch_dispatch(ctx, perm, seg_off, n, *p, batches, batches_cap, req_batch, req_row,
                                emit_order, batch_emit, summary, static_cast<cudaStream_t>(stream)),
