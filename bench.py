@@ -352,10 +352,14 @@ def main():
     if not args.no_e2e:
         h_lens = lens.cpu().pin_memory()
         h_cls = cls.cpu().pin_memory()
-        h_off = tok_off.cpu().pin_memory()
-        h_tok = tokens.cpu().pin_memory()
+        # the host token store is packed densely (rows 16-byte aligned, the smallest layout
+        # the 128-bit pack path accepts) so the PCIe copy moves no padding
+        e_off, e_tok = W.token_store_device(lens, seed=rank, align=4)
+        h_off = e_off.cpu().pin_memory()
+        h_tok = e_tok.cpu().pin_memory()
+        del e_off, e_tok
         d_lens, d_cls = torch.empty_like(lens), torch.empty_like(cls)
-        d_off, d_tok = torch.empty_like(tok_off), torch.empty_like(tokens)
+        d_off, d_tok = torch.empty_like(h_off, device=dev), torch.empty_like(h_tok, device=dev)
         nb = int(s["n_batches"])
         h_rb = torch.empty(n, dtype=torch.int32).pin_memory()
         h_bt = torch.empty(64 * nb, dtype=torch.uint8).pin_memory()
