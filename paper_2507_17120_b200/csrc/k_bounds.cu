@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(256)
 // pass d+1 iff its parent split, so every pass costs one level of work and the
 // change log is one scan over the split flags in heap (= pass-major, left-to-right)
 // order — exactly the reference's emission order.  Other modes run the general
-// pass loop.  Lookup tables and digit counts are built by the same CTA.
+// pass loop.  The per-length LUT, radix slots and digit counts are then built grid-wide
+// by k_tables from the published edge bitmask.
 constexpr int kSmallL = 16384;
 constexpr int kMaxDepth = 15;  // ceil(log2(kSmallL)) + 1
 
@@ -418,10 +419,10 @@ __global__ void __launch_bounds__(kBT, 1)
                    uint32_t* __restrict__ PcL, int32_t* __restrict__ gE,
                    int32_t* __restrict__ seg_base, int32_t* __restrict__ lut,
                    uint32_t* __restrict__ slot_lut, uint32_t* __restrict__ bins_cnt,
-                   int32_t* __restrict__ kinfo, bs_summary* sum, int32_t* __restrict__ slot_seg) {
+                   int32_t* __restrict__ kinfo, bs_summary* sum, int32_t* __restrict__ slot_seg,
+                   uint32_t* __restrict__ gbm, uint32_t* __restrict__ gwp) {
   extern __shared__ uint32_t dyn[];
   __shared__ BoundsShared sh;
-  __shared__ uint32_t sbins[4 * 256];
   __shared__ int32_t s_flag;
   const int32_t L = p.l_max, C = p.n_classes;
   const int W = (L + 1 + 31) / 32;
@@ -493,7 +494,6 @@ __global__ void __launch_bounds__(kBT, 1)
   }
   for (int w = tid; w < W; w += kBT) bm[w] = 0;
   for (int w = tid; w < NW; w += kBT) split_bits[w] = 0;
-  for (int i = tid; i < 4 * 256; i += kBT) sbins[i] = 0;
   if (tid == 0) { sh.bad = 0; s_flag = 0; }
   __syncthreads();
   const int64_t n_max = sh.n_max;
@@ -647,18 +647,16 @@ __global__ void __launch_bounds__(kBT, 1)
   const int32_t K = compact_edges(bm, W, E, sh);
   for (int i = tid; i <= K; i += kBT) { edges_out[i] = E[i]; gE[i] = E[i]; }
 
+  // ---- edge bitmask + popc prefix for the parallel tables kernel (k_tables) -------------
+  {
+    const uint32_t v = tid < W ? bm[tid] : 0u;
+    uint32_t tw;
+    const uint32_t o = block_excl_scan<uint32_t>(__popc(v), sh.s32, &tw);
+    for (int w = tid; w < W; w += kBT) gbm[w] = bm[w];
+    if (tid < W) gwp[tid] = o;
+  }
   // ---- E. segment offsets (local per-class counts) and radix slot bases -------------
   const int32_t S = K * C;
-  // ---- D. per-length bucket LUT (K3): largest b with E[b] <= x ----------------------
-  for (int x = tid; x < L; x += kBT) {
-    // binary search over E (smem): largest b with E[b] <= x
-    int32_t lo = 0, hi = K;
-    while (hi - lo > 1) {
-      const int32_t mid = (lo + hi) >> 1;
-      if (E[mid] <= x) lo = mid; else hi = mid;
-    }
-    lut[x] = lo;
-  }
   __syncthreads();
   int32_t run_cnt = 0, run_w = 0;
   for (int base = 0; base < S; base += kBT) {
@@ -683,24 +681,8 @@ __global__ void __launch_bounds__(kBT, 1)
   }
   if (tid == 0) seg_off_out[S] = run_cnt;
   __syncthreads();
-  // ---- F. radix slots per (class, length) + digit counts --------------------------------
-  const uint32_t dmask = (1u << sort_bits) - 1u;
-  for (int64_t idx = tid; idx < (int64_t)C * L; idx += kBT) {
-    const int c = (int)(idx / L), x = (int)(idx % L);
-    const int b = lut[x];
-    const int pol = p.policy[c];
-    uint32_t slot = (uint32_t)seg_base[b * C + c];
-    if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - E[b]);
-    else if (pol == BS_POLICY_LJF) slot += (uint32_t)(E[b + 1] - 1 - x);
-    slot_lut[idx] = slot;
-    slot_seg[slot] = b * C + c;
-    const uint32_t h = hist_local[idx];
-    if (h)  // consecutive lengths hit distinct low digits: plain shared atomics
-      for (int q = 0; q < sort_passes; ++q)
-        atomicAdd(&sbins[q * 256 + ((slot >> (q * sort_bits)) & dmask)], h);
-  }
-  __syncthreads();
-  for (int i = tid; i < 4 * 256; i += kBT) bins_cnt[i] = sbins[i];
+  // lookup tables and digit counts: k_tables (grid-wide) reads gbm / gwp / gE / seg_base
+  for (int i = tid; i < 4 * 256; i += kBT) bins_cnt[i] = 0;
   if (tid == 0) {
     kinfo[0] = K;
     kinfo[1] = run_w;
@@ -741,8 +723,16 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
                                          sp.bits, sp.passes, init_edges, k_init, edges_out,
                                          changes_out, changes_cap, seg_off_out, ctx->PcL, ctx->E,
                                          ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
-                                         ctx->kinfo, summary, ctx->slot_seg);
-    ++ctx->launches;
+                                         ctx->kinfo, summary, ctx->slot_seg, ctx->bmw, ctx->wp);
+    cudaError_t e0 = cudaGetLastError();
+    if (e0 != cudaSuccess) return e0;
+    const int64_t cells = (int64_t)C * L;
+    const unsigned tb = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((cells + 255) / 256, 4LL * ctx->num_sms));
+    k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
+                                 ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
+                                 ctx->slot_seg);
+    ctx->launches += 2;
     return cudaGetLastError();
   }
   const int ntiles = (L + kTileX - 1) / kTileX;
