@@ -184,3 +184,30 @@ def test_schedule_requests_matches_reference_fixture(name, dispatch):
     assert sorted(r.id for r in out.pending) == ref["pending"].tolist()
     assert out.n_max == int(ref["n_max"])
     assert out.bucket_set.edges() == ref["edges"].tolist()
+
+
+def test_trace_file_to_gpu_window(tmp_path):
+    """f4 -> hot path: a reference-format CSV trace parsed by the native loader feeds the
+    window scheduler; the result equals scheduling the same requests as objects."""
+    from paper_2507_17120_b200 import trace as T
+    rng = np.random.default_rng(3)
+    n = 5000
+    rows = ["arrival_s,input_tokens,output_tokens,class"]
+    arr = np.cumsum(rng.exponential(0.01, n))
+    lens = np.clip(np.rint(rng.lognormal(5.5, 1.1, n)), 1, 5000).astype(int)
+    cl = rng.random(n) < 0.4
+    for a, x, c in zip(arr, lens, cl):
+        rows.append(f"{float(a)!r},{int(x)},16,{'online' if c else 'offline'}")
+    p = tmp_path / "t.csv"
+    p.write_text("\n".join(rows) + "\n")
+    tr = T.load_trace_path(p)
+    model = ModelConfig(16, 8, 64, 2, 4096)
+    gpu = GpuConfig(8 << 30, 2 << 30, 0.1)
+    out = schedule_requests(tr.requests(), model, gpu)
+    from paper_2507_17120_b200.window import WindowScheduler
+    s = WindowScheduler(model, gpu, max_requests=n)
+    wl, wc = tr.window(model.max_seq_len)
+    res = s.schedule(wl, wc)
+    assert [len(p_) for p_ in out.plans] == res.batches()["n"].tolist()
+    assert out.bucket_set.edges() == res.edges().tolist()
+    s.close()

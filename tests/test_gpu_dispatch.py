@@ -154,3 +154,15 @@ def test_gpu_dispatch_multi_cta_path(classes, pledged):
     assert len(h["batches"]) > 8192
     _check_vs_oracle(spec, lens, cls, h)
     sched.close()
+
+
+def test_gpu_dispatch_long_context_c4():
+    """C4 shape (l_max 131,072: bucket ids need the full 17 key bits) vs the oracle."""
+    cfg, lens, cls = W.make_window("c4", n=20_000, seed=3)
+    spec = dict(l_max=cfg.l_max, n_classes=cfg.n_classes, policies=cfg.policies,
+                theta=cfg.theta, adjust=cfg.adjust, max_passes=0, init_edges=cfg.init_edges,
+                kvpt=cfg.kvpt, current_safe=cfg.current_safe, pledged=0,
+                accounting=cfg.accounting, truncate=True)
+    sched = _sched(spec, len(lens))
+    _check_vs_oracle(spec, lens, cls, sched.schedule(lens, cls).to_host())
+    sched.close()
