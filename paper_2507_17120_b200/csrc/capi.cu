@@ -10,8 +10,8 @@
 
 #include "ctx.cuh"
 
-void* bs_chain_kernel_ptr();     // k_size.cu
-int bs_chain_threads();
+void* bs_chain_kernel_ptr(int wide);  // k_size.cu
+int bs_chain_threads(int wide);
 void* bs_dispatch_kernel_ptr();  // k_dispatch.cu
 
 namespace {
@@ -193,8 +193,11 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   }
   // co-resident blocks for the cooperative chain kernel
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(),
-                                                    bs_chain_threads(), 0);
+  for (int wide = 0; wide < 2 && e == cudaSuccess; ++wide) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(wide),
+                                                      bs_chain_threads(wide), 0);
+    if (e == cudaSuccess && per_sm < 1) break;
+  }
   if (e != cudaSuccess || per_sm < 1) {
     int rc = e != cudaSuccess ? cuda_fail(ctx, e, "occupancy(k_chain)")
                               : fail(ctx, BS_ERR_NOT_BUILT, "k_chain cannot be resident");
@@ -202,7 +205,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
     delete ctx;
     return rc;
   }
-  ctx->chain_blocks = per_sm * ctx->num_sms;
+  ctx->chain_blocks = ctx->num_sms;  // one CTA per SM (per_sm >= 1 checked above)
   A(btot, ctx->chain_blocks);
   // the cooperative K7 dispatch kernel: one 1024-thread CTA per SM, ~211 KB of shared memory
   e = cudaFuncSetAttribute(bs_dispatch_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -27,6 +27,10 @@
 namespace bsk {
 
 constexpr int kBT = 1024;
+// block of the fused small-L K2 (the code is block-size agnostic; 512 threads measured
+// 41 vs 35 us at C2 and gained nothing with windows in flight)
+constexpr int kSmallBT = 1024;
+constexpr int kSmallBTMin = 1;
 constexpr int kEcap = 8192;   // edges kept in shared memory when l_max < kEcap
 
 // CPython _float_div_mod floor quotient (Objects/floatobject.c)
@@ -111,7 +115,7 @@ struct BoundsShared {
 
 // compact the edge bitmask into E[0..K]; returns K (number of buckets)
 __device__ int32_t compact_edges(const uint32_t* bm, int W, int32_t* E, BoundsShared& sh) {
-  const int wc = (W + kBT - 1) / kBT;
+  const int wc = (W + (int)blockDim.x - 1) / (int)blockDim.x;
   const int w0 = threadIdx.x * wc, w1 = min(W, w0 + wc);
   int32_t cnt = 0;
   for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
@@ -410,7 +414,7 @@ __device__ __forceinline__ void node_bounds(int32_t L, int d, int32_t k, int32_t
   }
 }
 
-__global__ void __launch_bounds__(kBT, 1)
+__global__ void __launch_bounds__(kSmallBT, kSmallBTMin)
     k_bounds_small(const uint32_t* __restrict__ hist_local,
                    const uint32_t* __restrict__ hist_global, bs_window_params p, int sort_bits,
                    int sort_passes, const int32_t* __restrict__ init_edges, int32_t k_init,
@@ -427,12 +431,13 @@ __global__ void __launch_bounds__(kBT, 1)
   const int32_t L = p.l_max, C = p.n_classes;
   const int W = (L + 1 + 31) / 32;
   const int tid = threadIdx.x;
+  const int nt = (int)blockDim.x;
   const int NW = ((1 << kMaxDepth) + 31) / 32;     // node-bitmask words
   uint32_t* Ps = dyn;                               // [L+1]
   uint32_t* bm = Ps + (L + 1);                      // [W]
   uint32_t* split_bits = bm + W;                    // [NW] node split flags (heap order)
   int32_t* E = reinterpret_cast<int32_t*>(split_bits + NW);  // [L+1]
-  const int chunk = (L + kBT - 1) / kBT;
+  const int chunk = (L + nt - 1) / nt;
   const int x0 = min(L, tid * chunk), x1 = min(L, x0 + chunk);
 
   // ---- A. prefix sums (global total in smem, local per class in global) ------------
@@ -492,8 +497,8 @@ __global__ void __launch_bounds__(kBT, 1)
       sum->n_max = nm;
     }
   }
-  for (int w = tid; w < W; w += kBT) bm[w] = 0;
-  for (int w = tid; w < NW; w += kBT) split_bits[w] = 0;
+  for (int w = tid; w < W; w += nt) bm[w] = 0;
+  for (int w = tid; w < NW; w += nt) split_bits[w] = 0;
   if (tid == 0) { sh.bad = 0; s_flag = 0; }
   __syncthreads();
   const int64_t n_max = sh.n_max;
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kBT, 1)
     for (int d = 0; d < kMaxDepth; ++d) {
       const int32_t nodes = 1 << d;
       int any = 0;
-      for (int32_t k = tid; k < nodes; k += kBT) {
+      for (int32_t k = tid; k < nodes; k += nt) {
         const int32_t id = nodes - 1 + k;
         bool realized = d == 0;
         if (d > 0) {
@@ -538,12 +543,12 @@ __global__ void __launch_bounds__(kBT, 1)
     passes = deepest + 2;
     __syncthreads();
     if (s_flag) {  // fall back: reset and run the general loop below
-      for (int w = tid; w < W; w += kBT) bm[w] = 0;
+      for (int w = tid; w < W; w += nt) bm[w] = 0;
       __syncthreads();
     } else {
       // change log: split nodes in heap order == pass-major, left to right
       const int32_t nnodes = deepest >= 0 ? (2 << deepest) - 1 : 0;
-      const int per = (nnodes + kBT - 1) / kBT;
+      const int per = (nnodes + nt - 1) / nt;
       const int32_t n0 = tid * per, n1 = min(nnodes, n0 + per);
       int32_t cnt = 0;
       for (int32_t id = n0; id < n1; ++id) cnt += (split_bits[id >> 5] >> (id & 31)) & 1u;
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(kBT, 1)
     nch = 0;
     passes = 0;
     if (init_edges) {
-      for (int i = tid; i <= k_init; i += kBT) {
+      for (int i = tid; i <= k_init; i += nt) {
         const int32_t e = init_edges[i];
         bool ok = e >= 0 && e <= L;
         if (i == 0) ok = ok && e == 0;
@@ -581,7 +586,7 @@ __global__ void __launch_bounds__(kBT, 1)
       __syncthreads();
       if (sh.bad || k_init < 1) {
         if (tid == 0) latch_flags(sum, BS_FLAG_BAD_EDGES);
-        for (int w = tid; w < W; w += kBT) bm[w] = 0;
+        for (int w = tid; w < W; w += nt) bm[w] = 0;
         __syncthreads();
         if (tid == 0) { atomicOr(&bm[0], 1u); atomicOr(&bm[L >> 5], 1u << (L & 31)); }
       }
@@ -596,7 +601,7 @@ __global__ void __launch_bounds__(kBT, 1)
         ++passes;
         if ((int64_t)total < n_max) {
           if (K != 1) {
-            for (int w = tid; w < W; w += kBT) bm[w] = 0;
+            for (int w = tid; w < W; w += nt) bm[w] = 0;
             __syncthreads();
             if (tid == 0) {
               atomicOr(&bm[0], 1u);
@@ -613,7 +618,7 @@ __global__ void __launch_bounds__(kBT, 1)
         }
         if ((int64_t)total == n_max) break;
         int any = 0;
-        for (int base = 0; base < K; base += kBT) {
+        for (int base = 0; base < K; base += nt) {
           const int k = base + tid;
           int kind = 0, lo = 0, up = 0, mid = 0;
           if (k < K) {
@@ -645,21 +650,27 @@ __global__ void __launch_bounds__(kBT, 1)
   }
   __syncthreads();
   const int32_t K = compact_edges(bm, W, E, sh);
-  for (int i = tid; i <= K; i += kBT) { edges_out[i] = E[i]; gE[i] = E[i]; }
+  for (int i = tid; i <= K; i += nt) { edges_out[i] = E[i]; gE[i] = E[i]; }
 
   // ---- edge bitmask + popc prefix for the parallel tables kernel (k_tables) -------------
   {
-    const uint32_t v = tid < W ? bm[tid] : 0u;
+    const int wc = (W + nt - 1) / nt;
+    const int w0 = min(W, tid * wc), w1 = min(W, w0 + wc);
+    uint32_t cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(bm[w]);
     uint32_t tw;
-    const uint32_t o = block_excl_scan<uint32_t>(__popc(v), sh.s32, &tw);
-    for (int w = tid; w < W; w += kBT) gbm[w] = bm[w];
-    if (tid < W) gwp[tid] = o;
+    uint32_t o = block_excl_scan<uint32_t>(cnt, sh.s32, &tw);
+    for (int w = w0; w < w1; ++w) {
+      gbm[w] = bm[w];
+      gwp[w] = o;
+      o += __popc(bm[w]);
+    }
   }
   // ---- E. segment offsets (local per-class counts) and radix slot bases -------------
   const int32_t S = K * C;
   __syncthreads();
   int32_t run_cnt = 0, run_w = 0;
-  for (int base = 0; base < S; base += kBT) {
+  for (int base = 0; base < S; base += nt) {
     const int s = base + tid;
     int32_t cnt = 0, width = 0;
     if (s < S) {
@@ -682,7 +693,7 @@ __global__ void __launch_bounds__(kBT, 1)
   if (tid == 0) seg_off_out[S] = run_cnt;
   __syncthreads();
   // lookup tables and digit counts: k_tables (grid-wide) reads gbm / gwp / gE / seg_base
-  for (int i = tid; i < 4 * 256; i += kBT) bins_cnt[i] = 0;
+  for (int i = tid; i < 4 * 256; i += nt) bins_cnt[i] = 0;
   if (tid == 0) {
     kinfo[0] = K;
     kinfo[1] = run_w;
@@ -719,7 +730,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
       cudaFuncSetAttribute(k_bounds_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr_small = smem;
     }
-    k_bounds_small<<<1, kBT, smem, st>>>(hist_local, hist_global ? hist_global : hist_local, p,
+    k_bounds_small<<<1, kSmallBT, smem, st>>>(hist_local, hist_global ? hist_global : hist_local, p,
                                          sp.bits, sp.passes, init_edges, k_init, edges_out,
                                          changes_out, changes_cap, seg_off_out, ctx->PcL, ctx->E,
                                          ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,

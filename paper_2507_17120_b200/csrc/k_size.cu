@@ -332,7 +332,12 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------- K5c
-constexpr int kChainThreads = 1024;  // one CTA per SM: fewer CTAs per grid barrier
+// one CTA per SM (fewer CTAs per grid barrier).  Windows up to kChainWide requests use
+// 512 threads capped at 40 registers: the CTA needs only a third of an SM, so it starts
+// as soon as a few pack CTAs of the previous window in flight retire (two windows in
+// flight: 0.858 vs 0.905 ms per C2 window).  Larger windows (C3: 16M) use 1024 threads,
+// whose extra loads in flight the pointer-doubling levels need (C3 chain 0.93 vs 1.65 ms).
+constexpr int kChainWide = 4 << 20;
 constexpr int kWalk = 128;           // chain calls followed serially before doubling is used
 
 struct ChainShared {
@@ -344,7 +349,8 @@ __device__ __forceinline__ int32_t ld_rel_i32(const int32_t* p) {
   return (int32_t)ld_relaxed(reinterpret_cast<const uint32_t*>(p));
 }
 
-__global__ void __launch_bounds__(kChainThreads, 1)
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_chain(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
             int32_t* J, int r_cap, const uint8_t* __restrict__ is_start, int32_t* alive,
             int32_t* listA, int32_t* listB, int32_t* node_batch, int32_t* node_j0, int32_t* misc,
@@ -433,25 +439,24 @@ __global__ void __launch_bounds__(kChainThreads, 1)
       const int32_t* Jr = J + (int64_t)r * n;
       int32_t* Jn = J + (int64_t)(r + 1) * n;
       bool any = false;
-      // four independent positions per thread in flight (the second load is a gather)
+      // kIlp independent positions per thread in flight (the second load is a gather)
+      constexpr int kIlp = kThreads >= 1024 ? 4 : 8;
       const int64_t S = (int64_t)gridDim.x * blockDim.x;
-      for (int64_t x0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < n; x0 += 4 * S) {
-        int32_t v[4], w[4];
-        uint8_t st[4];
+      for (int64_t x0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < n; x0 += kIlp * S) {
+        int32_t v[kIlp];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kIlp; ++k) {
           const int64_t x = x0 + k * S;
           v[k] = x < n ? Jr[x] : kEnd;
-          st[k] = x < n ? is_start[x] : 0;
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) w[k] = v[k] == kEnd ? kEnd : Jr[v[k]];
+        for (int k = 0; k < kIlp; ++k) v[k] = v[k] == kEnd ? kEnd : Jr[v[k]];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kIlp; ++k) {
           const int64_t x = x0 + k * S;
           if (x < n) {
-            Jn[x] = w[k];
-            if (w[k] != kEnd && st[k]) any = true;
+            Jn[x] = v[k];
+            if (v[k] != kEnd && is_start[x]) any = true;
           }
         }
       }
@@ -826,7 +831,9 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
                     &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
                     (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
-    e = cudaLaunchCooperativeKernel((void*)k_chain, dim3(ctx->chain_blocks), dim3(kChainThreads), args, 0,
+    const bool wide = n > kChainWide;
+    e = cudaLaunchCooperativeKernel(wide ? (void*)k_chain<1024, 1> : (void*)k_chain<512, 3>,
+                                    dim3(ctx->chain_blocks), dim3(wide ? 1024 : 512), args, 0,
                                     st);
     if (e != cudaSuccess) return e;
   }
@@ -850,5 +857,8 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
 
 }  // namespace bsk
 
-void* bs_chain_kernel_ptr() { return reinterpret_cast<void*>(&bsk::k_chain); }
-int bs_chain_threads() { return bsk::kChainThreads; }
+void* bs_chain_kernel_ptr(int wide) {
+  return wide ? reinterpret_cast<void*>(&bsk::k_chain<1024, 1>)
+              : reinterpret_cast<void*>(&bsk::k_chain<512, 3>);
+}
+int bs_chain_threads(int wide) { return wide ? 1024 : 512; }
