@@ -138,8 +138,13 @@ def token_store_device(lens, vocab: int = 32000, align: int = 32, seed: int = 0)
     tok_off = torch.zeros(lens.numel() + 1, dtype=torch.int64, device=lens.device)
     torch.cumsum(pitch, 0, out=tok_off[1:])
     total = int(tok_off[-1].item())
-    pos = torch.arange(total, dtype=torch.int64, device=lens.device)
-    tokens = (((pos * _HASH_MUL + (seed & 0xFFFFFFFF)) & 0xFFFFFFFF) % vocab).to(torch.int32)
+    tokens = torch.empty(total, dtype=torch.int32, device=lens.device)
+    chunk = 1 << 28  # bounded int64 temporaries (C3's store holds ~7e9 slots)
+    for a in range(0, total, chunk):
+        b = min(total, a + chunk)
+        pos = torch.arange(a, b, dtype=torch.int64, device=lens.device)
+        tokens[a:b] = (((pos * _HASH_MUL + (seed & 0xFFFFFFFF)) & 0xFFFFFFFF) % vocab).to(torch.int32)
+        del pos
     return tok_off, tokens
 
 
