@@ -249,7 +249,7 @@ def main():
     l_b = sched.ctx.launches
     res = sched.schedule(lens, cls, tok_off, tokens)
     kernels_per_window = sched.ctx.launches - l_b
-    use_graph = (not args.no_graph) and pg is None
+    use_graph = not args.no_graph
     # stage breakdown: a separate profiled pass (events between the kernels of the
     # eager launch sequence), not part of the timed region
     for _ in range(2):

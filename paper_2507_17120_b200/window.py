@@ -359,7 +359,8 @@ class WindowScheduler:
 
         graph=True replays the whole fused window (16-20 kernels) as one CUDA graph,
         captured on the first call for these input buffers (serving loops reuse
-        their input buffers); launch gaps between the stages disappear."""
+        their input buffers); launch gaps between the stages disappear.  Sharded
+        windows replay K2..K6 as a graph after the eager K1 + all-reduce."""
         dev = self.device
         lens, cls, n = self._inputs(lengths, classes)
         pack = tok_off is not None and tokens is not None
@@ -397,6 +398,37 @@ class WindowScheduler:
             return res
         if sharded and self.hist_global is None:
             self.hist_global = torch.zeros_like(self.hist)
+        if graph and sharded and not two_phase:
+            # K1 and the histogram all-reduce (C1) run eagerly; K2..K6 on the reduced
+            # histogram replay as one CUDA graph
+            with torch.cuda.device(dev):
+                N.check(lib.bs_histogram(self.ctx.ptr, _ptr(lens), _ptr(cls), n, C.byref(p),
+                                         _ptr(self.hist), _ptr(self.summary), st), self.ctx.ptr)
+                self.hist_global.copy_(self.hist)
+                if hist_reduce is not None:
+                    hist_reduce(self.hist_global)
+                else:
+                    allreduce_histogram(self.hist_global, self.process_group)
+            key = ("from_hist", lens.data_ptr(), cls.data_ptr(), n,
+                   tok_off.data_ptr() if pack else 0, tokens.data_ptr() if pack else 0,
+                   self.pack_capacity)
+            if self._graph is None or self._graph_key != key:
+                self._graph = None
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    io_g = self._io(lens, cls, n, tok_off, tokens, pack)
+                    io_g.hist_global = _ptr(self.hist_global)
+                    N.check(lib.bs_window_from_hist(self.ctx.ptr, C.byref(io_g), C.byref(p),
+                                                    _stream_handle(dev)), self.ctx.ptr)
+                self._graph, self._graph_key = g, key
+            self._graph.replay()
+            res = WindowResult(self, n, pack)
+            if sync:
+                torch.cuda.current_stream(dev).synchronize()
+                if check:
+                    res.check()
+            return res
         io = self._io(lens, cls, n, tok_off, tokens, pack and not two_phase)
         with torch.cuda.device(dev):
             if not sharded:

@@ -327,3 +327,30 @@ def test_packed_buffer_grows_when_window_needs_more():
     m = int(h["summary"]["packed_elems"])
     assert np.array_equal(h["out_tokens"][:m], o.out_tokens[:m])
     s.close()
+
+
+def test_sharded_window_graph_replay_matches_eager():
+    """Sharded windows with graph=True (eager K1 + histogram reduction, K2..K6 replayed
+    as a CUDA graph) give the eager sharded result on every call."""
+    cfg, lens, cls = W.make_window("c2", n=60_000, seed=21)
+    spec = _cfg_spec(cfg)
+    dev = torch.device("cuda", 0)
+    tok_off, tokens = W.token_store(lens)
+    t = [torch.as_tensor(x).to(dev) for x in (lens, cls, tok_off, tokens)]
+    other = W.make_window("c2", n=60_000, seed=22)[1]
+    other_hist = np.zeros((cfg.n_classes, cfg.l_max), np.int64)
+    np.add.at(other_hist, (W.make_window("c2", n=60_000, seed=22)[2].astype(np.int64),
+                           np.minimum(other, cfg.l_max - 1)), 1)
+    extra = torch.as_tensor(other_hist.reshape(-1).astype(np.int32)).to(dev)
+
+    def reduce(h):  # a second shard's histogram, added in place (stands in for C1)
+        h.add_(extra)
+
+    s = _sched(spec, len(lens))
+    eager = s.schedule(*t, hist_reduce=reduce).to_host()
+    for _ in range(3):
+        g = s.schedule(*t, hist_reduce=reduce, graph=True).to_host()
+        for k in ("edges", "perm", "req_batch", "req_row", "out_tokens", "out_mask"):
+            assert np.array_equal(g[k], eager[k]), k
+    assert int(g["summary"]["total_global"]) == 120_000
+    s.close()
