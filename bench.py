@@ -214,6 +214,12 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.config == "c5" and world < 2 and args.requests > 32_000_000:
+        # 64M requests: ~115 GB of token store + ~145 GB of packed output on one GPU
+        print(json.dumps({"metric": METRIC, "impl": "b200", "config": {"workload": "c5"},
+                          "unavailable": "C5 (64M requests) is sharded over >= 2 GPUs; pass "
+                                         "--requests to run a smaller window on one"}), flush=True)
+        return
 
     import torch
     import torch.distributed as dist
