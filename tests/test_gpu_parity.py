@@ -68,6 +68,16 @@ def test_gpu_matches_reference_fixture(name):
     assert np.array_equal(h["hist"].reshape(-1), o.hist.reshape(-1))
     assert h["summary"]["n_rejected"] == o.summary["n_rejected"]
     assert h["summary"]["n_pending"] == o.summary["n_pending"]
+    # memory statistics: exact integers; the padding ratio (mean of per-batch
+    # waste_ratio, pd_sim.py:898-899) within the north star's 1e-6 relative tolerance
+    # (the GPU sums the per-batch values in a parallel order)
+    for k in ("admitted_tokens", "padded_tokens", "packed_elems", "peak_footprint", "n_batches"):
+        assert h["summary"][k] == o.summary[k], k
+    w = ref["batch_waste"]
+    if len(w) and not np.isnan(w).any():
+        ref_mean = float(np.sum(w)) / len(w)
+        got_mean = h["summary"]["waste_sum"] / h["summary"]["n_batches"]
+        assert abs(got_mean - ref_mean) <= 1e-6 * max(abs(ref_mean), 1e-300)
     sched.close()
 
 
