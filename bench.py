@@ -238,7 +238,11 @@ def main():
         pg = dist.group.WORLD
     from paper_2507_17120_b200.window import WindowScheduler
 
-    cfg, lens_np, cls_np = W.make_window(args.config, n=args.requests, seed=1234 + rank)
+    if args.config == "c5":  # one 64M-request trace, contiguous arrival-order shard per rank
+        cfg, lens_np, cls_np = W.make_window("c5", n=args.requests * world, seed=1234,
+                                             shard=(rank, world))
+    else:
+        cfg, lens_np, cls_np = W.make_window(args.config, n=args.requests, seed=1234 + rank)
     n = len(lens_np)
     lens = torch.as_tensor(lens_np).to(dev)
     cls = torch.as_tensor(cls_np).to(dev)
