@@ -601,37 +601,29 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                               batch_end, batches_cap, out_tokens, out_mask, out_capacity, \
                               summary, st)
   int v = ctx->pack_variant;
-  // default: the TMA staging variant for long-context windows (rows of many KB),
-  // 128-bit register copies otherwise (measured on B200, C2 / C4)
-  // (non-persistent grid: CTAs retire as they finish, so the scheduling kernels of the
-  // next window in flight interleave with this pack — 0.903 vs 0.922 ms per C2 window
-  // with two windows in flight, identical when windows run one at a time)
+  // default: the TMA staging variant for long-context windows (rows of many KB: C4 at
+  // 89-91 % of the copy peak), the 128-bit register copy otherwise, on a non-persistent
+  // grid (CTAs retire as they finish, so the scheduling kernels of the next window in
+  // flight interleave with this pack: 0.903 vs 0.922 ms per C2 window with two windows in
+  // flight; 786 vs 793 us alone).  Tuning hook BS_PACK_VARIANT (all bit-identical):
+  //   1  register copy, persistent grid (6 CTAs/SM)     5  TMA bulk-copy staging
+  //   2  register copy, 8 vectors per lane, 4 CTAs/SM   6  cp.async shared-memory ring
+  //   17 register copy, non-persistent grid (default for l_max <= 16384)
   if (v == 0) v = p.l_max > 16384 ? 5 : 17;
-  switch (v) {  // tuning hook (BS_PACK_VARIANT)
+  switch (v) {
     case 1: BS_PACK_V(4, 6);
     case 2: BS_PACK_V(8, 4);
-    case 3: BS_PACK_V(8, 3);
-    case 4: BS_PACK_V(2, 8);
-#define BS_PACK_R(U, NS, W)                                                              \
-  return launch_pack_ring<U, NS, W>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, \
-                                    batch_end, batches_cap, out_tokens, out_mask,             \
-                                    out_capacity, summary, st)
-    case 6: BS_PACK_R(4, 4, 8);
-    case 7: BS_PACK_R(2, 8, 8);
-    case 8: BS_PACK_R(2, 6, 8);
-    case 9: BS_PACK_R(4, 6, 4);
-    case 10: BS_PACK_R(1, 16, 8);
-    case 15: BS_PACK_V(4, 4);
-    case 17:
-      return launch_pack_flat<4, 6>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
-                                    batch_end, batches_cap, out_tokens, out_mask, out_capacity,
-                                    summary, st);
-    case 16: BS_PACK_V(4, 3);
-#undef BS_PACK_R
     case 5:
       return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
                              batches_cap, out_tokens, out_mask, out_capacity, summary, st);
-    default: BS_PACK_V(4, 6);
+    case 6:
+      return launch_pack_ring<4, 4, 8>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
+                                       batch_end, batches_cap, out_tokens, out_mask,
+                                       out_capacity, summary, st);
+    default:
+      return launch_pack_flat<4, 6>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
+                                    batch_end, batches_cap, out_tokens, out_mask, out_capacity,
+                                    summary, st);
   }
 #undef BS_PACK_V
 }

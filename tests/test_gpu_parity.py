@@ -274,7 +274,7 @@ def test_sharded_window_on_one_gpu(world):
         s.close()
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 15, 16, 17])
+@pytest.mark.parametrize("variant", [1, 2, 5, 6, 17])
 def test_pack_variants_bit_exact(variant, monkeypatch):
     """Every K6 variant (BS_PACK_VARIANT tuning hook) packs the same bytes."""
     monkeypatch.setenv("BS_PACK_VARIANT", str(variant))
