@@ -47,7 +47,9 @@ struct SizeArgs {
   int32_t padded;
   int32_t L;
   int32_t truncate;
-  int32_t pad0;
+  int32_t C;         // classes (segment s holds class s % C)
+  int32_t sjf_mask;  // bit c: class c drains SJF (lengths ascending in its segments)
+  int32_t ljf_mask;  // bit c: class c drains LJF (lengths descending)
 };
 
 struct Stat {
@@ -175,8 +177,9 @@ __global__ void __launch_bounds__(256)
     const uint32_t nrm = bmask[g];
     const int32_t x = valid ? slen[j] : 0;
     int64_t e = 0;
+    int64_t seg_c = 0;
     bool start = false;
-    {  // segment of j: one binary search per warp, then a short walk per lane
+    {  // segment of j: one lookup per warp, then a short walk per lane
       int64_t s0 = 0;
       // the sorted radix slot names the segment (K2 slot_seg LUT); binary search otherwise
       if (lane == 0) s0 = skeys ? slot_seg[skeys[g << 5]] : seg_of(seg_off, n_segs, g << 5);
@@ -185,6 +188,51 @@ __global__ void __launch_bounds__(256)
         while (seg_off[s + 1] <= j) ++s;
         e = seg_off[s + 1];
         start = seg_off[s] == j;
+      }
+      seg_c = s;
+    }
+    // PADDED drains of length-sorted segments have closed forms (no gallop):
+    //   SJF: lengths ascend, rejected (> S) form the tail: next(j) = first k > j with
+    //        slen[k] > S or slen[k] * (k - j + 1) > T (both monotone: exponential +
+    //        binary search);
+    //   LJF: lengths descend, rejected form the head: the call starts at the first
+    //        admissible j0 and admits floor(T / slen[j0]) requests.
+    int fast = 0;
+    int32_t fast_nx = kEnd;
+    if (valid && a.padded) {
+      const int c = (int)(seg_c % a.C);
+      if ((a.sjf_mask >> c) & 1) {
+        fast = 1;
+        if ((int64_t)x <= a.S && (int64_t)x <= a.T) {
+          auto bad = [&](int64_t k) {
+            const int64_t y = slen[k];
+            return y > a.S || y * (k - j + 1) > a.T;
+          };
+          int64_t lo = j + 1, hi = e, step = 1;
+          for (;;) {  // exponential search: [j+1, lo) are admitted
+            const int64_t q = lo + step - 1;
+            if (q >= e) break;
+            if (bad(q)) { hi = q; break; }
+            lo = q + 1;
+            step <<= 1;
+          }
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (bad(mid)) hi = mid; else lo = mid + 1;
+          }
+          // lo: first violation, or the rejected tail (consumed by this call), or e
+          fast_nx = (lo < e && (int64_t)slen[lo] <= a.S) ? (int32_t)lo : kEnd;
+        }
+      } else if ((a.ljf_mask >> c) & 1) {
+        fast = 1;
+        const int64_t j0 = first_nonrej(j, e, bmask);
+        if (j0 < e) {
+          const int64_t x0 = slen[j0];
+          if (x0 <= a.T) {
+            const int64_t k = j0 + a.T / x0;
+            fast_nx = k < e ? (int32_t)k : kEnd;
+          }
+        }
       }
     }
     const int64_t gend = ((g << 5) + 32) < a.n ? ((g << 5) + 32) : a.n;
@@ -204,7 +252,9 @@ __global__ void __launch_bounds__(256)
     int32_t nx = kEnd;
     Stat st{0, 0, 0};
     int64_t p = 0;
-    if (valid) {
+    if (fast) {
+      nx = fast_nx;  // mode 0: done
+    } else if (valid) {
       if (e <= gend || rem == 0) {
         mode = 2;
       } else {
@@ -794,7 +844,12 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   a.padded = p.accounting == BS_ACCOUNTING_PADDED;
   a.L = p.l_max;
   a.truncate = p.truncate;
-  a.pad0 = 0;
+  a.C = p.n_classes;
+  a.sjf_mask = a.ljf_mask = 0;
+  for (int c = 0; c < p.n_classes; ++c) {
+    if (p.policy[c] == BS_POLICY_SJF) a.sjf_mask |= 1 << c;
+    if (p.policy[c] == BS_POLICY_LJF) a.ljf_mask |= 1 << c;
+  }
   int32_t* misc = ctx->misc;
   e = cudaMemsetAsync(misc, 0, sizeof(int32_t) * 128, st);
   if (e != cudaSuccess) return e;
