@@ -196,6 +196,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=131_072)
     ap.add_argument("--dispatch", action="store_true", help="also compute the simulator's "
                     "global dispatch order (K7, SURVEY f3) inside every window")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
+                    help="C1 for N > 1: torch.distributed all-reduce (NCCL over NVLink) or the "
+                         "device-side exchange over CUDA-IPC peer memory (bs_peer_*), which "
+                         "keeps the whole window inside one CUDA graph")
     ap.add_argument("--inflight", type=int, default=2, help="windows in flight: consecutive "
                     "windows alternate over this many schedulers (own scratch, outputs and CUDA "
                     "stream), so the latency-bound scheduling of one window overlaps the "
@@ -251,7 +255,8 @@ def main():
                             policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
                             buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
                             current_safe=cfg.current_safe, accounting=cfg.accounting,
-                            device=dev, process_group=pg, dispatch=args.dispatch)
+                            device=dev, process_group=pg, dispatch=args.dispatch,
+                            collective=args.collective)
     # first window sizes the reusable packed-output buffer
     l_a = sched.ctx.launches
     res = sched.schedule(lens, cls, tok_off, tokens)
@@ -278,7 +283,8 @@ def main():
                         policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
                         buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
                         current_safe=cfg.current_safe, accounting=cfg.accounting, device=dev,
-                        process_group=pg, dispatch=args.dispatch, pack_capacity=sched.pack_capacity)
+                        process_group=pg, dispatch=args.dispatch, pack_capacity=sched.pack_capacity,
+                        collective=args.collective)
         for _ in range(inflight - 1)]
     streams = [torch.cuda.Stream(dev) for _ in range(inflight)]
 
@@ -430,8 +436,9 @@ def main():
             "l_max": cfg.l_max, "classes": cfg.n_classes,
             "kv_bytes_per_token": cfg.kvpt, "safe_memory_bytes": cfg.current_safe,
             "accounting": "padded" if cfg.accounting == 0 else "exact",
-            "parallelism": f"dp{world} (request shards, "
-                           f"{os.environ.get('BS_DIST_BACKEND', 'nccl').upper()} histogram all-reduce)",
+            "parallelism": f"dp{world} (request shards, " + (
+                "histogram exchange over CUDA-IPC peer memory)" if args.collective == "peer"
+                else f"{os.environ.get('BS_DIST_BACKEND', 'nccl').upper()} histogram all-reduce)"),
             "pipeline": f"{inflight} windows in flight (one scheduler context + CUDA stream each); "
                         "ms_per_step = timed region / steps",
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"

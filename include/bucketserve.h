@@ -63,6 +63,7 @@ extern "C" {
 #define BS_FLAG_BATCH_CAP     0x40 /* more batches than batches_cap                                       */
 #define BS_FLAG_BAD_EDGES     0x80 /* init_edges not strictly increasing from 0 to l_max: ValueError      */
 #define BS_FLAG_DISPATCH_RANGE 0x100 /* dispatch keys out of range (token mass >= 2^43 or > 2^17 buckets) */
+#define BS_FLAG_PEER_TIMEOUT  0x200 /* a peer rank's histogram did not arrive within the timeout   */
 
 /* ---- enums ------------------------------------------------------------------ */
 /* Dispatch order inside one (bucket, class) segment, batch_controller.py:33-41.
@@ -275,6 +276,25 @@ typedef struct bs_window_io {
 int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p, void* stream);
 /* K2..K6 given io->hist (local) and io->hist_global (all-reduced). */
 int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p, void* stream);
+
+/* ---- C1 over peer memory (alternative to an NCCL all-reduce) --------------------------
+ * One process per GPU; every rank's context owns an exchange buffer (two histogram
+ * slots + an epoch flag) that the other ranks map with CUDA IPC (NVLink / NVSwitch
+ * peer memory on a multi-GPU node).  bs_peer_export writes the buffer's
+ * cudaIpcMemHandle_t (BS_PEER_HANDLE_BYTES) into handle_out; after the handles of all
+ * ranks are gathered (any host transport), bs_peer_connect maps them (handles[r] is
+ * rank r's handle; the own entry is ignored).  bs_peer_reduce then runs C1 on the
+ * device, after bs_histogram on the same stream: it publishes this rank's histogram
+ * for the next epoch (device-side counter: graph-capturable), waits on every peer's
+ * epoch flag (acquire, system scope) and sums the peers' slots into hist_global
+ * (read straight from peer memory).  Two slots per rank make a rank that runs one
+ * window ahead safe.  A peer that does not arrive within ~5 s latches
+ * BS_FLAG_PEER_TIMEOUT instead of hanging. */
+#define BS_PEER_HANDLE_BYTES 64
+int bs_peer_export(bs_ctx* ctx, void* handle_out);
+int bs_peer_connect(bs_ctx* ctx, int32_t rank, int32_t world, const void* handles);
+int bs_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params* p,
+                   uint32_t* hist_global, bs_summary* summary, void* stream);
 
 /* ---- monitor statistic ------------------------------------------
  * 64-bin view of the window histogram: out64[b] = #{len : (len*bins)//l_max == b}

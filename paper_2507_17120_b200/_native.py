@@ -33,6 +33,8 @@ FLAG_NONPOS_LEN = 0x20
 FLAG_BATCH_CAP = 0x40
 FLAG_BAD_EDGES = 0x80
 FLAG_DISPATCH_RANGE = 0x100
+FLAG_PEER_TIMEOUT = 0x200
+PEER_HANDLE_BYTES = 64
 
 POLICY_FCFS, POLICY_SJF, POLICY_LJF = 0, 1, 2
 ACCOUNTING_PADDED, ACCOUNTING_EXACT = 0, 1
@@ -45,7 +47,8 @@ EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "
            "bs_histogram", "bs_boundaries", "bs_assign", "bs_order", "bs_size", "bs_pack",
            "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_profile_enable",
            "bs_profile_read", "bs_launch_count", "bs_dispatch", "bs_trace_parse",
-           "bs_trace_write_bst", "bs_trace_read_bst")
+           "bs_trace_write_bst", "bs_trace_read_bst", "bs_peer_export", "bs_peer_connect",
+           "bs_peer_reduce")
 STAGES = ("histogram", "boundaries", "order", "size.prep", "size.next", "size.chain",
           "size.describe", "size.outcome", "dispatch", "pack")
 
@@ -124,6 +127,9 @@ def load():
         "bs_profile_read": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(i32)]),
         "bs_launch_count": (i64, [vp]),
         "bs_dispatch": (C.c_int, [vp, vp, vp, i64, P, vp, i32, vp, vp, vp, vp, vp, vp]),
+        "bs_peer_export": (C.c_int, [vp, vp]),
+        "bs_peer_connect": (C.c_int, [vp, i32, i32, vp]),
+        "bs_peer_reduce": (C.c_int, [vp, vp, P, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -161,6 +167,8 @@ def raise_for_flags(flags: int, l_max: int | None = None):
         raise SimulationError("batch descriptor capacity exceeded")
     if flags & FLAG_PACK_CAPACITY:
         raise ValueError("packed output buffer too small")
+    if flags & FLAG_PEER_TIMEOUT:
+        raise SimulationError("a peer rank's histogram did not arrive (peer-memory C1 timeout)")
     if flags & FLAG_DISPATCH_RANGE:
         raise ValueError("dispatch order: queued token mass or bucket count out of range")
 

@@ -7,6 +7,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "ctx.cuh"
 
@@ -232,6 +233,10 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
 int bs_destroy(bs_ctx* ctx) {
   if (!ctx) return BS_OK;
   cudaSetDevice(ctx->device);
+  for (void* m : ctx->peer_mapped)
+    if (m) cudaIpcCloseMemHandle(m);
+  if (ctx->peer_ptrs) cudaFree(ctx->peer_ptrs);
+  if (ctx->xbuf) cudaFree(ctx->xbuf);
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
   free_all(ctx);
   delete ctx;
@@ -374,6 +379,67 @@ int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_
   return BS_OK;
 }
 
+int bs_peer_export(bs_ctx* ctx, void* handle_out) {
+  if (!ctx || !handle_out) return fail(ctx, BS_ERR_INVALID_ARG, "NULL argument");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (!ctx->xbuf) {
+    const int64_t slot_words = (int64_t)ctx->l_cap * ctx->c_max;
+    ctx->xbuf_bytes = (int64_t)sizeof(uint32_t) * 2 * slot_words +
+                      (int64_t)sizeof(int64_t) * bsk::peer_flag_words();
+    BS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->xbuf), (size_t)ctx->xbuf_bytes), "cudaMalloc xbuf");
+    BS_CUDA(cudaMemset(ctx->xbuf, 0, (size_t)ctx->xbuf_bytes), "cudaMemset xbuf");
+    ctx->scratch_bytes += ctx->xbuf_bytes;
+  }
+  cudaIpcMemHandle_t h;
+  BS_CUDA(cudaIpcGetMemHandle(&h, ctx->xbuf), "cudaIpcGetMemHandle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == BS_PEER_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof h);
+  return BS_OK;
+}
+
+int bs_peer_connect(bs_ctx* ctx, int32_t rank, int32_t world, const void* handles) {
+  if (!ctx || !handles) return fail(ctx, BS_ERR_INVALID_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ctx, BS_ERR_INVALID_ARG, "bad rank/world");
+  if (!ctx->xbuf) return fail(ctx, BS_ERR_INVALID_ARG, "bs_peer_export must come first");
+  if (ctx->peer_world) return fail(ctx, BS_ERR_INVALID_ARG, "context already connected");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::vector<uint32_t*> table((size_t)world, nullptr);
+  const unsigned char* hb = static_cast<const unsigned char*>(handles);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      table[r] = ctx->xbuf;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hb + (size_t)r * BS_PEER_HANDLE_BYTES, sizeof h);
+    void* ptr = nullptr;
+    BS_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    ctx->peer_mapped.push_back(ptr);
+    table[r] = static_cast<uint32_t*>(ptr);
+  }
+  BS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->peer_ptrs), sizeof(uint32_t*) * world),
+          "cudaMalloc peer table");
+  BS_CUDA(cudaMemcpy(ctx->peer_ptrs, table.data(), sizeof(uint32_t*) * world, cudaMemcpyHostToDevice),
+          "copy peer table");
+  ctx->peer_rank = rank;
+  ctx->peer_world = world;
+  return BS_OK;
+}
+
+int bs_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params* p,
+                   uint32_t* hist_global, bs_summary* summary, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK) return rc;
+  if (!hist_local || !hist_global) return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  if (ctx->peer_world < 1) return fail(ctx, BS_ERR_INVALID_ARG, "bs_peer_connect must come first");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_peer_reduce(ctx, hist_local, *p, hist_global, summary,
+                                  static_cast<cudaStream_t>(stream)),
+          "k_peer_reduce");
+  return BS_OK;
+}
+
 static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
                                  cudaStream_t st) {
   int rc;
@@ -438,9 +504,19 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
   ++ctx->launches;
   BS_CUDA(bsk::launch_histogram(ctx, io->len, io->cls, io->n, *p, io->hist, io->summary, st),
           "k_histogram");
-  bsk::prof_mark(ctx, 1, st);
   bs_window_io local = *io;
   local.hist_global = io->hist;
+  if (ctx->peer_world > 1) {  // C1 over peer memory (bs_peer_connect): io->hist_global required
+    if (!io->hist_global || io->hist_global == io->hist) {
+      ctx->prof_in_window = false;
+      return fail(ctx, BS_ERR_INVALID_ARG, "a peer-connected context needs io->hist_global");
+    }
+    BS_CUDA(bsk::launch_peer_reduce(ctx, io->hist, *p, const_cast<uint32_t*>(io->hist_global),
+                                    io->summary, st),
+            "k_peer_reduce");
+    local.hist_global = io->hist_global;
+  }
+  bsk::prof_mark(ctx, 1, st);
   rc = window_from_hist_impl(ctx, &local, p, st);
   ctx->prof_in_window = false;
   return rc;

@@ -80,6 +80,12 @@ struct bs_ctx {
   int32_t* disp_nulls = nullptr;     // [l_cap*c_max+1] sorted positions of null calls
   int32_t* disp_runs = nullptr;      // [2*l_cap*c_max+32][4] runs of consecutive plans
   int64_t* disp_misc = nullptr;      // [32]
+  // C1 over peer memory (bs_peer_*)
+  uint32_t* xbuf = nullptr;          // own exchange buffer: [2][c_max*l_cap] hist slots + flags
+  int64_t xbuf_bytes = 0;
+  int peer_rank = -1, peer_world = 0;
+  std::vector<void*> peer_mapped;    // IPC mappings of the other ranks' exchange buffers
+  uint32_t** peer_ptrs = nullptr;    // device table [world] of exchange-buffer base pointers
   int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
                                  //        [66] n_batches, [67] pack rows cursor, [69] long chains
 };
@@ -132,7 +138,10 @@ cudaError_t launch_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg
                             int32_t* emit_order, int32_t* batch_emit, bs_summary* summary,
                             cudaStream_t st);
 int dispatch_smem_bytes();
+int peer_flag_words();
 int dispatch_threads();
+cudaError_t launch_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params& p,
+                               uint32_t* hist_global, bs_summary* summary, cudaStream_t st);
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);

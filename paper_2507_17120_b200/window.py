@@ -227,7 +227,7 @@ class WindowScheduler:
                  current_safe: int | None = None, n_max: int | None = None, device=None,
                  pack_capacity: int | None = None, with_mask: bool = True,
                  changes_cap: int | None = None, batches_cap: int | None = None,
-                 process_group=None, dispatch: bool = False):
+                 process_group=None, dispatch: bool = False, collective: str = "nccl"):
         if not torch.cuda.is_available():
             raise N.NativeUnavailable("no CUDA device: the window scheduler runs only on a B200")
         if max_seq_len is None:
@@ -261,6 +261,11 @@ class WindowScheduler:
         self.hist = torch.zeros(Cn * L, **i32)
         self.hist_global = torch.zeros(Cn * L, **i32) if process_group is not None else None
         self.process_group = process_group
+        if collective not in ("nccl", "peer"):
+            raise ValueError("collective must be 'nccl' (torch.distributed all-reduce) or 'peer'")
+        self.collective = collective if process_group is not None else "nccl"
+        if self.collective == "peer":
+            self._peer_connect()
         self.edges = torch.zeros(L + 1, **i32)
         self.changes_cap = int(changes_cap if changes_cap is not None else 4 * L + 64)
         self.changes = torch.zeros(4 * self.changes_cap, **i32)
@@ -290,6 +295,20 @@ class WindowScheduler:
             self._ensure_pack(int(pack_capacity))
 
     # ------------------------------------------------------------------------
+    def _peer_connect(self):
+        """C1 over peer memory: share this context's exchange buffer with the other ranks
+        (CUDA IPC handles gathered over the process group) and map theirs."""
+        import torch.distributed as dist
+        lib = N.load()
+        h = (C.c_ubyte * N.PEER_HANDLE_BYTES)()
+        N.check(lib.bs_peer_export(self.ctx.ptr, h), self.ctx.ptr)
+        world = dist.get_world_size(self.process_group)
+        rank = dist.get_rank(self.process_group)
+        got = [None] * world
+        dist.all_gather_object(got, bytes(h), group=self.process_group)
+        allh = (C.c_ubyte * (N.PEER_HANDLE_BYTES * world)).from_buffer_copy(b"".join(got))
+        N.check(lib.bs_peer_connect(self.ctx.ptr, rank, world, allh), self.ctx.ptr)
+
     def _ensure_pack(self, cap: int):
         if cap <= self.pack_capacity:
             return
@@ -376,7 +395,8 @@ class WindowScheduler:
             self._ensure_pack(64)  # nothing to pack; keep the result shape uniform
         two_phase = pack and self.pack_capacity == 0
         sharded = self.process_group is not None or hist_reduce is not None
-        if graph and not sharded and not two_phase:
+        fused = not sharded or (self.collective == "peer" and hist_reduce is None)
+        if graph and fused and not two_phase:
             key = (lens.data_ptr(), cls.data_ptr(), n,
                    tok_off.data_ptr() if pack else 0, tokens.data_ptr() if pack else 0,
                    self.pack_capacity)
@@ -386,6 +406,8 @@ class WindowScheduler:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     io_g = self._io(lens, cls, n, tok_off, tokens, pack)
+                    if sharded:  # peer-connected context: C1 runs inside the fused call
+                        io_g.hist_global = _ptr(self.hist_global)
                     N.check(lib.bs_window_schedule(self.ctx.ptr, C.byref(io_g), C.byref(p),
                                                    _stream_handle(dev)), self.ctx.ptr)
                 self._graph, self._graph_key = g, key
@@ -398,7 +420,7 @@ class WindowScheduler:
             return res
         if sharded and self.hist_global is None:
             self.hist_global = torch.zeros_like(self.hist)
-        if graph and sharded and not two_phase:
+        if graph and sharded and not fused and not two_phase:
             # K1 and the histogram all-reduce (C1) run eagerly; K2..K6 on the reduced
             # histogram replay as one CUDA graph
             with torch.cuda.device(dev):
@@ -431,7 +453,9 @@ class WindowScheduler:
             return res
         io = self._io(lens, cls, n, tok_off, tokens, pack and not two_phase)
         with torch.cuda.device(dev):
-            if not sharded:
+            if fused:
+                if sharded:
+                    io.hist_global = _ptr(self.hist_global)
                 N.check(lib.bs_window_schedule(self.ctx.ptr, C.byref(io), C.byref(p), st), self.ctx.ptr)
             else:
                 N.check(lib.bs_histogram(self.ctx.ptr, _ptr(lens), _ptr(cls), n, C.byref(p),
