@@ -239,9 +239,11 @@ int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_
                 bs_summary* summary, void* stream);
 
 /* ---- fused window ------------------------------------------------------------------
- * K1..K6 in one call on one stream (single-GPU window).  For a sharded window
- * call bs_histogram, all-reduce the histogram across ranks, then
- * bs_window_from_hist on every rank. */
+ * K1..K6 (+ K7 when p->dispatch) in one call on one stream.  Single rank: the local
+ * histogram is the global one.  Sharded window: either call bs_histogram, all-reduce
+ * the histogram across ranks (NCCL) and then bs_window_from_hist on every rank, or
+ * connect the contexts once (bs_peer_*) and call bs_window_schedule, which then reduces
+ * the ranks' histograms over peer memory into io->hist_global on the device. */
 typedef struct bs_window_io {
   /* inputs */
   const int32_t* len;         /* [n]  */
@@ -257,7 +259,8 @@ typedef struct bs_window_io {
   int64_t        out_capacity;/* elements in out_tokens / out_mask */
   /* outputs (device; any may be NULL except where noted) */
   uint32_t*      hist;        /* [n_classes * l_max]  required */
-  const uint32_t* hist_global;/* NULL = hist (single rank)     */
+  const uint32_t* hist_global;/* NULL = hist (single rank); with a peer-connected ctx
+                                 bs_window_schedule writes the reduced histogram here */
   int32_t*       edges;       /* [l_max + 1]          required */
   int32_t*       changes;     /* [changes_cap * 4]             */
   int32_t*       bucket;      /* [n]                           */
