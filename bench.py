@@ -411,7 +411,9 @@ def main():
         d2h = n * 4 + 64 * nb + 256
         e2e = {"value": world * n / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": float(te.item()), "steps": k_e2e}
+               "ms_per_step": float(te.item()), "steps": k_e2e,
+               # the copies dominate: the achieved host<->device rate is the e2e roofline
+               "pcie_gbs": (h2d + d2h) / (float(te.item()) / 1e3) / 1e9}
 
     if rank != 0:
         if pg is not None:
