@@ -152,6 +152,15 @@ def test_c3_four_class_4m():
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True, sample_rows=2000)
 
 
+def test_c3_full_16m_schedule_bit_exact():
+    """BASELINE configs[2] at its full 16M size: edges, drain order, batches and every
+    request's outcome bit-exact vs the oracle, which also drives K5c's pointer-doubling
+    path (C3 has chains beyond the serial walk).  The pack at this size is checked on
+    sampled rows by test_c3_four_class_4m (a 16M packed copy is ~35 GB on the host)."""
+    cfg, lens, cls = W.make_window("c3", seed=1234)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=False)
+
+
 def test_c4_long_context_pack():
     cfg, lens, cls = W.make_window("c4", n=20_000, seed=8)
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
