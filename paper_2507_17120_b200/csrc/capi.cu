@@ -176,7 +176,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(listA, N + 1); A(listB, N + 1);
   A(node_batch, N + 1);
   A(node_j0, N + 1);
-  A(segw, 6 * (L * C + 1));
+  A(segw, 7 * (L * C + 1));
   A(rowpos, N + 1);
   A(task_base, N + 2);
   A(misc, 128);

@@ -60,7 +60,7 @@ struct bs_ctx {
   int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
                                  //   <= kPiece tokens; exclusive prefix, K5f)
   int32_t* node_j0 = nullptr;
-  int32_t* segw = nullptr;       // [6][l_cap*c_max+1] per-segment chain length / tail / bases    // [max_n + 1] first admissible position at/after each chain node
+  int32_t* segw = nullptr;       // [7][l_cap*c_max+1] per-segment chain length / tail / bases    // [max_n + 1] first admissible position at/after each chain node
   int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
   uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
   int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)
@@ -87,7 +87,8 @@ struct bs_ctx {
   std::vector<void*> peer_mapped;    // IPC mappings of the other ranks' exchange buffers
   uint32_t** peer_ptrs = nullptr;    // device table [world] of exchange-buffer base pointers
   int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
-                                 //        [66] n_batches, [67] pack rows cursor, [69] long chains
+                                 //        [66] n_batches, [67] pack rows cursor, [69] long chains,
+                                 //        [70] long-segment count
 };
 
 namespace bsk {

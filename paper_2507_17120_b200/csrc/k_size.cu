@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   int32_t* seg_nbase = segw + 3 * (n_segs + 1);
   int32_t* seg_ebase = segw + 4 * (n_segs + 1);
   int32_t* seg_long = segw + 5 * (n_segs + 1);
+  int32_t* long_list = segw + 6 * (n_segs + 1);
   // ---- phase 0: Rg = exclusive prefix of admissible counts per 32-position group ----
   const int64_t G = (n + 31) >> 5;
   const int64_t per = (G + gridDim.x - 1) / gridDim.x;
@@ -461,6 +462,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       seg_empty[sg] = empty;
       seg_tailj0[sg] = tj0;
       seg_long[sg] = lng;
+      if (lng) {  // compact list of the long segments: doubling only touches their positions
+        const int32_t idx = atomicAdd(misc + 70, 1);
+        if (idx <= n_segs) long_list[idx] = (int32_t)sg;
+      }
       any_long |= lng != 0;
     }
     if (any_long) misc[69] = 1;
@@ -484,29 +489,64 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   int r = 0;
   const bool need_doubling = ld_rel_i32(misc + 69) != 0;
   if (need_doubling) {
-    // ---- phase 1: pointer doubling -------------------------------------------------------
+    // ---- phase 1: pointer doubling over the positions of the long segments ---------------
+    // (chain successors stay inside their segment, so the other segments' entries of
+    // J[r >= 1] are never read); every CTA maps a virtual index onto the long segments
+    // through a shared-memory prefix of their sizes (all positions beyond kMaxLong)
+    constexpr int kMaxLong = 256;
+    __shared__ int32_t s_lseg[kMaxLong];
+    __shared__ int64_t s_lpre[kMaxLong + 1];
+    const int32_t n_long = ld_rel_i32(misc + 70);
+    const bool listed = n_long <= kMaxLong;
+    int64_t span = n;
+    if (listed) {
+      int64_t sz = 0;
+      if (tid < n_long) {
+        const int32_t sg = ld_rel_i32(long_list + tid);
+        s_lseg[tid] = sg;
+        sz = (int64_t)seg_off[sg + 1] - seg_off[sg];
+      }
+      __shared__ int64_t s_sc[33];
+      int64_t tot;
+      const int64_t o = block_excl_scan<int64_t>(tid < kMaxLong ? sz : 0, s_sc, &tot);
+      if (tid < kMaxLong) s_lpre[tid] = o;
+      if (tid == 0) s_lpre[kMaxLong] = tot;
+      __syncthreads();
+      span = tot;
+    }
+    auto position = [&](int64_t v) -> int64_t {
+      if (!listed) return v;
+      int lo = 0, hi = n_long;  // last i with s_lpre[i] <= v
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_lpre[mid] <= v) lo = mid; else hi = mid;
+      }
+      return (int64_t)seg_off[s_lseg[lo]] + (v - s_lpre[lo]);
+    };
     while (r + 1 < r_cap && ld_rel_i32(alive + r)) {
       const int32_t* Jr = J + (int64_t)r * n;
       int32_t* Jn = J + (int64_t)(r + 1) * n;
       bool any = false;
       // kIlp independent positions per thread in flight (the second load is a gather)
-      constexpr int kIlp = kThreads >= 1024 ? 4 : 8;
+      constexpr int kIlp = 4;
       const int64_t S = (int64_t)gridDim.x * blockDim.x;
-      for (int64_t x0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < n; x0 += kIlp * S) {
+      for (int64_t x0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < span;
+           x0 += kIlp * S) {
         int32_t v[kIlp];
+        int64_t xs[kIlp];
 #pragma unroll
         for (int k = 0; k < kIlp; ++k) {
-          const int64_t x = x0 + k * S;
-          v[k] = x < n ? Jr[x] : kEnd;
+          const int64_t q = x0 + k * S;
+          xs[k] = q < span ? position(q) : -1;
+          v[k] = xs[k] >= 0 ? Jr[xs[k]] : kEnd;
         }
 #pragma unroll
         for (int k = 0; k < kIlp; ++k) v[k] = v[k] == kEnd ? kEnd : Jr[v[k]];
 #pragma unroll
         for (int k = 0; k < kIlp; ++k) {
-          const int64_t x = x0 + k * S;
-          if (x < n) {
-            Jn[x] = v[k];
-            if (v[k] != kEnd && is_start[x]) any = true;
+          if (xs[k] >= 0) {
+            Jn[xs[k]] = v[k];
+            if (v[k] != kEnd && is_start[xs[k]]) any = true;
           }
         }
       }
