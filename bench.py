@@ -47,13 +47,21 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _profile_traffic(cfg_name):
+def _pack_kernel(l_max):
+    """the K6 kernel the library launches by default (k_pack.cu: launch_pack)."""
+    v = int(os.environ.get("BS_PACK_VARIANT", "0") or 0)
+    if v == 0:
+        v = 5 if l_max > 16384 else 20
+    return {5: "k_pack_tma", 6: "k_pack_ring", 18: "k_pack_stream", 20: "k_pack_stream"}.get(v, "k_pack")
+
+
+def _profile_traffic(cfg_name, kernel):
     """dram bytes per pack launch from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        ent = d.get("k_pack", {}).get(cfg_name)
+        ent = d.get(kernel, {}).get(cfg_name)
         return ent.get("dram_bytes") if ent else None
     except Exception:
         return None
@@ -446,9 +454,9 @@ def main():
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
                   % (tokens.numel() * 4 / 1e9, int(s["packed_elems"]) * 5 / 1e9),
         },
-        "roofline": {"bound": "hbm", "kernel": "k_pack", "achieved": pack_gbs, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": _pack_kernel(cfg.l_max), "achieved": pack_gbs, "peak": peak,
                      "unit": "GB/s", "frac": (pack_gbs / peak) if pack_gbs else None,
-                     "traffic": _profile_traffic(args.config), "algorithmic_bytes": pack_bytes,
+                     "traffic": _profile_traffic(args.config, _pack_kernel(cfg.l_max)), "algorithmic_bytes": pack_bytes,
                      "avg_launch_ms": pack_ms, "peak_source": peak_src},
         "stages_ms": stage_ms,
         "schedule_roofline": {"bytes": sched_bytes, "ms": sched_ms,

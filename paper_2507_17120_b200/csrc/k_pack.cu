@@ -164,6 +164,137 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
 }
 
 // ---------------------------------------------------------------------------------
+// Flattened variant: the 16-byte token vectors of the warp's 32 pieces form one
+// stream (exclusive scan of the per-piece vector counts), and every iteration moves
+// 32 * kU consecutive vectors of that stream, whichever pieces they belong to.  With
+// k_pack a short row (C2's median is 245 tokens = 62 vectors) leaves most of the
+// 4 x 32 vector slots of its iteration empty and every row costs one load round trip;
+// here each round trip carries a full 32 * kU * 16 bytes.  A lane finds the piece of
+// stream position q by a 5-step binary search over the lanes' scan values (shuffles);
+// rows whose source is not 16-byte aligned take copy_row_range's scalar path after
+// the stream.  The mask is written per piece as in k_pack.
+template <int kU, int kMinBlocks>
+__global__ void __launch_bounds__(kPackThreads, kMinBlocks)
+    k_pack_stream(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
+                  const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
+                  const int64_t* __restrict__ tok_off, const int32_t* __restrict__ tokens,
+                  int32_t L, int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
+                  int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in,
+                  int32_t batches_cap, int32_t* __restrict__ out_tokens,
+                  uint8_t* __restrict__ out_mask, int64_t out_cap, bs_summary* sum) {
+  const unsigned FULL = 0xffffffffu;
+  int64_t b_end = b_end_arg;
+  if (b_end < 0) {
+    b_end = sum_in->n_batches;
+    if (b_end > batches_cap) b_end = batches_cap;
+  }
+  if (b_begin >= b_end) return;
+  const int64_t base_off = batches[b_begin].out_offset;
+  const bs_batch last = batches[b_end - 1];
+  if (last.out_offset + (int64_t)last.n * last.pitch - base_off > out_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
+    return;
+  }
+  const int64_t t0 = task_base[b_begin], t1 = task_base[b_end];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int4 pad4 = make_int4(pad_id, pad_id, pad_id, pad_id);
+  unsigned fl = 0;
+  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
+    const int64_t t = gt + lane;
+    const int32_t* src = nullptr;
+    int32_t* dst = nullptr;
+    uint8_t* mdst = nullptr;
+    int32_t x = 0, vb = 0, ve = 0;
+    if (t < t1) {
+      int64_t lo = b_begin, hi = b_end;  // batch of task t: last b with task_base[b] <= t
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (task_base[mid] <= t) lo = mid; else hi = mid;
+      }
+      const bs_batch B = batches[lo];
+      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int64_t local = t - task_base[lo];
+      const int64_t row = local / pieces;
+      const int32_t piece = (int32_t)(local - row * pieces);
+      const int64_t rstart = (B.out_offset - base_off) + row * (int64_t)B.pitch;
+      const int32_t r = perm[rowpos[B.row_base + row]];
+      x = eff_len(len[r], L, truncate, fl);
+      src = tokens + tok_off[r];
+      dst = out_tokens + rstart;
+      mdst = out_mask ? out_mask + rstart : nullptr;
+      vb = piece * (kPiece / 4);
+      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      ve = c1 >> 2;
+    }
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    const int32_t cnt = (t < t1 && aligned) ? ve - vb : 0;
+    const int32_t incl = warp_incl_scan(cnt);
+    const int32_t pre = incl - cnt;  // stream position of this lane's first vector
+    const int32_t total = __shfl_sync(FULL, incl, 31);
+    for (int32_t q0 = 0; q0 < total; q0 += 32 * kU) {
+      int4 val[kU];
+      int32_t jv[kU];  // (piece lane << 26) | vector in row, -1 past the stream
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int32_t q = q0 + u * 32 + lane;
+        // piece of q: the last lane with pre <= q (pre is non-decreasing and a zero-count
+        // piece shares its pre with the next lane, so the last such lane has vectors)
+        int j = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int32_t pj = __shfl_sync(FULL, pre, j + s);
+          if (pj <= q) j += s;
+        }
+        const int32_t* s_j = reinterpret_cast<const int32_t*>(
+            __shfl_sync(FULL, reinterpret_cast<unsigned long long>(src), j));
+        const int32_t x_j = __shfl_sync(FULL, x, j);
+        const int32_t v = __shfl_sync(FULL, vb, j) + (q - __shfl_sync(FULL, pre, j));
+        jv[u] = q < total ? (j << 26) | v : -1;
+        const int32_t full = x_j >> 2, rem = x_j & 3;
+        int4 r = pad4;
+        if (q < total) {
+          if (v < full) {
+            r = ld_stream_v4(reinterpret_cast<const int4*>(s_j) + v);
+          } else if (v == full && rem) {
+            r.x = s_j[4 * v];
+            if (rem > 1) r.y = s_j[4 * v + 1];
+            if (rem > 2) r.z = s_j[4 * v + 2];
+          }
+        }
+        val[u] = r;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        int4* d_j = reinterpret_cast<int4*>(__shfl_sync(
+            FULL, reinterpret_cast<unsigned long long>(dst), jv[u] < 0 ? 0 : jv[u] >> 26));
+        if (jv[u] >= 0) st_stream_v4(d_j + (jv[u] & 0x3ffffff), val[u]);
+      }
+    }
+    const int nv = __popc(__ballot_sync(FULL, t < t1));
+    for (int i = 0; i < nv; ++i) {
+      uint8_t* m_i = reinterpret_cast<uint8_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(mdst), i));
+      const int32_t x_i = __shfl_sync(FULL, x, i);
+      const int32_t vb_i = __shfl_sync(FULL, vb, i);
+      const int32_t ve_i = __shfl_sync(FULL, ve, i);
+      if (__shfl_sync(FULL, (int)aligned, i)) {
+        if (m_i) store_mask_range(m_i, x_i, vb_i, ve_i, lane);
+      } else {
+        const int32_t* s_i = reinterpret_cast<const int32_t*>(
+            __shfl_sync(FULL, reinterpret_cast<unsigned long long>(src), i));
+        int32_t* d_i = reinterpret_cast<int32_t*>(
+            __shfl_sync(FULL, reinterpret_cast<unsigned long long>(dst), i));
+        copy_row_range<1>(s_i, d_i, m_i, x_i, vb_i, ve_i, lane, pad_id);
+      }
+    }
+  }
+  if (fl) latch_flags(sum, fl);
+}
+
+// ---------------------------------------------------------------------------------
 // TMA variant: the token bytes of each piece are fetched by one elected lane with a
 // bulk asynchronous copy (cp.async.bulk global -> shared, completion counted on an
 // mbarrier), two 8 KB staging slots per warp, so every warp keeps up to 16 KB of
@@ -569,6 +700,25 @@ static cudaError_t launch_pack_flat(bs_ctx* ctx, const int32_t* len, const int32
   return cudaGetLastError();
 }
 
+// non-persistent: one 32-piece group per warp
+template <int kU, int kMinB>
+static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                                      const int64_t* tok_off, const int32_t* tokens,
+                                      const bs_window_params& p, const bs_batch* batches,
+                                      int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                                      int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                                      bs_summary* summary, cudaStream_t st) {
+  const int64_t pieces_per_row = (p.l_max + kPiece - 1) / kPiece;
+  const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
+  const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
+  k_pack_stream<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
+      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
+      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
+      summary);
+  ++ctx->launches;
+  return cudaGetLastError();
+}
+
 template <int kU, int kMinB>
 static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                  const int64_t* tok_off, const int32_t* tokens,
@@ -602,20 +752,32 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                               summary, st)
   int v = ctx->pack_variant;
   // default: the TMA staging variant for long-context windows (rows of many KB: C4 at
-  // 89-91 % of the copy peak), the 128-bit register copy otherwise, on a non-persistent
-  // grid (CTAs retire as they finish, so the scheduling kernels of the next window in
-  // flight interleave with this pack: 0.903 vs 0.922 ms per C2 window with two windows in
-  // flight; 786 vs 793 us alone).  Tuning hook BS_PACK_VARIANT (all bit-identical):
-  //   1  register copy, persistent grid (6 CTAs/SM)     5  TMA bulk-copy staging
-  //   2  register copy, 8 vectors per lane, 4 CTAs/SM   6  cp.async shared-memory ring
-  //   17 register copy, non-persistent grid (default for l_max <= 16384)
-  if (v == 0) v = p.l_max > 16384 ? 5 : 17;
+  // 91-93 % of the copy peak with two windows in flight; the flattened stream packs
+  // faster alone, 96 %, but fills every SM and slows the window in flight), the
+  // flattened 128-bit register stream otherwise (C3 11.45 vs 12.0 ms, C2 786 vs 795 us
+  // per pack), on a non-persistent grid (CTAs retire as they finish, so the scheduling
+  // kernels of the next window in flight interleave with this pack; persistent grids of
+  // 3-4 CTAs per SM measured 2-8 % slower per window).  Tuning hook BS_PACK_VARIANT (all
+  // bit-identical):
+  //   1  k_pack, persistent grid (6 CTAs/SM)             5  TMA bulk-copy staging
+  //   2  k_pack, 8 vectors per lane, 4 CTAs/SM           6  cp.async shared-memory ring
+  //   17 k_pack, non-persistent grid                     18 k_pack_stream, 5 CTAs/SM bound
+  //   20 k_pack_stream, 4 CTAs/SM register bound (default for l_max <= 16384)
+  if (v == 0) v = p.l_max > 16384 ? 5 : 20;
   switch (v) {
     case 1: BS_PACK_V(4, 6);
     case 2: BS_PACK_V(8, 4);
     case 5:
       return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
                              batches_cap, out_tokens, out_mask, out_capacity, summary, st);
+    case 18:
+      return launch_pack_stream<4, 5>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
+                                      batch_end, batches_cap, out_tokens, out_mask, out_capacity,
+                                      summary, st);
+    case 20:
+      return launch_pack_stream<4, 4>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
+                                      batch_end, batches_cap, out_tokens, out_mask, out_capacity,
+                                      summary, st);
     case 6:
       return launch_pack_ring<4, 4, 8>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
                                        batch_end, batches_cap, out_tokens, out_mask,

@@ -283,7 +283,10 @@ def test_sharded_window_on_one_gpu(world):
         s.close()
 
 
-@pytest.mark.parametrize("variant", [1, 2, 5, 6, 17])
+PACK_VARIANTS = [1, 2, 5, 6, 17, 18, 20]
+
+
+@pytest.mark.parametrize("variant", PACK_VARIANTS)
 def test_pack_variants_bit_exact(variant, monkeypatch):
     """Every K6 variant (BS_PACK_VARIANT tuning hook) packs the same bytes."""
     monkeypatch.setenv("BS_PACK_VARIANT", str(variant))
@@ -291,6 +294,25 @@ def test_pack_variants_bit_exact(variant, monkeypatch):
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
     cfg, lens, cls = W.make_window("c2", n=50_000, seed=2)
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+
+
+@pytest.mark.parametrize("align", [1, 2, 4])
+@pytest.mark.parametrize("variant", PACK_VARIANTS)
+def test_pack_token_store_alignment(variant, align, monkeypatch):
+    """Token rows at any int32 offset (a dense CSR store, align 1) pack the same bytes as
+    the oracle: rows whose source is not 16-byte aligned take the scalar path."""
+    monkeypatch.setenv("BS_PACK_VARIANT", str(variant))
+    cfg, lens, cls = W.make_window("c2", n=20_000, seed=5)
+    spec = _cfg_spec(cfg)
+    tok_off, tokens = W.token_store(lens, align=align, seed=7)
+    sched = _sched(spec, len(lens))
+    dev = torch.device("cuda", 0)
+    h = sched.schedule(*(torch.as_tensor(a).to(dev) for a in (lens, cls, tok_off, tokens))).to_host()
+    o = _oracle(spec, lens, cls, tok_off, tokens)
+    m = int(h["summary"]["packed_elems"])
+    assert m == int(o.summary["packed_elems"])
+    assert np.array_equal(h["out_tokens"][:m], o.out_tokens[:m])
+    assert np.array_equal(h["out_mask"][:m], o.out_mask[:m])
 
 
 @pytest.mark.parametrize("agg", ["0", "1"])

@@ -23,7 +23,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
    -k regex:"k_pack|k_sort_pass|k_histogram|k_dispatch|k_bounds_small|k_size_next|k_chain|k_size_outcome" -c 9 -f -o /tmp/full \
    python tools/stage_profile.py --config c2 --steps 1 --dispatch > $OUT/ncu_full.log 2>&1
 python tools/ncu_summary.py /tmp/full.ncu-rep --json $OUT/full_summary.json > $OUT/full_summary.txt 2>&1
-for k in k_pack k_histogram k_sort_pass k_dispatch k_size_next; do
+for k in k_pack_stream k_histogram k_sort_pass k_dispatch k_size_next; do
   python tools/ncu_source.py /tmp/full.ncu-rep $k 25 > $OUT/src_$k.txt 2>&1
 done
 tail -3 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; cat $OUT/bench.json

@@ -14,7 +14,7 @@ for src, dst in (("bench.json", "bench_c2"), ("bench_c3.json", "bench_c3"), ("be
     if os.path.exists(os.path.join(S, src)):
         shutil.copy(os.path.join(S, src), os.path.join(P, f"{pre}_{dst}.json"))
 shutil.copy(os.path.join(S, "full_summary.json"), os.path.join(P, f"{pre}_ncu_c2_kernels.json"))
-for k in ("k_pack", "k_histogram", "k_sort_pass", "k_dispatch", "k_size_next"):
+for k in ("k_pack_stream", "k_pack", "k_histogram", "k_sort_pass", "k_dispatch", "k_size_next"):
     f = os.path.join(S, f"src_{k}.txt")
     if os.path.exists(f):
         shutil.copy(f, os.path.join(P, f"{pre}_ncu_src_{k}.txt"))
