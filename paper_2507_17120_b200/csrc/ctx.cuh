@@ -59,8 +59,8 @@ struct bs_ctx {
   int32_t* rowpos = nullptr;     // [max_n] admitted window row -> drain position (K6)
   int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
                                  //   <= kPiece tokens; exclusive prefix, K5f)
-  int32_t* node_j0 = nullptr;
-  int32_t* segw = nullptr;       // [7][l_cap*c_max+1] per-segment chain length / tail / bases    // [max_n + 1] first admissible position at/after each chain node
+  int32_t* node_j0 = nullptr;    // [max_n + 1] first admissible position at/after each chain node
+  int32_t* segw = nullptr;       // [7][l_cap*c_max+1] per-segment chain length / tail / bases
   int32_t* J = nullptr;          // [r_cap][max_n] 2^r-th successor in the greedy chain
   uint8_t* is_start = nullptr;   // [max_n] position starts a non-empty segment
   int32_t* listA = nullptr;      // [max_n + 1] chain-node lists (expansion ping-pong)

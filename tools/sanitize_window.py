@@ -1,0 +1,31 @@
+"""Small windows through every stage (K1..K7, all pack paths: 128-byte, 16-byte and
+unaligned token stores, long-context TMA pack, four classes), for compute-sanitizer:
+
+    compute-sanitizer --tool memcheck  --error-exitcode 9 python tools/sanitize_window.py
+    compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_window.py --small
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2507_17120_b200 import workloads as W  # noqa: E402
+from paper_2507_17120_b200.window import WindowScheduler  # noqa: E402
+
+cases = [("c2", 30000, 32), ("c2", 20000, 1), ("c4", 2000, 32), ("c3", 40000, 4)]
+if "--small" in sys.argv:
+    cases = [("c2", 3000, 32), ("c3", 3000, 1), ("c4", 300, 32)]
+for name, n, align in cases:
+    cfg, lens, cls = W.make_window(name, n=n, seed=11)
+    tok_off, tokens = W.token_store(lens, align=align)
+    s = WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
+                        policies=cfg.policies, kv_bytes_per_token=cfg.kvpt,
+                        current_safe=cfg.current_safe, device=torch.device("cuda", 0),
+                        dispatch=True)
+    h = s.schedule(*(torch.as_tensor(a).cuda() for a in (lens, cls, tok_off, tokens))).to_host()
+    assert int(h["summary"]["flags"]) == 0
+    print(name, n, align, int(h["summary"]["n_batches"]))
+    s.close()
