@@ -208,10 +208,10 @@ def main():
                     help="C1 for N > 1: torch.distributed all-reduce (NCCL over NVLink) or the "
                          "device-side exchange over CUDA-IPC peer memory (bs_peer_*), which "
                          "keeps the whole window inside one CUDA graph")
-    ap.add_argument("--inflight", type=int, default=2, help="windows in flight: consecutive "
+    ap.add_argument("--inflight", type=int, default=0, help="windows in flight: consecutive "
                     "windows alternate over this many schedulers (own scratch, outputs and CUDA "
                     "stream), so the latency-bound scheduling of one window overlaps the "
-                    "HBM-bound pack of the previous one")
+                    "HBM-bound pack of the previous ones; 0 = as many as HBM holds, up to 4")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -259,6 +259,8 @@ def main():
     lens = torch.as_tensor(lens_np).to(dev)
     cls = torch.as_tensor(cls_np).to(dev)
     tok_off, tokens = W.token_store_device(lens, seed=rank)
+    torch.cuda.synchronize(dev)
+    free0 = torch.cuda.mem_get_info(dev)[0]
     sched = WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
                             policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
                             buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
@@ -285,7 +287,13 @@ def main():
     stage_ms = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
     sched.ctx.profile_enable(0)
     # windows in flight: scheduler k (own context, outputs, stream) takes windows k, k+I, ...
-    inflight = max(1, args.inflight)
+    inflight = args.inflight
+    if inflight <= 0:  # auto: every scheduler holds its own scratch + packed output
+        torch.cuda.synchronize(dev)
+        free1 = torch.cuda.mem_get_info(dev)[0]
+        per_sched = max(1, free0 - free1)
+        inflight = int(min(4, 1 + (0.85 * free1) // per_sched))
+    inflight = max(1, inflight)
     scheds = [sched] + [
         WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
                         policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
