@@ -136,6 +136,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* v = getenv("BS_PACK_VARIANT")) ctx->pack_variant = atoi(v);
   if (const char* v = getenv("BS_HIST_AGG")) ctx->hist_agg = atoi(v);
+  if (const char* v = getenv("BS_CHAIN_WIDE")) ctx->chain_wide = atoi(v);
   int r = 1;
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;

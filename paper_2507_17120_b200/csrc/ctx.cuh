@@ -19,6 +19,8 @@ struct bs_ctx {
   int64_t launches = 0;     // kernels launched through this ctx
   int pack_variant = 0;     // K6 tuning variant (env BS_PACK_VARIANT)
   int hist_agg = 0;         // K1: 1 = warp-aggregated shared atomics (env BS_HIST_AGG)
+  int32_t piece_tok = 2048;  // K6 piece size of the last sized window (piece_tokens_for)
+  int chain_wide = -1;      // K5c: -1 = by window size, 0/1 = 512/1024 threads (env BS_CHAIN_WIDE)
   std::string err;
   // stage profiler: ring of (BS_STAGES+1) events per recorded step
   std::vector<cudaEvent_t> prof_events;
@@ -95,6 +97,14 @@ namespace bsk {
 
 constexpr int kTileX = 4096;  // lengths per K2a tile
 constexpr int kPiece = 2048;  // K6 work unit: at most this many tokens of one row
+// K6 piece size for a window of n requests: kPiece from 64k requests up; smaller windows
+// use proportionally smaller pieces (>= 32 tokens, one 128-byte line) so the pack still
+// spreads over every SM (C1's 1k requests: 32 pieces of 2048 tokens would be 32 warps)
+inline int32_t piece_tokens_for(int64_t n) {
+  int32_t t = kPiece;
+  while (t > 32 && n * (kPiece / t) < (int64_t)65536) t >>= 1;
+  return t;
+}
 
 // records boundary event `stage` (0..BS_STAGES) of the current profiled step
 inline void prof_mark(bs_ctx* ctx, int stage, cudaStream_t st) {

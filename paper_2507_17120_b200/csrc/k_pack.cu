@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
            int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
            int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
            int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
-           bs_summary* sum) {
+           bs_summary* sum, int32_t ptok) {
   const unsigned FULL = 0xffffffffu;
   int64_t b_end = b_end_arg;
   if (b_end < 0) {
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
         if (task_base[mid] <= t) lo = mid; else hi = mid;
       }
       const bs_batch B = batches[lo];
-      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int32_t pieces = (B.pitch + ptok - 1) / ptok;
       const int64_t local = t - task_base[lo];
       const int64_t row = local / pieces;
       const int32_t piece = (int32_t)(local - row * pieces);
@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
       src = tokens + tok_off[r];
       dst = out_tokens + rstart;
       mdst = out_mask ? out_mask + rstart : nullptr;
-      vb = piece * (kPiece / 4);
-      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      vb = piece * (ptok / 4);
+      const int32_t c1 = (piece + 1) * ptok < B.pitch ? (piece + 1) * ptok : B.pitch;
       ve = c1 >> 2;
     }
     const int nv = __popc(__ballot_sync(FULL, t < t1));
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
                   int32_t L, int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
                   int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in,
                   int32_t batches_cap, int32_t* __restrict__ out_tokens,
-                  uint8_t* __restrict__ out_mask, int64_t out_cap, bs_summary* sum) {
+                  uint8_t* __restrict__ out_mask, int64_t out_cap, bs_summary* sum, int32_t ptok) {
   const unsigned FULL = 0xffffffffu;
   int64_t b_end = b_end_arg;
   if (b_end < 0) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
         if (task_base[mid] <= t) lo = mid; else hi = mid;
       }
       const bs_batch B = batches[lo];
-      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int32_t pieces = (B.pitch + ptok - 1) / ptok;
       const int64_t local = t - task_base[lo];
       const int64_t row = local / pieces;
       const int32_t piece = (int32_t)(local - row * pieces);
@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
       src = tokens + tok_off[r];
       dst = out_tokens + rstart;
       mdst = out_mask ? out_mask + rstart : nullptr;
-      vb = piece * (kPiece / 4);
-      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      vb = piece * (ptok / 4);
+      const int32_t c1 = (piece + 1) * ptok < B.pitch ? (piece + 1) * ptok : B.pitch;
       ve = c1 >> 2;
     }
     const bool aligned =
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
                int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
                int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
-               bs_summary* sum) {
+               bs_summary* sum, int32_t ptok) {
   extern __shared__ __align__(128) uint8_t tma_smem[];
   __shared__ __align__(8) uint64_t bars[kTmaWarps][kTmaSlots];
   const unsigned FULL = 0xffffffffu;
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
         if (task_base[mid] <= t) lo = mid; else hi = mid;
       }
       const bs_batch B = batches[lo];
-      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int32_t pieces = (B.pitch + ptok - 1) / ptok;
       const int64_t local = t - task_base[lo];
       const int64_t row = local / pieces;
       const int32_t piece = (int32_t)(local - row * pieces);
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
       my.src = tokens + tok_off[r];
       my.dst = out_tokens + rstart;
       my.mdst = out_mask ? out_mask + rstart : nullptr;
-      my.vb = piece * (kPiece / 4);
-      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      my.vb = piece * (ptok / 4);
+      const int32_t c1 = (piece + 1) * ptok < B.pitch ? (piece + 1) * ptok : B.pitch;
       my.ve = c1 >> 2;
     }
     const int nv = __popc(__ballot_sync(FULL, t < t1));
@@ -493,7 +493,7 @@ static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_
   k_pack_tma<<<blocks, kTmaWarps * 32, smem, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary);
+      summary, ctx->piece_tok);
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 int32_t L, int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
                 int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
                 int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
-                bs_summary* sum) {
+                bs_summary* sum, int32_t ptok) {
   constexpr int kChunkV = 32 * kU;  // vectors per chunk
   extern __shared__ __align__(128) uint8_t ring_smem[];
   const unsigned FULL = 0xffffffffu;
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         if (task_base[mid] <= t) lo = mid; else hi = mid;
       }
       const bs_batch B = batches[lo];
-      const int32_t pieces = (B.pitch + kPiece - 1) / kPiece;
+      const int32_t pieces = (B.pitch + ptok - 1) / ptok;
       const int64_t local = t - task_base[lo];
       const int64_t row = local / pieces;
       const int32_t piece = (int32_t)(local - row * pieces);
@@ -567,8 +567,8 @@ __global__ void __launch_bounds__(kWarps * 32)
       my.src = tokens + tok_off[r];
       my.dst = out_tokens + rstart;
       my.mdst = out_mask ? out_mask + rstart : nullptr;
-      my.vb = piece * (kPiece / 4);
-      const int32_t c1 = (piece + 1) * kPiece < B.pitch ? (piece + 1) * kPiece : B.pitch;
+      my.vb = piece * (ptok / 4);
+      const int32_t c1 = (piece + 1) * ptok < B.pitch ? (piece + 1) * ptok : B.pitch;
       my.ve = c1 >> 2;
       my_chunks = (my.ve - my.vb + kChunkV - 1) / kChunkV;
       if (((reinterpret_cast<uintptr_t>(my.src) | reinterpret_cast<uintptr_t>(my.dst)) & 15) != 0)
@@ -675,7 +675,7 @@ static cudaError_t launch_pack_ring(bs_ctx* ctx, const int32_t* len, const int32
   k_pack_ring<kU, kNS, kWarps><<<blocks, kWarps * 32, smem, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary);
+      summary, ctx->piece_tok);
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -689,13 +689,13 @@ static cudaError_t launch_pack_flat(bs_ctx* ctx, const int32_t* len, const int32
                                     int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
                                     int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                     bs_summary* summary, cudaStream_t st) {
-  const int64_t pieces_per_row = (p.l_max + kPiece - 1) / kPiece;
+  const int64_t pieces_per_row = (p.l_max + ctx->piece_tok - 1) / ctx->piece_tok;
   const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
   k_pack<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary);
+      summary, ctx->piece_tok);
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -708,13 +708,13 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
                                       int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
                                       int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                       bs_summary* summary, cudaStream_t st) {
-  const int64_t pieces_per_row = (p.l_max + kPiece - 1) / kPiece;
+  const int64_t pieces_per_row = (p.l_max + ctx->piece_tok - 1) / ctx->piece_tok;
   const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
   k_pack_stream<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary);
+      summary, ctx->piece_tok);
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -736,7 +736,7 @@ static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t*
   k_pack<kU, kMinB><<<blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary);
+      summary, ctx->piece_tok);
   ++ctx->launches;
   return cudaGetLastError();
 }

@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(1024)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
                    const int32_t* __restrict__ misc, int64_t* __restrict__ task_base,
-                   bs_summary* sum) {
+                   bs_summary* sum, int32_t ptok) {
   __shared__ int64_t s_l[33];
   __shared__ double s_d[32];
   __shared__ int64_t s_a[32], s_p[32], s_pk[32];
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(1024)
     int64_t v = 0, rows = 0, tasks = 0;
     if (i < nb) {
       rows = batches[i].n;
-      tasks = rows * ((batches[i].pitch + kPiece - 1) / kPiece);
+      tasks = rows * ((batches[i].pitch + ptok - 1) / ptok);
       const bs_batch& B = batches[i];
       v = (int64_t)B.n * B.pitch;
       adm += B.token_sum;
@@ -926,7 +926,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
                     &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
                     (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
-    const bool wide = n > kChainWide;
+    const bool wide = ctx->chain_wide >= 0 ? ctx->chain_wide != 0 : n > kChainWide;
     e = cudaLaunchCooperativeKernel(wide ? (void*)k_chain<1024, 1> : (void*)k_chain<512, 3>,
                                     dim3(ctx->chain_blocks), dim3(wide ? 1024 : 512), args, 0,
                                     st);
@@ -938,7 +938,9 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                            ctx->listB, ctx->node_batch, misc, batches,
                                            batches_cap, summary, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary);
+  ctx->piece_tok = piece_tokens_for(n);
+  k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary,
+                                     ctx->piece_tok);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 7, st);
   k_size_outcome<<<wblocks, 256, 0, st>>>(a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB,
