@@ -404,7 +404,7 @@ class WindowScheduler:
                 self._graph = None
                 torch.cuda.synchronize(dev)
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     io_g = self._io(lens, cls, n, tok_off, tokens, pack)
                     if sharded:  # peer-connected context: C1 runs inside the fused call
                         io_g.hist_global = _ptr(self.hist_global)
@@ -438,7 +438,7 @@ class WindowScheduler:
                 self._graph = None
                 torch.cuda.synchronize(dev)
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     io_g = self._io(lens, cls, n, tok_off, tokens, pack)
                     io_g.hist_global = _ptr(self.hist_global)
                     N.check(lib.bs_window_from_hist(self.ctx.ptr, C.byref(io_g), C.byref(p),
