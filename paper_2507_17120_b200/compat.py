@@ -4,11 +4,13 @@ Drop-in classes for the scheduling path with the reference's names, argument
 meaning and error behaviour (bucket_manager.py, batch_controller.py):
 
 * `BucketSet` / `Bucket` — the stateful bucket structure the simulator drives
-  (`assign`, `adjust_buckets`, `check_partition`, counters, `dirty`).  The split /
-  merge decisions of `adjust_buckets` run on the GPU: the queued lengths are
-  histogrammed (K1) and one Alg. 1 pass runs from the current edges (K2,
-  `max_passes=1`); the host then moves the Python `Request` objects between the
-  deques exactly as bucket_manager.py:148-188 does.
+  (`assign`, `adjust_buckets`, `check_partition`, counters, `dirty`).  The set keeps
+  an incremental per-length histogram of its queued requests (+1 on assign, -1 when
+  form_batch removes a batch; revalidated against the queued total, recounted if the
+  deques were changed behind its back), and the split / merge decisions of
+  `adjust_buckets` run on the GPU as one Alg. 1 pass from the current edges over that
+  histogram (K2, `max_passes=1`); the host then moves the Python `Request` objects
+  between the deques exactly as bucket_manager.py:148-188 does.
 * `BatchController` — `form_batch` runs K4+K5 on the GPU over the bucket's
   class-filtered candidates and returns the first batch of the drain (one
   form_batch call, batch_controller.py:141-191), with the same side effects
@@ -81,6 +83,8 @@ class Bucket:
     low: int
     up: int
     requests: Deque[Request] = field(default_factory=deque)
+    # per-length counts of the owning BucketSet (kept current on add / remove_ids)
+    _counts: np.ndarray | None = field(default=None, repr=False, compare=False)
 
     def __post_init__(self) -> None:
         self.mid = (self.low + self.up) // 2
@@ -93,6 +97,8 @@ class Bucket:
         self.requests.append(request)
         if request.input_len < self.mid:
             self.short_count += 1
+        if self._counts is not None:
+            self._counts[request.input_len] += 1
 
     def remove_ids(self, ids: set) -> None:
         kept: Deque[Request] = deque()
@@ -100,6 +106,8 @@ class Bucket:
             if r.id in ids:
                 if r.input_len < self.mid:
                     self.short_count -= 1
+                if self._counts is not None:
+                    self._counts[r.input_len] -= 1
             else:
                 kept.append(r)
         self.requests = kept
@@ -110,7 +118,7 @@ class Bucket:
 
 class BucketSet:
     """Ordered contiguous buckets + split/merge policy (bucket_manager.py:72-216).
-    Split/merge decisions run on the GPU (K1 histogram + one K2 pass)."""
+    Split/merge decisions run on the GPU (one K2 pass over the incremental histogram)."""
 
     def __init__(self, max_seq_len: int, split_threshold: float = 0.5,
                  buckets: list[Bucket] | None = None):
@@ -121,6 +129,10 @@ class BucketSet:
         self.max_seq_len = max_seq_len
         self.split_threshold = split_threshold
         self.buckets: list[Bucket] = buckets if buckets is not None else [Bucket(0, max_seq_len)]
+        # incremental per-length histogram of the queued requests: +1 on
+        # assign / Bucket.add, -1 on Bucket.remove_ids; adjust_buckets uploads it
+        self._counts = np.zeros(max_seq_len, np.int64)
+        self._rebuild_counts()
         self.dirty = True
         self.assign_calls = 0
         self.assign_comparisons = 0
@@ -143,6 +155,26 @@ class BucketSet:
     def edges(self) -> list[int]:
         return [b.low for b in self.buckets] + [self.buckets[-1].up]
 
+    def _rebuild_counts(self) -> bool:
+        """Recount from the deques (construction, or after the deques were changed
+        behind the set's back); False if some queued length is outside [0, L)."""
+        self._counts[:] = 0
+        lens = np.fromiter((r.input_len for r in self.iter_requests()), np.int64)
+        ok = bool(lens.size == 0 or (lens.min() >= 0 and lens.max() < self.max_seq_len))
+        if ok:
+            np.add.at(self._counts, lens, 1)
+        for b in self.buckets:
+            b._counts = self._counts if ok else None
+        return ok
+
+    def _current_counts(self) -> np.ndarray | None:
+        """The incremental histogram, revalidated in O(L + K): every bucket must be
+        attached and the counts must add up to the queued total; otherwise recount."""
+        if (all(b._counts is self._counts for b in self.buckets)
+                and int(self._counts.sum()) == self.total_requests):
+            return self._counts
+        return self._counts if self._rebuild_counts() else None
+
     def assign(self, request: Request) -> int:
         """bucket_manager.py:110-131 (bisect over the uppers; same result and counters)."""
         if not 0 <= request.input_len < self.max_seq_len:
@@ -157,6 +189,8 @@ class BucketSet:
         b.requests.append(request)
         if request.input_len < b.mid:
             b.short_count += 1
+        if b._counts is not None:
+            b._counts[request.input_len] += 1
         self.assign_comparisons += idx + 1
         self.last_assign_comparisons = idx + 1
         return idx
@@ -165,22 +199,32 @@ class BucketSet:
         """One Alg. 1 pass (bucket_manager.py:133-191); decisions from the GPU."""
         self.adjust_calls += 1
         self.adjust_bucket_scans += len(self.buckets)
-        reqs = list(self.iter_requests())
         edges = self.edges()
-        lens = np.fromiter((r.input_len for r in reqs), np.int32, len(reqs))
-        sched = _scheduler(len(reqs), max_seq_len=self.max_seq_len, n_classes=1,
-                           policies=(DispatchPolicy.FCFS,), split_threshold=self.split_threshold,
-                           kv_bytes_per_token=1, current_safe=0, truncate=False)
-        new_edges, changes, _ = sched.boundaries(lens, init_edges=edges, n_max=int(n_max),
-                                                 max_passes=1)
+        counts = self._current_counts()
+        if counts is not None:  # K2 on the incremental histogram (C*L words uploaded)
+            sched = _scheduler(1, max_seq_len=self.max_seq_len, n_classes=1,
+                               policies=(DispatchPolicy.FCFS,),
+                               split_threshold=self.split_threshold, kv_bytes_per_token=1,
+                               current_safe=0, truncate=False)
+            new_edges, changes, _ = sched.boundaries_from_hist(
+                counts, init_edges=edges, n_max=int(n_max), max_passes=1)
+        else:  # a queued length outside [0, L): K1 latches it and the reference error is raised
+            reqs = list(self.iter_requests())
+            lens = np.fromiter((r.input_len for r in reqs), np.int32, len(reqs))
+            sched = _scheduler(len(reqs), max_seq_len=self.max_seq_len, n_classes=1,
+                               policies=(DispatchPolicy.FCFS,),
+                               split_threshold=self.split_threshold, kv_bytes_per_token=1,
+                               current_safe=0, truncate=False)
+            new_edges, changes, _ = sched.boundaries(lens, init_edges=edges, n_max=int(n_max),
+                                                     max_passes=1)
         new_edges = [int(e) for e in new_edges]
         if not changes:
             self.dirty = False
             return []
         if changes[0].kind == "merge":  # bucket_manager.py:148-156
-            merged = sorted(reqs, key=_ARRIVAL_ORDER)
+            merged = sorted(self.iter_requests(), key=_ARRIVAL_ORDER)
             self.requests_moved += len(merged)
-            self.buckets = [Bucket(0, self.max_seq_len, deque(merged))]
+            self.buckets = [Bucket(0, self.max_seq_len, deque(merged), self._counts)]
             return changes
         split_mid = {c.parent_low: c.midpoint for c in changes if c.kind == "split"}
         new_buckets: list[Bucket] = []
@@ -189,8 +233,10 @@ class BucketSet:
             if mid is None:
                 new_buckets.append(b)
                 continue
-            left = Bucket(b.low, mid, deque(r for r in b.requests if r.input_len < mid))
-            right = Bucket(mid, b.up, deque(r for r in b.requests if r.input_len >= mid))
+            left = Bucket(b.low, mid, deque(r for r in b.requests if r.input_len < mid),
+                          b._counts)
+            right = Bucket(mid, b.up, deque(r for r in b.requests if r.input_len >= mid),
+                           b._counts)
             self.requests_moved += len(b.requests)
             new_buckets.extend((left, right))
         self.buckets = new_buckets

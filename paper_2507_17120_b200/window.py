@@ -527,6 +527,41 @@ class WindowScheduler:
         res.check()
         return res.edges(), res.changes(), res.summary()
 
+    def boundaries_from_hist(self, hist, *, init_edges=None, n_max=None, max_passes=None):
+        """K2 only, on a caller-maintained histogram (int [C, L] or [L] for one class):
+        the incremental form SURVEY f1 asks for — the stateful BucketSet keeps per-length
+        counts up to date on assign / removal and uploads C*L words per adjust instead of
+        re-histogramming every queued request.  Same returns as boundaries()."""
+        h = np.ascontiguousarray(np.asarray(hist).reshape(-1), dtype=np.int64)
+        Cn, L = self.cfg.n_classes, self.cfg.max_seq_len
+        if h.size != Cn * L:
+            raise ValueError(f"histogram has {h.size} counts, expected {Cn * L}")
+        if h.size and (h.min() < 0 or h.max() > 0xFFFFFFFF):
+            raise ValueError("histogram counts out of range")
+        p = N.WindowParams.from_buffer_copy(self._params)
+        if n_max is not None:
+            p.n_max = int(n_max)
+        if max_passes is not None:
+            p.max_passes = int(max_passes)
+        ie, k_init = self.init_edges, self.k_init
+        if init_edges is not None:
+            e = np.asarray(init_edges, np.int32)
+            ie, k_init = torch.as_tensor(e).to(self.device), len(e) - 1
+        lib = N.load()
+        st = _stream_handle(self.device)
+        with torch.cuda.device(self.device):
+            # an empty K1 initialises the summary; the counts then replace the histogram
+            N.check(lib.bs_histogram(self.ctx.ptr, None, None, 0, C.byref(p), _ptr(self.hist),
+                                     _ptr(self.summary), st), self.ctx.ptr)
+            self.hist.copy_(torch.from_numpy(h.astype(np.uint32).view(np.int32)))
+            N.check(lib.bs_boundaries(self.ctx.ptr, _ptr(self.hist), _ptr(self.hist), C.byref(p),
+                                      _ptr(ie), k_init, _ptr(self.edges), _ptr(self.changes),
+                                      self.changes_cap, _ptr(self.summary), st), self.ctx.ptr)
+        torch.cuda.current_stream(self.device).synchronize()
+        res = WindowResult(self, int(h.sum()), False)
+        res.check()
+        return res.edges(), res.changes(), res.summary()
+
     def monitor_bins(self, bins: int = 64) -> np.ndarray:
         """f2: the 64-bin LengthHistogram view of the last window (pd_sim.py:828-833)."""
         out = torch.zeros(bins, dtype=torch.int64, device=self.device)

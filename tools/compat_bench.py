@@ -50,7 +50,7 @@ def build(q, seed=3):
 
 
 for q in a.q:
-    t_adj, t_form, nb = [], [], 0
+    t_adj, t_form, t_steady, nb = [], [], [], 0
     for rep in range(a.reps):
         bs, ctl = build(q, seed=3 + rep)
         n_max = ctl.current_n_max(bs)
@@ -61,6 +61,9 @@ for q in a.q:
                 t_adj.append(time.perf_counter() - t0)
             if not any(c.kind == "split" for c in ch):
                 break
+        t0 = time.perf_counter()  # steady state: a pass at the fixpoint (no change)
+        bs.adjust_buckets(n_max)
+        t_steady.append(time.perf_counter() - t0)
         # one form_batch on the bucket holding the most offline requests
         big = max(range(len(bs.buckets)), key=lambda k: sum(
             1 for r in bs.buckets[k].requests if r.task_class is TaskClass.OFFLINE))
@@ -70,5 +73,6 @@ for q in a.q:
         nb = len(plan) if plan is not None else 0
     print(json.dumps({"impl": a.impl, "queue": q, "buckets": len(bs.buckets),
                       "adjust_first_pass_ms_median": 1e3 * float(np.median(t_adj)),
+                      "adjust_steady_ms_median": 1e3 * float(np.median(t_steady)),
                       "form_batch_ms_median": 1e3 * float(np.median(t_form)),
                       "batch_size": nb, "reps": a.reps}))
