@@ -211,3 +211,42 @@ def test_trace_file_to_gpu_window(tmp_path):
     assert [len(p_) for p_ in out.plans] == res.batches()["n"].tolist()
     assert out.bucket_set.edges() == res.edges().tolist()
     s.close()
+
+
+def test_boundaries_from_hist_equals_k1_path():
+    """K2 on a caller-maintained histogram (the BucketSet's incremental counts) gives
+    the same edges / change log / n_max as K1 + K2 on the lengths themselves."""
+    import torch
+
+    from paper_2507_17120_b200.window import WindowScheduler
+    rng = np.random.default_rng(11)
+    s = WindowScheduler(max_requests=50_000, max_seq_len=4096, n_classes=1,
+                        policies=(DispatchPolicy.FCFS,), kv_bytes_per_token=2,
+                        current_safe=10**9, truncate=False, device=torch.device("cuda", 0))
+    for trial in range(12):
+        n = int(rng.integers(0, 50_000))
+        lens = np.clip(np.rint(rng.lognormal(5.5, 1.2, n)), 0, 4095).astype(np.int32)
+        edges = [0, 4096] if trial % 3 == 0 else sorted({0, 4096, *map(int, rng.integers(1, 4095, 5))})
+        n_max = int(rng.integers(1, 3000))
+        passes = [1, 0][trial % 2]
+        a = s.boundaries(lens, init_edges=edges, n_max=n_max, max_passes=passes)
+        b = s.boundaries_from_hist(np.bincount(lens, minlength=4096), init_edges=edges,
+                                   n_max=n_max, max_passes=passes)
+        assert list(a[0]) == list(b[0])
+        assert [(c.kind, c.parent_low, c.parent_up, c.midpoint) for c in a[1]] == \
+               [(c.kind, c.parent_low, c.parent_up, c.midpoint) for c in b[1]]
+        assert a[2]["n_max"] == b[2]["n_max"] and a[2]["total_global"] == b[2]["total_global"]
+
+
+def test_adjust_after_outside_deque_mutation_recounts():
+    """Requests appended to a deque without assign() are still counted by the next
+    adjust_buckets (the incremental histogram is revalidated and rebuilt)."""
+    bs = BucketSet(2048, buckets=[_bucket(0, 2048, [500] * 8)])
+    for i in range(8):
+        bs.buckets[0].requests.append(_req(100 + i, 1500))  # 8 + 8: no split at n_max 16
+    assert bs.adjust_buckets(16) == []
+    for i in range(8):
+        bs.buckets[0].requests.append(_req(200 + i, 300))   # 16 short of 24 > n_max: split
+    ch = bs.adjust_buckets(16)
+    assert [c.kind for c in ch] == ["split"]
+    assert [(b.low, b.up, len(b)) for b in bs.buckets] == [(0, 1024, 16), (1024, 2048, 8)]

@@ -1,2 +1,1 @@
-python -m pytest tests -m gpu -q -x -k "compat" 2>&1 | tail -2
-python tools/compat_bench.py --q 10000 100000 --reps 3
+python -m pytest tests/test_compat_gpu.py tests/test_compat_sim_replay.py -q -x 2>&1 | tail -3
