@@ -51,8 +51,9 @@ def _pack_kernel(l_max):
     """the K6 kernel the library launches by default (k_pack.cu: launch_pack)."""
     v = int(os.environ.get("BS_PACK_VARIANT", "0") or 0)
     if v == 0:
-        v = 5 if l_max > 16384 else 20
-    return {5: "k_pack_tma", 6: "k_pack_ring", 18: "k_pack_stream", 20: "k_pack_stream"}.get(v, "k_pack")
+        v = 5 if l_max > 16384 else 21
+    return {5: "k_pack_tma", 6: "k_pack_ring", 18: "k_pack_stream", 20: "k_pack_stream",
+            21: "k_pack_stream", 22: "k_pack_stream"}.get(v, "k_pack")
 
 
 def _profile_traffic(cfg_name, kernel):

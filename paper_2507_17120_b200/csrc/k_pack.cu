@@ -172,8 +172,12 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
 // here each round trip carries a full 32 * kU * 16 bytes.  A lane finds the piece of
 // stream position q by a 5-step binary search over the lanes' scan values (shuffles);
 // rows whose source is not 16-byte aligned take copy_row_range's scalar path after
-// the stream.  The mask is written per piece as in k_pack.
-template <int kU, int kMinBlocks>
+// the stream.  The mask is written per piece as in k_pack.  kUni adds the fast path
+// for uniform groups — 32 consecutive one-piece rows of equal pitch, i.e. nearly every
+// group inside a batch: their output rows are contiguous, so a vector's row is q / V
+// (one multiply, no search), tokens and mask go out as two contiguous streams and only
+// the row's source pointer and length are shuffled per vector.
+template <int kU, int kMinBlocks, bool kUni>
 __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
     k_pack_stream(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
                   const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
@@ -234,6 +238,74 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
     const int32_t incl = warp_incl_scan(cnt);
     const int32_t pre = incl - cnt;  // stream position of this lane's first vector
     const int32_t total = __shfl_sync(FULL, incl, 31);
+    if constexpr (kUni) {
+      // uniform group (the common case: 32 consecutive one-piece rows of one batch):
+      // the output rows are contiguous, so the token and mask streams are plain
+      // contiguous stores and a vector's row is q / V (no search, no dst shuffles)
+      const int32_t V0 = __shfl_sync(FULL, ve - vb, 0);
+      int32_t* d0 = reinterpret_cast<int32_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(dst), 0));
+      uint8_t* m0 = reinterpret_cast<uint8_t*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(mdst), 0));
+      const bool mine =
+          t >= t1 || (aligned && vb == 0 && ve == V0 && dst == d0 + (int64_t)lane * 4 * V0 &&
+                      mdst == (m0 ? m0 + (int64_t)lane * 4 * V0 : nullptr));
+      if (__all_sync(FULL, mine) && V0 > 0 &&
+          (reinterpret_cast<uintptr_t>(m0) & 15) == 0) {
+        const int nvl = __popc(__ballot_sync(FULL, t < t1));
+        const int32_t tot = nvl * V0;
+        const float rcp = 1.0f / (float)V0;
+        int4* d4 = reinterpret_cast<int4*>(d0);
+        for (int32_t q0 = 0; q0 < tot; q0 += 32 * kU) {
+          int4 val[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int32_t q = q0 + u * 32 + lane;
+            int j = __float2int_rz((float)q * rcp);
+            if (j * V0 > q) --j; else if ((j + 1) * V0 <= q) ++j;
+            j = j > 31 ? 31 : j;
+            const int32_t* s_j = reinterpret_cast<const int32_t*>(
+                __shfl_sync(FULL, reinterpret_cast<unsigned long long>(src), j));
+            const int32_t x_j = __shfl_sync(FULL, x, j);
+            const int32_t v = q - j * V0;
+            const int32_t full = x_j >> 2, rem = x_j & 3;
+            int4 r = pad4;
+            if (q < tot) {
+              if (v < full) {
+                r = ld_stream_v4(reinterpret_cast<const int4*>(s_j) + v);
+              } else if (v == full && rem) {
+                r.x = s_j[4 * v];
+                if (rem > 1) r.y = s_j[4 * v + 1];
+                if (rem > 2) r.z = s_j[4 * v + 2];
+              }
+            }
+            val[u] = r;
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int32_t q = q0 + u * 32 + lane;
+            if (q < tot) st_stream_v4(d4 + q, val[u]);
+          }
+        }
+        if (m0) {  // 16-byte mask words (16 columns; rows are 32-byte multiples)
+          const int32_t words = tot >> 2;
+          int4* mw = reinterpret_cast<int4*>(m0);
+          const float rcpw = 4.0f / (float)V0;
+          for (int32_t mb = 0; mb < words; mb += 32) {
+            const int32_t m = mb + lane;
+            int j = __float2int_rz((float)m * rcpw);
+            if (j * V0 > 4 * m) --j; else if ((j + 1) * V0 <= 4 * m) ++j;
+            j = j > 31 ? 31 : j;
+            const int32_t x_j = __shfl_sync(FULL, x, j);
+            const int32_t k = x_j - (16 * m - j * 4 * V0);
+            if (m < words)
+              st_stream_v4(mw + m, make_int4((int)mask_word(k), (int)mask_word(k - 4),
+                                             (int)mask_word(k - 8), (int)mask_word(k - 12)));
+          }
+        }
+        continue;
+      }
+    }
     for (int32_t q0 = 0; q0 < total; q0 += 32 * kU) {
       int4 val[kU];
       int32_t jv[kU];  // (piece lane << 26) | vector in row, -1 past the stream
@@ -701,7 +773,7 @@ static cudaError_t launch_pack_flat(bs_ctx* ctx, const int32_t* len, const int32
 }
 
 // non-persistent: one 32-piece group per warp
-template <int kU, int kMinB>
+template <int kU, int kMinB, bool kUni = false>
 static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                       const int64_t* tok_off, const int32_t* tokens,
                                       const bs_window_params& p, const bs_batch* batches,
@@ -711,7 +783,7 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
   const int64_t pieces_per_row = (p.l_max + ctx->piece_tok - 1) / ctx->piece_tok;
   const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
-  k_pack_stream<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
+  k_pack_stream<kU, kMinB, kUni><<<(unsigned)blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
       summary, ctx->piece_tok);
@@ -752,18 +824,19 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                               summary, st)
   int v = ctx->pack_variant;
   // default: the TMA staging variant for long-context windows (rows of many KB: C4 at
-  // 91-93 % of the copy peak with two windows in flight; the flattened stream packs
-  // faster alone, 96 %, but fills every SM and slows the window in flight), the
-  // flattened 128-bit register stream otherwise (C3 11.45 vs 12.0 ms, C2 786 vs 795 us
-  // per pack), on a non-persistent grid (CTAs retire as they finish, so the scheduling
-  // kernels of the next window in flight interleave with this pack; persistent grids of
-  // 3-4 CTAs per SM measured 2-8 % slower per window).  Tuning hook BS_PACK_VARIANT (all
-  // bit-identical):
+  // 90-91 % of the copy peak with windows in flight; the register stream packs faster
+  // alone, 96 %, but fills every SM and slows the windows in flight), the flattened
+  // 128-bit register stream with the uniform-group fast path otherwise (C2 758 vs 786
+  // us, C3 11.11 vs 11.45 ms against the stream without it), on a non-persistent grid
+  // (CTAs retire as they finish, so the scheduling kernels of the windows in flight
+  // interleave with this pack; persistent grids of 3-4 CTAs per SM measured 2-8 %
+  // slower per window).  Tuning hook BS_PACK_VARIANT (all bit-identical):
   //   1  k_pack, persistent grid (6 CTAs/SM)             5  TMA bulk-copy staging
   //   2  k_pack, 8 vectors per lane, 4 CTAs/SM           6  cp.async shared-memory ring
   //   17 k_pack, non-persistent grid                     18 k_pack_stream, 5 CTAs/SM bound
-  //   20 k_pack_stream, 4 CTAs/SM register bound (default for l_max <= 16384)
-  if (v == 0) v = p.l_max > 16384 ? 5 : 20;
+  //   20 k_pack_stream, 4 CTAs/SM, no uniform fast path  22 as 21, 8 vectors per lane
+  //   21 k_pack_stream, 4 CTAs/SM + uniform-group fast path (default for l_max <= 16384)
+  if (v == 0) v = p.l_max > 16384 ? 5 : 21;
   switch (v) {
     case 1: BS_PACK_V(4, 6);
     case 2: BS_PACK_V(8, 4);
@@ -774,6 +847,14 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
       return launch_pack_stream<4, 5>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
                                       batch_end, batches_cap, out_tokens, out_mask, out_capacity,
                                       summary, st);
+    case 21:
+      return launch_pack_stream<4, 4, true>(ctx, len, perm, tok_off, tokens, p, batches,
+                                            batch_begin, batch_end, batches_cap, out_tokens,
+                                            out_mask, out_capacity, summary, st);
+    case 22:
+      return launch_pack_stream<8, 3, true>(ctx, len, perm, tok_off, tokens, p, batches,
+                                            batch_begin, batch_end, batches_cap, out_tokens,
+                                            out_mask, out_capacity, summary, st);
     case 20:
       return launch_pack_stream<4, 4>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
                                       batch_end, batches_cap, out_tokens, out_mask, out_capacity,

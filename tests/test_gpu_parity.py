@@ -283,7 +283,7 @@ def test_sharded_window_on_one_gpu(world):
         s.close()
 
 
-PACK_VARIANTS = [1, 2, 5, 6, 17, 18, 20]
+PACK_VARIANTS = [1, 2, 5, 6, 17, 18, 20, 21, 22]
 
 
 @pytest.mark.parametrize("variant", PACK_VARIANTS)
