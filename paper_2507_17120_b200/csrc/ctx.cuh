@@ -20,6 +20,7 @@ struct bs_ctx {
   int pack_variant = 0;     // K6 tuning variant (env BS_PACK_VARIANT)
   int hist_agg = 0;         // K1: 1 = warp-aggregated shared atomics (env BS_HIST_AGG)
   int32_t piece_tok = 2048;  // K6 piece size of the last sized window (piece_tokens_for)
+  int64_t pack_pieces = 0;   // upper bound on its K6 pieces: n * ceil(l_max / piece_tok)
   int chain_wide = -1;      // K5c: -1 = by window size, 0/1 = 512/1024 threads (env BS_CHAIN_WIDE)
   std::string err;
   // stage profiler: ring of (BS_STAGES+1) events per recorded step

@@ -761,8 +761,7 @@ static cudaError_t launch_pack_flat(bs_ctx* ctx, const int32_t* len, const int32
                                     int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
                                     int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                     bs_summary* summary, cudaStream_t st) {
-  const int64_t pieces_per_row = (p.l_max + ctx->piece_tok - 1) / ctx->piece_tok;
-  const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
+  const int64_t groups = (ctx->pack_pieces + 31) / 32;  // bound from the last sized window
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
   k_pack<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
@@ -780,8 +779,7 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
                                       int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
                                       int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                       bs_summary* summary, cudaStream_t st) {
-  const int64_t pieces_per_row = (p.l_max + ctx->piece_tok - 1) / ctx->piece_tok;
-  const int64_t groups = (ctx->max_n * pieces_per_row + 31) / 32;
+  const int64_t groups = (ctx->pack_pieces + 31) / 32;  // bound from the last sized window
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
   k_pack_stream<kU, kMinB, kUni><<<(unsigned)blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,

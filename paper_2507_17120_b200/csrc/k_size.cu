@@ -939,6 +939,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                            batches_cap, summary, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ctx->piece_tok = piece_tokens_for(n);
+  ctx->pack_pieces = n * (((int64_t)p.l_max + ctx->piece_tok - 1) / ctx->piece_tok);
   k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary,
                                      ctx->piece_tok);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
