@@ -16,6 +16,7 @@ timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --dispatch --steps 50 --no-cpu-baseline --no-e2e > $OUT/bench_dispatch.json 2> $OUT/bench_dispatch.err
 timeout 600 python bench.py --config c3 --steps 20 --no-cpu-baseline > $OUT/bench_c3.json 2> $OUT/bench_c3.err
 timeout 600 python bench.py --config c4 --steps 20 --no-cpu-baseline > $OUT/bench_c4.json 2> $OUT/bench_c4.err
+timeout 600 python bench.py --config c1 --steps 200 > $OUT/bench_c1.json 2> $OUT/bench_c1.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1

@@ -10,6 +10,7 @@ S = sys.argv[1]
 pre = sys.argv[2] if len(sys.argv) > 2 else "r1"
 P = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
 for src, dst in (("bench.json", "bench_c2"), ("bench_c3.json", "bench_c3"), ("bench_c4.json", "bench_c4"),
+                 ("bench_c1.json", "bench_c1"),
                  ("bench_dispatch.json", "bench_c2_dispatch"), ("bench_ref.json", "bench_reference_arm")):
     if os.path.exists(os.path.join(S, src)):
         shutil.copy(os.path.join(S, src), os.path.join(P, f"{pre}_{dst}.json"))
