@@ -927,9 +927,11 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                     &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
                     (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
     const bool wide = ctx->chain_wide >= 0 ? ctx->chain_wide != 0 : n > kChainWide;
+    // small windows: fewer CTAs (a grid barrier over 148 CTAs costs more than the work)
+    const unsigned cblocks = (unsigned)std::min<int64_t>(
+        ctx->chain_blocks, std::max<int64_t>(1, (n + 4095) / 4096));
     e = cudaLaunchCooperativeKernel(wide ? (void*)k_chain<1024, 1> : (void*)k_chain<512, 3>,
-                                    dim3(ctx->chain_blocks), dim3(wide ? 1024 : 512), args, 0,
-                                    st);
+                                    dim3(cblocks), dim3(wide ? 1024 : 512), args, 0, st);
     if (e != cudaSuccess) return e;
   }
   prof_mark(ctx, 6, st);
