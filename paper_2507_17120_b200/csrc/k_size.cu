@@ -732,17 +732,21 @@ __global__ void __launch_bounds__(256)
   for (int64_t g = wg; g < G; g += wstride) {
     const int64_t j = (g << 5) + lane;
     // chain node covering j: last node position <= j (nodes ascend and every segment
-    // start is a node, so the node lies in j's segment); one binary search per warp
-    int lo0 = 0;
-    if (lane == 0) {
-      int lo = 0, hi = M;
+    // start is a node, so the node lies in j's segment); one 32-ary search per warp
+    // (every lane probes one point per step: log32(M) dependent loads instead of log2)
+    int lo = 0;
+    {
+      int hi = M;
+      const int64_t target = g << 5;
       while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (list[mid] <= (g << 5)) lo = mid; else hi = mid;
+        const int step = (hi - lo + 31) >> 5;
+        const int pidx = lo + (lane + 1) * step;
+        const bool le = pidx < hi && list[pidx] <= target;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, le));
+        lo += cnt * step;
+        hi = min(hi, lo + step);
       }
-      lo0 = lo;
     }
-    int lo = __shfl_sync(0xffffffffu, lo0, 0);
     const bool in = j < a.n;
     if (in)
       while (lo + 1 < M && list[lo + 1] <= j) ++lo;
