@@ -8,15 +8,17 @@
 // batch's waste_ratio (memory_model.py:92-100).
 //
 // B200 mapping: purely HBM-bound (read 4*len bytes, write 5*pitch bytes per row).
-// Work unit = a piece of <= kPiece tokens of one row (long-context rows split into
-// many pieces, so 128k-token rows are spread over many warps).  Groups of 32
-// consecutive pieces go round-robin to the warps of the resident grid, so the
-// warps in flight touch neighbouring rows (DRAM-page / TLB locality; an equal-
-// slice split was measured 3.6x slower).  The lanes fetch the 32 pieces' metadata
-// in parallel (batch by binary search, row map -> request -> token offset /
-// length), then the warp copies them with 128-bit streaming loads
-// (ld.global.nc.L1::no_allocate, 4 in flight per lane) and evict-first 128-bit
-// stores (st.global.cs), the mask as 32-bit stores.
+// Work unit = a piece of <= piece_tok tokens of one row (kPiece = 2048 from 64k
+// requests up, smaller for small windows; long-context rows split into many pieces,
+// so 128k-token rows are spread over many warps).  Groups of 32 consecutive pieces
+// go to the warps of a non-persistent grid, so the warps in flight touch
+// neighbouring rows (DRAM-page / TLB locality; an equal-slice split was measured
+// 3.6x slower).  The lanes fetch the 32 pieces' metadata in parallel (batch by
+// binary search, row map -> request -> token offset / length), then the warp copies
+// them with 128-bit streaming loads (ld.global.nc.L1::no_allocate, 4 in flight per
+// lane) and evict-first 128-bit stores (st.global.cs).  Default kernel:
+// k_pack_stream with the uniform-group fast path (L <= 16384), k_pack_tma above;
+// the other variants are tuning hooks (launch_pack, bottom of this file).
 #include "ctx.cuh"
 
 namespace bsk {
