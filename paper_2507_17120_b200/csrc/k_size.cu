@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(256)
                    int32_t* __restrict__ req_batch, int32_t* __restrict__ req_row,
                    int32_t* __restrict__ rowpos, bs_summary* sum,
                    const int32_t* __restrict__ slen, int32_t* __restrict__ dmin,
-                   int64_t* __restrict__ dsum) {
+                   int64_t* __restrict__ dsum, int32_t r_lo, int32_t r_hi, int first) {
   const int M = misc[64];
   const int32_t* list = misc[68] ? listB : listA;
   const int lane = threadIdx.x & 31;
@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(256)
     const bool in = j < a.n;
     if (in)
       while (lo + 1 < M && list[lo + 1] <= j) ++lo;
-    if (dmin) {
+    if (dmin && first) {
       // K7 per-call accumulators: min arrival rank and length sum over the call's range
       // (lanes of one call are contiguous: one atomic per call and warp)
       const unsigned peers = __match_any_sync(0xffffffffu, in ? lo : -1);
@@ -769,24 +769,35 @@ __global__ void __launch_bounds__(256)
     const uint32_t m = bmask[g];
     const bool nr = (m >> lane) & 1u;
     const int32_t r = perm[j];
+    // large windows run this kernel once per request-id range, so each pass's scattered
+    // outcome writes stay inside L2 and fill whole sectors (no DRAM read-modify-write);
+    // the position-ordered row map and the counters are written by the first pass
+    const bool mine = r >= r_lo && r < r_hi;
     if (b >= 0) {
       if (nr) {
         const int64_t gc = c >> 5;
         const int32_t Rj = Rg[g] + __popc(m & ((1u << lane) - 1u));
         const int32_t Rc = Rg[gc] + __popc(bmask[gc] & ((1u << (c & 31)) - 1u));
-        req_batch[r] = b;
-        req_row[r] = Rj - Rc;
-        if (b < batches_cap) rowpos[batches[b].row_base + (Rj - Rc)] = (int32_t)j;  // K6 row map
+        if (mine) {
+          req_batch[r] = b;
+          req_row[r] = Rj - Rc;
+        }
+        if (first && b < batches_cap)
+          rowpos[batches[b].row_base + (Rj - Rc)] = (int32_t)j;  // K6 row map
       } else {
-        req_batch[r] = BS_REQ_REJECTED;
-        req_row[r] = -1;
-        ++rej;
+        if (mine) {
+          req_batch[r] = BS_REQ_REJECTED;
+          req_row[r] = -1;
+        }
+        rej += first;
       }
     } else {  // a segment's empty tail: rejected up to the first admissible request, pending after
       const int64_t j0 = node_j0[lo];
-      req_row[r] = -1;
-      if (j < j0) { req_batch[r] = BS_REQ_REJECTED; ++rej; }
-      else { req_batch[r] = BS_REQ_PENDING; ++pend; }
+      if (mine) {
+        req_row[r] = -1;
+        req_batch[r] = j < j0 ? BS_REQ_REJECTED : BS_REQ_PENDING;
+      }
+      if (j < j0) rej += first; else pend += first;
     }
   }
   rej = warp_sum(rej);
@@ -955,12 +966,23 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                      ctx->piece_tok);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 7, st);
-  k_size_outcome<<<wblocks, 256, 0, st>>>(a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB,
-                                          ctx->node_batch, ctx->node_j0, misc, batches,
-                                          batches_cap, req_batch, req_row, ctx->rowpos, summary,
-                                          ctx->sorted_len, p.dispatch ? ctx->disp_cmin : nullptr,
-                                          p.dispatch ? ctx->disp_csum : nullptr);
-  ctx->launches += 6;
+  // outcome arrays beyond 32 MB (4M requests) are scattered in request-id ranges of
+  // <= 32 MB (C3, 16M requests: 4 passes, 0.60 vs 0.72 ms; 3 passes of 43 MB gain
+  // nothing, every extra pass re-reads the positions, ~0.1 ms at 16M)
+  const char* pv = getenv("BS_OUTCOME_PARTS");  // tuning / test hook
+  const int parts_env = pv ? std::max(1, atoi(pv)) : 0;
+  const int parts = parts_env ? parts_env
+                              : (int)std::max<int64_t>(1, (n * 8 + (32LL << 20) - 1) / (32LL << 20));
+  const int64_t span = (n + parts - 1) / parts;
+  for (int q = 0; q < parts; ++q) {
+    k_size_outcome<<<wblocks, 256, 0, st>>>(
+        a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB, ctx->node_batch, ctx->node_j0, misc,
+        batches, batches_cap, req_batch, req_row, ctx->rowpos, summary, ctx->sorted_len,
+        p.dispatch ? ctx->disp_cmin : nullptr, p.dispatch ? ctx->disp_csum : nullptr,
+        (int32_t)std::min<int64_t>(n, q * span), (int32_t)std::min<int64_t>(n, (q + 1) * span),
+        q == 0);
+  }
+  ctx->launches += 5 + parts;
   return cudaGetLastError();
 }
 

@@ -395,3 +395,15 @@ def test_sharded_window_graph_replay_matches_eager():
             assert np.array_equal(g[k], eager[k]), k
     assert int(g["summary"]["total_global"]) == 120_000
     s.close()
+
+
+@pytest.mark.parametrize("parts", ["2", "3", "7"])
+def test_outcome_in_request_id_ranges(parts, monkeypatch):
+    """K5e's range-partitioned scatter (used above 32 MB of outcome arrays) writes the
+    same outcomes, rows, row map and counters as one pass — forced here on windows with
+    rejections, pending requests and four classes."""
+    monkeypatch.setenv("BS_OUTCOME_PARTS", parts)
+    cfg, lens, cls = W.make_window("c3", n=60_000, seed=9)
+    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+    for name in ("reject_heavy_acc0", "pledged_acc1", "zero_headroom", "four_class_exact"):
+        test_gpu_matches_reference_fixture(name)
