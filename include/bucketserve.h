@@ -201,7 +201,8 @@ int bs_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
  * batches_out: capacity batches_cap; count in summary->n_batches.
  * req_batch_out[i]: batch index, BS_REQ_PENDING or BS_REQ_REJECTED; req_row_out[i]:
  * row inside its batch (-1 if none).  out_offset of each batch is the exclusive
- * prefix of n * pitch in emission order. */
+ * prefix of n * pitch in emission order.  perm / seg_off must be the last bs_order
+ * result on ctx (its sorted slots give each position's segment and SJF/LJF length). */
 int bs_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t* seg_off,
             int64_t n, const bs_window_params* p, bs_batch* batches_out, int32_t batches_cap,
             int32_t* req_batch_out, int32_t* req_row_out, bs_summary* summary, void* stream);

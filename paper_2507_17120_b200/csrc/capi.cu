@@ -76,7 +76,7 @@ cudaError_t alloc(bs_ctx* ctx, T** p, size_t count) {
 }
 
 void free_all(bs_ctx* c) {
-  void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->slot_seg, c->bins_cnt,
+  void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->slot_seg, c->slot_len, c->bins_cnt,
                   c->tile_tot, c->tile_slen, c->tile_carry, c->bmw, c->wp, c->kinfo,
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
                   c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
@@ -158,6 +158,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(seg_off, L * C + 1);
   A(slot_lut, C * L);
   A(slot_seg, C * L + 1);
+  A(slot_len, C * L + 1);
   A(bins_cnt, 4 * 256);
   const int64_t ntiles = (L + bsk::kTileX - 1) / bsk::kTileX;
   A(tile_tot, ntiles * (C + 1));

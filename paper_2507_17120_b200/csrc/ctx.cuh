@@ -38,6 +38,7 @@ struct bs_ctx {
   int32_t* seg_off = nullptr;    // [l_cap*c_max+1] segment offsets of the last bs_boundaries
   uint32_t* slot_lut = nullptr;  // [c_max*l_cap] radix slot per (class, length)
   int32_t* slot_seg = nullptr;   // [c_max*l_cap] segment of each radix slot
+  int32_t* slot_len = nullptr;  // [C*L+1] radix slot -> length (SJF / LJF slots; -1 for FCFS)
   const uint32_t* sorted_keys = nullptr;  // drain-order slots of the last bs_order (K4)
   uint32_t* bins_cnt = nullptr;  // [4][256] per-pass radix digit counts (K2c -> K4)
   uint32_t* tile_tot = nullptr;  // [ntiles][C+1] K2a tile totals (per class, then total)

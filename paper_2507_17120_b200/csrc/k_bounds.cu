@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(256)
              int sort_passes, const int32_t* __restrict__ gE, const uint32_t* __restrict__ gbm,
              const uint32_t* __restrict__ gwp, const int32_t* __restrict__ seg_base,
              int32_t* __restrict__ lut, uint32_t* __restrict__ slot_lut,
-             uint32_t* __restrict__ bins_cnt, int32_t* __restrict__ slot_seg) {
+             uint32_t* __restrict__ bins_cnt, int32_t* __restrict__ slot_seg,
+             int32_t* __restrict__ slot_len) {
   __shared__ uint32_t sbins[4 * 256];
   const int32_t L = p.l_max, C = p.n_classes;
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) sbins[i] = 0;
@@ -382,6 +383,9 @@ __global__ void __launch_bounds__(256)
     else if (pol == BS_POLICY_LJF) slot += (uint32_t)(gE[b + 1] - 1 - x);
     slot_lut[idx] = slot;
     slot_seg[slot] = b * C + c;
+    // length of a slot (K5a reads it instead of gathering len[perm[j]]); an FCFS slot
+    // holds every length of its segment: -1 (all writers agree)
+    slot_len[slot] = (pol == BS_POLICY_SJF || pol == BS_POLICY_LJF) ? x : -1;
     const uint32_t h = hist_local[idx];
     if (h)  // consecutive lengths hit distinct low digits: plain shared atomics
       for (int q = 0; q < sort_passes; ++q)
@@ -742,7 +746,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
         1, std::min<int64_t>((cells + 255) / 256, 4LL * ctx->num_sms));
     k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
                                  ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
-                                 ctx->slot_seg);
+                                 ctx->slot_seg, ctx->slot_len);
     ctx->launches += 2;
     return cudaGetLastError();
   }
@@ -771,7 +775,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
       1, std::min<int64_t>((cells + 1023) / 1024, 4LL * ctx->num_sms));
   k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
                                ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
-                               ctx->slot_seg);
+                               ctx->slot_seg, ctx->slot_len);
   ctx->launches += 3;
   return cudaGetLastError();
 }

@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(256)
     k_size_prep(const int32_t* __restrict__ len, const int32_t* __restrict__ perm, SizeArgs a,
                 int32_t* __restrict__ slen, uint32_t* __restrict__ bmask,
                 int32_t* __restrict__ bmax, int32_t* __restrict__ bmin,
-                int32_t* __restrict__ bcnt, int32_t* __restrict__ bsum) {
+                int32_t* __restrict__ bcnt, int32_t* __restrict__ bsum,
+                const uint32_t* __restrict__ skeys, const int32_t* __restrict__ slot_len) {
   const int lane = threadIdx.x & 31;
   const int64_t groups = (a.n + 31) >> 5;
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -143,7 +144,10 @@ __global__ void __launch_bounds__(256)
     const bool valid = j < a.n;
     int32_t x = 0;
     if (valid) {
-      x = eff_len(len[perm[j]], a.L, a.truncate, fl);
+      // SJF / LJF positions: the length is the sorted slot's (no random gather); FCFS
+      // positions gather it through perm
+      x = skeys ? slot_len[skeys[j]] : -1;
+      if (x < 0) x = eff_len(len[perm[j]], a.L, a.truncate, fl);
       slen[j] = x;
     }
     const bool nr = valid && (int64_t)x <= a.S;
@@ -911,7 +915,8 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   const int64_t groups = (n + 31) >> 5;
   const unsigned wblocks = (unsigned)std::min<int64_t>((groups + 7) / 8, 16LL * ctx->num_sms);
   k_size_prep<<<wblocks, 256, 0, st>>>(len, perm, a, ctx->sorted_len, ctx->bmask, ctx->bmax,
-                                       ctx->bmin, ctx->bcnt, ctx->bsum);
+                                       ctx->bmin, ctx->bcnt, ctx->bsum, ctx->sorted_keys,
+                                       ctx->slot_len);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 4, st);
   k_size_next<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmask,
