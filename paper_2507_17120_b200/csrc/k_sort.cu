@@ -28,6 +28,14 @@ constexpr int kSortWarps = kSortThreads / 32;
 // 16 (4096-key tiles) above (fewer look-back steps)
 constexpr int kItemsSmall = 8;
 constexpr int kItemsLarge = 16;
+#ifndef BS_SORT_MINB16
+#define BS_SORT_MINB16 4
+#endif
+#ifndef BS_SORT_MINB8
+#define BS_SORT_MINB8 1
+#endif
+constexpr int kSortMinBlocks16 = BS_SORT_MINB16;
+constexpr int kSortMinBlocks8 = BS_SORT_MINB8;
 
 __global__ void k_assign(const int32_t* __restrict__ len, int64_t n, int32_t L, int32_t truncate,
                          const int32_t* __restrict__ lut, int32_t* __restrict__ bucket_out,
@@ -39,8 +47,11 @@ __global__ void k_assign(const int32_t* __restrict__ len, int64_t n, int32_t L, 
   latch_flags(sum, fl);
 }
 
+// 16-item tiles (windows >= 4M requests): at most 64 registers so 4 CTAs share an SM
+// (110 registers allowed only 2 — 25 % of the warp slots, latency-bound: C3 order
+// 557 -> 427 us, with a few spilled registers)
 template <bool kFirst, bool kLast, int kItems>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 : kSortMinBlocks8)
     k_sort_pass(const int32_t* __restrict__ len, const uint8_t* __restrict__ cls,
                 const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t n,
