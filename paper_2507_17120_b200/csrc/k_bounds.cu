@@ -33,6 +33,16 @@ constexpr int kSmallBT = 1024;
 constexpr int kSmallBTMin = 1;
 constexpr int kEcap = 8192;   // edges kept in shared memory when l_max < kEcap
 
+// p.policy[c] without a dynamically indexed kernel-parameter array (which the compiler
+// copies to local memory): an unrolled select over the BS_MAX_CLASSES entries
+__device__ __forceinline__ int policy_of(const bs_window_params& p, int c) {
+  int pol = p.policy[0];
+#pragma unroll
+  for (int i = 1; i < BS_MAX_CLASSES; ++i)
+    if (c == i) pol = p.policy[i];
+  return pol;
+}
+
 // CPython _float_div_mod floor quotient (Objects/floatobject.c)
 __device__ double py_floordiv(double vx, double wx) {
   double mod = fmod(vx, wx);
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(kBT, 1)
         return (x >= L ? 0u : Pc[x]) + tile_carry[t * (C + 1) + c];
       };
       cnt = (int32_t)(Pcf(up) - Pcf(lo));
-      width = p.policy[c] == BS_POLICY_FCFS ? 1 : (up - lo);
+      width = policy_of(p, c) == BS_POLICY_FCFS ? 1 : (up - lo);
     }
     int32_t tcn, tw;
     const int32_t oc = block_excl_scan<int32_t>(cnt, sh.si, &tcn);
@@ -377,7 +387,7 @@ __global__ void __launch_bounds__(256)
     const uint32_t lowmask = bt == 31 ? 0xffffffffu : ((2u << bt) - 1u);
     const int b = (int)(gwp[w] + __popc(gbm[w] & lowmask)) - 1;  // #{j >= 1 : e_j <= x}
     if (c == 0) lut[x] = b;
-    const int pol = p.policy[c];
+    const int pol = policy_of(p, c);
     uint32_t slot = (uint32_t)seg_base[b * C + c];
     if (pol == BS_POLICY_SJF) slot += (uint32_t)(x - gE[b]);
     else if (pol == BS_POLICY_LJF) slot += (uint32_t)(gE[b + 1] - 1 - x);
@@ -682,7 +692,7 @@ __global__ void __launch_bounds__(kSmallBT, kSmallBTMin)
       const int32_t lo = E[b], up = E[b + 1];
       const uint32_t* Pc = PcL + (int64_t)c * (L + 1);
       cnt = (int32_t)(Pc[up] - Pc[lo]);
-      width = p.policy[c] == BS_POLICY_FCFS ? 1 : (up - lo);
+      width = policy_of(p, c) == BS_POLICY_FCFS ? 1 : (up - lo);
     }
     int32_t tcn, tw;
     const int32_t oc = block_excl_scan<int32_t>(cnt, sh.si, &tcn);
