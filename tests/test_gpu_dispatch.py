@@ -6,6 +6,8 @@ The reference fixtures hold the plan sequence of Simulator._next_plan repeated
 requests must be identical; four-class windows (no reference rule for classes >= 2)
 are checked against the C restatement (oracle/bso.c: bso_dispatch)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -75,7 +77,7 @@ def test_gpu_dispatch_four_classes_vs_oracle():
     sched.close()
 
 
-@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("BS_RANDOM_CONFIGS", "10"))))
 def test_gpu_dispatch_random_vs_oracle(seed):
     rng = np.random.default_rng(700 + seed)
     C = int(rng.integers(1, 5))
@@ -166,3 +168,11 @@ def test_gpu_dispatch_long_context_c4():
     sched = _sched(spec, len(lens))
     _check_vs_oracle(spec, lens, cls, sched.schedule(lens, cls).to_host())
     sched.close()
+
+
+@pytest.mark.xfail(strict=False, reason="known K7 walk mismatch (open item, DESIGN.md §9): "
+                   "3-4 classes with pledged memory blocking several buckets, found by a "
+                   "2,000-configuration soak (BS_RANDOM_CONFIGS=2000)")
+@pytest.mark.parametrize("seed", [275, 1614])
+def test_gpu_dispatch_known_mismatch(seed):
+    test_gpu_dispatch_random_vs_oracle(seed)

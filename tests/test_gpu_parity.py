@@ -5,6 +5,8 @@ batch membership / rows / sizes / footprints, rejections, pending, packed
 tokens and masks); waste_ratio bit-exact as well (same float64 expression,
 tolerance in north_star is 1e-6 relative, checked separately)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -166,8 +168,9 @@ def test_c4_long_context_pack():
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("BS_RANDOM_CONFIGS", "12"))))
 def test_random_configs_vs_oracle(seed):
+    """Random configurations (BS_RANDOM_CONFIGS=N widens the sweep for a soak run)."""
     rng = np.random.default_rng(1000 + seed)
     L = int(rng.choice([16, 100, 1000, 4096, 65536]))
     n = int(rng.integers(1, 60_000))
