@@ -101,6 +101,7 @@ struct DispArgs {
   int32_t batches_cap;
   int32_t C;
   const int32_t* perm;
+  const int32_t* slen;        // lengths in drain order (K5a)
   const int32_t* cseg;        // per call: segment, min rank, length sum over its own range
   const int32_t* cmin;
   const int64_t* csum;
@@ -375,10 +376,16 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
   int64_t p[BS_MAX_CLASSES], e[BS_MAX_CLASSES];
   int q[BS_MAX_CLASSES];
   bool stuck[BS_MAX_CLASSES];
+  // thr[c]: key of a blocked bucket of class c after its null call.  form_batch removes
+  // the oversize requests it meets before the blocking one, so the bucket re-enters
+  // select_bucket with the key of its remaining requests; the class is stuck once that
+  // key is the best it has left (first call whose key sorts after it)
+  uint64_t thr[BS_MAX_CLASSES];
   for (int c = 0; c < C; ++c) {
     p[c] = s_cb[c];
     e[c] = s_cb[c + 1];
     stuck[c] = false;
+    thr[c] = kUnreach;
     int lo = 0, hi = nn;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -386,6 +393,17 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
     }
     q[c] = lo;
   }
+  unsigned fl = 0;
+  auto blocked_key = [&](uint32_t call) -> uint64_t {
+    const int32_t sg = a.cseg[call];
+    const int64_t j0 = a.node_j0[call], en = a.seg_off[sg + 1];
+    SegVal x{1, INT32_MAX, 0};
+    for (int64_t j = j0; j < en; ++j) {
+      x.mn = min(x.mn, a.perm[j]);
+      x.sm += a.slen[j];
+    }
+    return call_key(sg, x, C, fl);
+  };
   int64_t t = 0;
   int nr = 0;
   for (;;) {
@@ -393,17 +411,33 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
     for (int c = 0; c < C; ++c)
       if (!stuck[c] && p[c] < e[c]) { c0 = c; break; }
     if (c0 < 0) break;
-    // consecutive plans of c0 up to its next null call (one per _next_plan call)
-    const int64_t z = (q[c0] < nn && nulls[q[c0]] < e[c0]) ? (int64_t)nulls[q[c0]] : e[c0];
+    // consecutive plans of c0 up to its next null call (one per _next_plan call) or up
+    // to the first call that sorts after its pending blocked bucket
+    int64_t lim = e[c0];
+    if (thr[c0] != kUnreach) {
+      int64_t lo = p[c0], hi = e[c0];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (K[mid] <= thr[c0]) lo = mid + 1; else hi = mid;
+      }
+      lim = lo;
+    }
+    int64_t z = (q[c0] < nn && nulls[q[c0]] < e[c0]) ? (int64_t)nulls[q[c0]] : e[c0];
+    z = z < lim ? z : lim;
     if (z > p[c0]) {
       runs[nr++] = Run{(int32_t)p[c0], (int32_t)(z - p[c0]), (int32_t)t, 0};
       t += z - p[c0];
       p[c0] = z;
     }
     if (p[c0] == e[c0]) continue;
-    // the null call at p[c0], then the cascade inside the same _next_plan call
+    // a null call or the blocked bucket at p[c0], then the cascade inside the same
+    // _next_plan call
     for (int c = c0; c < C; ++c) {
       if (stuck[c] || p[c] >= e[c]) continue;
+      if (thr[c] != kUnreach && K[p[c]] > thr[c]) {
+        stuck[c] = true;  // select_bucket returns the blocked bucket from now on
+        continue;
+      }
       const bool is_null = q[c] < nn && nulls[q[c]] == p[c];
       if (!is_null) {
         runs[nr++] = Run{(int32_t)p[c], 1, (int32_t)t, 0};
@@ -412,19 +446,20 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
         break;
       }
       const uint32_t call = V[p[c]];
-      if (a.node_j0[call] < a.seg_off[a.cseg[call] + 1]) {
-        stuck[c] = true;  // blocked drain: select_bucket keeps returning this bucket
-      } else {
-        ++p[c];           // every remaining request was rejected: the bucket empties
-        ++q[c];
+      if (a.node_j0[call] < a.seg_off[a.cseg[call] + 1]) {  // blocked drain
+        const uint64_t k2 = blocked_key(call);
+        thr[c] = k2 < thr[c] ? k2 : thr[c];
       }
+      ++p[c];  // the call itself is spent (its oversize requests are rejected)
+      ++q[c];
     }
   }
+  if (fl) latch_flags(a.sum, fl);
   a.dmisc[kEmitted] = t;
   a.dmisc[kRuns] = nr;
   int unr = 0;
   for (int c = 0; c < C; ++c) {
-    const int64_t u = p[c] + (stuck[c] ? 1 : 0);
+    const int64_t u = p[c];  // calls from here on are never reached
     a.dmisc[kUBeg + c] = u;
     a.dmisc[kCEnd + c] = s_cb[c + 1];
     if (u < s_cb[c + 1]) unr = 1;
@@ -695,6 +730,7 @@ cudaError_t launch_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg
   a.batches_cap = batches_cap;
   a.C = p.n_classes;
   a.perm = perm;
+  a.slen = ctx->sorted_len;
   a.cseg = ctx->disp_cseg;
   a.cmin = ctx->disp_cmin;
   a.csum = ctx->disp_csum;
