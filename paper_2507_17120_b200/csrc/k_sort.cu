@@ -32,7 +32,7 @@ constexpr int kItemsLarge = 16;
 #define BS_SORT_MINB16 4
 #endif
 #ifndef BS_SORT_MINB8
-#define BS_SORT_MINB8 1
+#define BS_SORT_MINB8 4
 #endif
 constexpr int kSortMinBlocks16 = BS_SORT_MINB16;
 constexpr int kSortMinBlocks8 = BS_SORT_MINB8;
@@ -49,7 +49,8 @@ __global__ void k_assign(const int32_t* __restrict__ len, int64_t n, int32_t L, 
 
 // 16-item tiles (windows >= 4M requests): at most 64 registers so 4 CTAs share an SM
 // (110 registers allowed only 2 — 25 % of the warp slots, latency-bound: C3 order
-// 557 -> 427 us, with a few spilled registers)
+// 557 -> 427 us, with a few spilled registers); 8-item tiles likewise 64 registers
+// (an explicit min-blocks of 1 let them grow to 96 and cost C2 ~5 us per window)
 template <bool kFirst, bool kLast, int kItems>
 __global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 : kSortMinBlocks8)
     k_sort_pass(const int32_t* __restrict__ len, const uint8_t* __restrict__ cls,
