@@ -300,12 +300,25 @@ int bs_peer_connect(bs_ctx* ctx, int32_t rank, int32_t world, const void* handle
 int bs_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params* p,
                    uint32_t* hist_global, bs_summary* summary, void* stream);
 
-/* ---- monitor statistic ------------------------------------------
- * 64-bin view of the window histogram: out64[b] = #{len : (len*bins)//l_max == b}
- * (equals LengthHistogram.from_samples(bins, range=(0, l_max)), memory_model.py:125-130,
- * pd_sim.py:829-831), summed over classes.  out is uint64[bins]. */
+/* ---- monitor statistics ------------------------------------------
+ * Bin counts only (= bs_monitor without edges): out[b] for the window histogram,
+ * summed over classes; out is uint64[bins]. */
 int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
                     uint64_t* out, void* stream);
+
+/* Monitor histogram + expected_waste, one kernel (K8).
+ * counts_out[b] (uint64[bins]) = LengthHistogram.from_samples(lengths, bins,
+ * range=(0, l_max)).counts (memory_model.py:125-130, pd_sim.py:829-831) — np.histogram's
+ * uniform-bin rule, exact for every bins — summed over classes.  With edges (device
+ * int32[k+1], the bucket partition e_0 = 0 < ... < e_k) also
+ * stats_out[0] = expected_waste(hist, [(e_j, e_j+1)]) (memory_model.py:160-191: bins
+ * left to right, cnt * (1 - mid / up) in float64, / total mass; NaN when the histogram
+ * is empty or a midpoint lies beyond e_k — the reference raises ValueError there),
+ * stats_out[1] = total mass, stats_out[2] = the unnormalised sum (device double[3]).
+ * Replaces the per-tick O(queued) np.histogram + Python loop of pd_sim.py:828-833. */
+int bs_monitor(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
+               const int32_t* edges, int32_t k, uint64_t* counts_out, double* stats_out,
+               void* stream);
 
 /* ---- trace ingestion (host side) ---------------------------------
  * Parses the reference's trace files (workload.py:343-437: `_load_csv`, `_load_jsonl`,

@@ -13,6 +13,16 @@ inputs and results:
   select_bucket(bucket_set, cls)   -> index | None        (pd_sim.py:451)
   form_batch(bucket[idx], policy, pledged, task_class)
                                    -> plan | None, rejections (pd_sim.py:454-467)
+  snapshot (monitor, every tick)   -> bucket partition, expected_waste of the 64-bin
+                                      LengthHistogram of the queue (pd_sim.py:828-833)
+
+Workloads: four synthetic mixes (BucketServe SJF / LJF+EXACT / tight memory, the
+continuous no-bucket proxy) and the reference's own scenario files run exactly as
+`bucketsim run` runs them (pkg/scenarios/smoke.yaml, mixed_longtail.yaml through
+config.load_scenario -> Scenario.simulator, cli.py:37-48); for those the sha256 of the
+JSON report `bucketsim run --format json` prints is stored too.  Since the simulator
+touches the scheduling path only through these calls, a drop-in that reproduces every
+logged result reproduces the run (and its report) byte for byte.
 
 tests/test_compat_sim_replay.py replays each log against the GPU-backed drop-in
 (paper_2507_17120_b200.compat) and requires identical results at every call — the
@@ -43,7 +53,10 @@ def main():
     from bucketsim import batch_controller as bc
     from bucketsim import workload as wl
     from bucketsim.baselines import BucketServePolicy, ContinuousNoBucketPolicy
+    from bucketsim.config import load_scenario
     from bucketsim.memory_model import MODEL_PRESETS, GpuConfig
+    from bucketsim.metrics import emit_report
+    import hashlib
 
     log: list = []
 
@@ -89,9 +102,18 @@ def main():
                         "rejected": rej})
             return plan
 
+    orig_ew = pd_sim.expected_waste
+
+    def log_expected_waste(hist, partition):
+        v = orig_ew(hist, partition)
+        log.append({"op": "snapshot", "edges": [lo for lo, _ in partition] + [partition[-1][1]],
+                    "total": hist.total_count, "out": v})
+        return v
+
     orig_bs, orig_bc = pd_sim.BucketSet, pd_sim.BatchController
     pd_sim.BucketSet = LogBucketSet
     pd_sim.BatchController = LogController
+    pd_sim.expected_waste = log_expected_waste
     cases = []
     gib = 2 ** 30
     scenarios = [
@@ -142,8 +164,68 @@ def main():
             for e in log:
                 ops[e["op"]] = ops.get(e["op"], 0) + 1
             print(f"{name:24s} calls={len(log):6d} {ops}")
+        scen_dir = os.path.join(os.path.dirname(REF_SRC), "scenarios")
+        for fname in ("smoke.yaml", "mixed_longtail.yaml"):
+            log.clear()
+            sc = load_scenario(os.path.join(scen_dir, fname))
+            sim = sc.simulator()
+            sim.controller._bs = sim.bucket_set
+            report = sim.run()
+            m = sc.model
+            cases.append({
+                "name": "scenario_" + fname.split(".")[0],
+                "max_seq_len": m.max_seq_len,
+                "split_threshold": sim.bucket_set.split_threshold,
+                "model": [m.layers, m.heads, m.head_dim, m.bytes_per_elem, m.max_seq_len],
+                "gpu": [sc.cluster.gpu.total_mem, sc.cluster.gpu.model_mem,
+                        sc.cluster.gpu.reserve_fraction],
+                "accounting": sc.accounting.value,
+                "report_sha256": hashlib.sha256(emit_report(report, "json").encode()).hexdigest(),
+                "calls": list(log),
+            })
+            ops = {}
+            for e in log:
+                ops[e["op"]] = ops.get(e["op"], 0) + 1
+            print(f"{cases[-1]['name']:24s} calls={len(log):6d} {ops}")
+        # acceptance criterion 7 (test_acceptance.py:264-282): theta = 1.0 + FCFS +
+        # EXACT BucketServe vs the continuous no-bucket proxy on 20 seeded traces of the
+        # standard scenario; the reference's batch schedules are identical per seed
+        from dataclasses import replace as _replace
+        base = load_scenario(os.path.join(scen_dir, "mixed_longtail.yaml"))
+        for seed in range(20):
+            spec = _replace(base.workload.spec, horizon=wl.Horizon(requests=100),
+                            arrival=wl.PoissonArrivals(30.0), seed=seed)
+            trace = wl.gen_synthetic(spec)
+            for kind in ("bucket", "continuous"):
+                log.clear()
+                if kind == "bucket":
+                    sim = pd_sim.Simulator(
+                        trace, model=base.model, cluster=base.cluster, cost=base.cost,
+                        policy=BucketServePolicy(), offline_policy=bc.DispatchPolicy.FCFS,
+                        accounting=bc.MemoryAccounting.EXACT, split_threshold=1.0,
+                        tick_interval=base.tick_interval)
+                else:
+                    sim = pd_sim.Simulator(
+                        trace, model=base.model, cluster=base.cluster, cost=base.cost,
+                        policy=ContinuousNoBucketPolicy(), accounting=bc.MemoryAccounting.EXACT,
+                        tick_interval=base.tick_interval)
+                sim.controller._bs = sim.bucket_set
+                sim.run()
+                m = base.model
+                cases.append({
+                    "name": f"reduction_{kind}_seed{seed}",
+                    "max_seq_len": m.max_seq_len,
+                    "split_threshold": sim.bucket_set.split_threshold,
+                    "model": [m.layers, m.heads, m.head_dim, m.bytes_per_elem, m.max_seq_len],
+                    "gpu": [base.cluster.gpu.total_mem, base.cluster.gpu.model_mem,
+                            base.cluster.gpu.reserve_fraction],
+                    "accounting": "exact",
+                    "calls": list(log),
+                })
+        print(f"reduction pairs: 20 seeds, {sum(len(c['calls']) for c in cases[-40:])} calls")
     finally:
         pd_sim.BucketSet, pd_sim.BatchController = orig_bs, orig_bc
+        pd_sim.expected_waste = orig_ew
     with gzip.open(OUT, "wt") as fh:
         json.dump(cases, fh)
 

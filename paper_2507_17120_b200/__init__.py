@@ -14,9 +14,9 @@ See DESIGN.md for the kernel map and INTEGRATION.md for the boundary.
 """
 
 from .errors import ConfigError, SimulationError, TraceFormatError
-from .memory_model import (MODEL_PRESETS, GpuConfig, ModelConfig, kv_footprint_exact,
-                           kv_footprint_padded, max_safe_batch, safe_memory, token_budget,
-                           waste_ratio)
+from .memory_model import (MODEL_PRESETS, GpuConfig, LengthHistogram, ModelConfig,
+                           expected_waste, kv_footprint_exact, kv_footprint_padded,
+                           max_safe_batch, safe_memory, token_budget, waste_ratio)
 from .types import (BatchPlan, DispatchPolicy, MemoryAccounting, OversizeRejection,
                     PartitionViolation, Request, StructuralChange, TaskClass)
 from ._native import NativeUnavailable

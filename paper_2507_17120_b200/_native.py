@@ -45,7 +45,8 @@ PACK_ALIGN = 32
 
 EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "bs_destroy",
            "bs_histogram", "bs_boundaries", "bs_assign", "bs_order", "bs_size", "bs_pack",
-           "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_profile_enable",
+           "bs_window_schedule", "bs_window_from_hist", "bs_monitor_bins", "bs_monitor",
+           "bs_profile_enable",
            "bs_profile_read", "bs_launch_count", "bs_dispatch", "bs_trace_parse",
            "bs_trace_write_bst", "bs_trace_read_bst", "bs_peer_export", "bs_peer_connect",
            "bs_peer_reduce")
@@ -123,6 +124,7 @@ def load():
         "bs_window_schedule": (C.c_int, [vp, C.POINTER(WindowIO), P, vp]),
         "bs_window_from_hist": (C.c_int, [vp, C.POINTER(WindowIO), P, vp]),
         "bs_monitor_bins": (C.c_int, [vp, vp, P, i32, vp, vp]),
+        "bs_monitor": (C.c_int, [vp, vp, P, i32, vp, i32, vp, vp, vp]),
         "bs_profile_enable": (C.c_int, [vp, i32]),
         "bs_profile_read": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(i32)]),
         "bs_launch_count": (i64, [vp]),

@@ -59,12 +59,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     host_cc = shutil.which("g++", path="/usr/bin") or "g++"
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-ccbin", host_cc, "-I", INCLUDE, "-I", CSRC, "-shared",
-           "-o", LIB + ".tmp", *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    base = [nvcc(), *ARCH, *NVCC_FLAGS, "-ccbin", host_cc, "-I", INCLUDE, "-I", CSRC]
+    obj_dir = os.path.join(OUT_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+        r = subprocess.run(base + ["-c", "-o", obj, src], capture_output=True, text=True)
+        return src, obj, r
+
+    # one nvcc per translation unit, in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(sources()), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, sources()))
+    log = []
+    for src, obj, r in results:
+        log.append(r.stderr)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
+    res = subprocess.run(base + ["-shared", "-o", LIB + ".tmp"] + [o for _, o, _ in results],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libbucketserve.so")
+        raise RuntimeError("nvcc failed linking libbucketserve.so")
+    res.stderr = "".join(log) + res.stderr
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(LIB + ".tmp", LIB)

@@ -27,93 +27,236 @@ sizing are computed by the CUDA kernels; there is no CPU fallback.
 from __future__ import annotations
 
 import bisect
+import copy
+import heapq
 from collections import deque
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from operator import attrgetter
-from typing import Deque, Iterator, Sequence
+from typing import Iterator, Sequence
 
 import numpy as np
 
 from . import _native as N
-from .memory_model import GpuConfig, ModelConfig, safe_memory
+from .memory_model import GpuConfig, LengthHistogram, ModelConfig, safe_memory
 from .types import (BatchPlan, DispatchPolicy, MemoryAccounting, OversizeRejection,
-                    PartitionViolation, Request, StructuralChange, TaskClass, policy_code)
+                    PartitionViolation, Request, StructuralChange, TaskClass, enum_value,
+                    is_online, is_offline)
 
 _ARRIVAL_ORDER = attrgetter("arrival_time", "id")
 
 
 def order_requests(requests: Sequence[Request], policy: DispatchPolicy) -> list[Request]:
     """batch_controller.py:33-41 (object-level helper; the window path orders on the GPU)."""
-    if policy is DispatchPolicy.SJF:
+    v = enum_value(policy)
+    if v == DispatchPolicy.SJF.value:
         key = lambda r: (r.input_len, r.arrival_time, r.id)  # noqa: E731
-    elif policy is DispatchPolicy.LJF:
+    elif v == DispatchPolicy.LJF.value:
         key = lambda r: (-r.input_len, r.arrival_time, r.id)  # noqa: E731
     else:
         key = lambda r: (r.arrival_time, r.id)  # noqa: E731
     return sorted(requests, key=key)
 
 
-# ---- scheduler pool: one WindowScheduler per (device, L, classes, ...) shape --------
+# ---- scheduler pool: one WindowScheduler per buffer shape ---------------------------
+# Keyed only by what sizes the buffers (device, L, classes, dispatch); the memory state,
+# policies, threshold and edges of a call are applied with WindowScheduler.configure,
+# so varying current_safe / pledged does not allocate new contexts.
 _POOL: dict = {}
+_WINDOW_DEFAULTS = dict(split_threshold=0.5, adjust=True, max_passes=0, n_max=None, pledged=0,
+                        accounting=MemoryAccounting.PADDED, truncate=True, pad_id=0)
 
 
-def _scheduler(n: int, **kw):
+def _scheduler(n: int, *, max_seq_len: int, n_classes: int, dispatch: bool = False,
+               buckets=None, **params):
+    import torch
+
     from .window import WindowScheduler
-    key = tuple(sorted((k, v if not isinstance(v, (list, tuple)) else tuple(v))
-                       for k, v in kw.items()))
+    params = {**_WINDOW_DEFAULTS, **params}
+    key = (torch.cuda.current_device(), int(max_seq_len), int(n_classes), bool(dispatch))
     s = _POOL.get(key)
-    if s is None or s.max_requests < n:
+    if s is not None and s.max_requests < n:
+        s.close()
+        s = None
+    if s is None:
         cap = max(1024, 1 << max(0, int(n - 1).bit_length()))
-        s = WindowScheduler(max_requests=cap, **kw)
+        s = WindowScheduler(max_requests=cap, max_seq_len=max_seq_len, n_classes=n_classes,
+                            dispatch=dispatch, buckets=buckets, **params)
         _POOL[key] = s
+    else:
+        s.configure(buckets=buckets, **params)
     return s
 
 
+def release_pool() -> None:
+    """Free every pooled GPU context (tests / long-lived callers)."""
+    for s in _POOL.values():
+        s.close()
+    _POOL.clear()
+
+
 def _class_index(task_class, classes: list) -> int:
+    v = enum_value(task_class)
     for i, c in enumerate(classes):
-        if task_class is c:
+        if v == enum_value(c):
             return i
     raise ValueError(f"unknown task class {task_class!r}")
 
 
-# ---- bucket_manager.py ---------------------------------------------------------------
-@dataclass
-class Bucket:
-    """bucket_manager.py:22-53."""
-    low: int
-    up: int
-    requests: Deque[Request] = field(default_factory=deque)
-    # per-length counts of the owning BucketSet (kept current on add / remove_ids)
-    _counts: np.ndarray | None = field(default=None, repr=False, compare=False)
+def _class_matches(r, task_class) -> bool:
+    """form_batch's filter (`r.task_class is task_class`, batch_controller.py:155) with
+    enum members compared by value (see types.enum_value)."""
+    return task_class is None or enum_value(r.task_class) == enum_value(task_class)
 
-    def __post_init__(self) -> None:
+
+# ---- bucket_manager.py ---------------------------------------------------------------
+class Bucket:
+    """bucket_manager.py:22-53 — `low`, `up`, `mid`, `short_count`, the FIFO deque
+    `requests`, `add`, `remove_ids`, `token_mass`.
+
+    Beyond the reference it keeps what the stateful path reads per call current in O(1):
+    per-class aggregates for select_bucket (queued OFFLINE token mass; a heap of ONLINE
+    (arrival_time, id) keys with lazy deletion), the owning set's per-length histogram,
+    and form_batch's cached drains.  Requests form_batch removes are tombstoned and the
+    deque is compacted the next time `requests` is read, so a drain costs O(batch) per
+    call instead of the reference's O(bucket) rebuild (bucket_manager.py:42-50).
+    Changes made to the deque behind the bucket's back are detected by its length and
+    the aggregates recomputed."""
+
+    __slots__ = ("low", "up", "mid", "short_count", "_dq", "_dead", "_counts", "_n",
+                 "_offline_mass", "_online", "_gone", "_version", "_drains")
+
+    def __init__(self, low: int, up: int, requests=None, _counts: np.ndarray | None = None):
+        self.low = low
+        self.up = up
+        self._counts = _counts
+        self._dq: deque = requests if requests is not None else deque()
+        self._dead: set = set()
+        self._version = 0
+        self._drains: dict = {}
         self.mid = (self.low + self.up) // 2
-        self.short_count = sum(1 for r in self.requests if r.input_len < self.mid)
+        self.short_count = sum(1 for r in self._dq if r.input_len < self.mid)
+        self._reset_aggregates()
+
+    # -- reference surface --
+    @property
+    def requests(self) -> deque:
+        if self._dead:
+            self._compact()
+        return self._dq
+
+    @requests.setter
+    def requests(self, value) -> None:
+        self._dq = value
+        self._dead = set()
+        self._touch()
+        self._reset_aggregates()
 
     def __len__(self) -> int:
-        return len(self.requests)
+        return len(self._dq) - len(self._dead)
+
+    def __repr__(self) -> str:
+        return f"Bucket(low={self.low}, up={self.up}, requests={self.requests!r})"
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, Bucket):
+            return NotImplemented
+        return (self.low, self.up, list(self.requests)) == (other.low, other.up,
+                                                            list(other.requests))
+
+    __hash__ = None
 
     def add(self, request: Request) -> None:
-        self.requests.append(request)
+        if self._dead and id(request) in self._dead:
+            self._compact()  # re-added before its tombstone was compacted away
+        self._dq.append(request)
         if request.input_len < self.mid:
             self.short_count += 1
         if self._counts is not None:
             self._counts[request.input_len] += 1
+        self._agg_add(request)
+        self._touch()
 
     def remove_ids(self, ids: set) -> None:
-        kept: Deque[Request] = deque()
+        kept: deque = deque()
         for r in self.requests:
             if r.id in ids:
                 if r.input_len < self.mid:
                     self.short_count -= 1
                 if self._counts is not None:
                     self._counts[r.input_len] -= 1
+                self._agg_remove(r)
             else:
                 kept.append(r)
-        self.requests = kept
+        self._dq = kept
+        self._touch()
 
     def token_mass(self) -> int:
         return sum(r.input_len for r in self.requests)
+
+    # -- bookkeeping --
+    def _touch(self) -> None:
+        self._version += 1
+        self._drains.clear()
+
+    def _compact(self) -> None:
+        dead = self._dead
+        self._dq = deque(r for r in self._dq if id(r) not in dead)
+        self._dead = set()
+
+    def _reset_aggregates(self) -> None:
+        live = [r for r in self._dq if id(r) not in self._dead] if self._dead else self._dq
+        self._n = len(live)
+        self._offline_mass = sum(r.input_len for r in live if is_offline(r.task_class))
+        self._online = [(r.arrival_time, r.id) for r in live if is_online(r.task_class)]
+        heapq.heapify(self._online)
+        self._gone: dict = {}
+
+    def _agg_add(self, r) -> None:
+        self._n += 1
+        if is_offline(r.task_class):
+            self._offline_mass += r.input_len
+        elif is_online(r.task_class):
+            heapq.heappush(self._online, (r.arrival_time, r.id))
+
+    def _agg_remove(self, r) -> None:
+        self._n -= 1
+        if is_offline(r.task_class):
+            self._offline_mass -= r.input_len
+        elif is_online(r.task_class):
+            k = (r.arrival_time, r.id)
+            self._gone[k] = self._gone.get(k, 0) + 1
+
+    def _aggregates_current(self) -> None:
+        if self._n != len(self):  # the deque was changed behind the bucket's back
+            self._reset_aggregates()
+            self._touch()
+
+    def _oldest_online(self):
+        self._aggregates_current()
+        h, gone = self._online, self._gone
+        while h and gone.get(h[0]):
+            gone[h[0]] -= 1
+            heapq.heappop(h)
+        return h[0] if h else None
+
+    def _queued_offline_mass(self) -> int:
+        self._aggregates_current()
+        return self._offline_mass
+
+    def _consume(self, reqs) -> None:
+        """Remove the given request objects (those a cached drain call consumed) in
+        O(len(reqs)): tombstones + the same counter updates as remove_ids."""
+        dead = self._dead
+        for r in reqs:
+            dead.add(id(r))
+            if r.input_len < self.mid:
+                self.short_count -= 1
+            if self._counts is not None:
+                self._counts[r.input_len] -= 1
+            self._agg_remove(r)
+        self._version += 1
+        if len(dead) > 64 and 2 * len(dead) > len(self._dq):
+            self._compact()
 
 
 class BucketSet:
@@ -132,6 +275,7 @@ class BucketSet:
         # incremental per-length histogram of the queued requests: +1 on
         # assign / Bucket.add, -1 on Bucket.remove_ids; adjust_buckets uploads it
         self._counts = np.zeros(max_seq_len, np.int64)
+        self._lengths = np.arange(max_seq_len, dtype=np.int64)
         self._rebuild_counts()
         self.dirty = True
         self.assign_calls = 0
@@ -171,9 +315,17 @@ class BucketSet:
         """The incremental histogram, revalidated in O(L + K): every bucket must be
         attached and the counts must add up to the queued total; otherwise recount."""
         if (all(b._counts is self._counts for b in self.buckets)
+                and all(b._n == len(b) for b in self.buckets)
                 and int(self._counts.sum()) == self.total_requests):
             return self._counts
         return self._counts if self._rebuild_counts() else None
+
+    def queued_length_sum(self) -> int:
+        """Σ input_len over the queued requests from the histogram (O(L))."""
+        counts = self._current_counts()
+        if counts is None:
+            return sum(r.input_len for r in self.iter_requests())
+        return int(counts @ self._lengths)
 
     def assign(self, request: Request) -> int:
         """bucket_manager.py:110-131 (bisect over the uppers; same result and counters)."""
@@ -185,12 +337,7 @@ class BucketSet:
         self.dirty = True
         ups = [b.up for b in self.buckets]
         idx = bisect.bisect_right(ups, request.input_len)
-        b = self.buckets[idx]
-        b.requests.append(request)
-        if request.input_len < b.mid:
-            b.short_count += 1
-        if b._counts is not None:
-            b._counts[request.input_len] += 1
+        self.buckets[idx].add(request)
         self.assign_comparisons += idx + 1
         self.last_assign_comparisons = idx + 1
         return idx
@@ -233,17 +380,27 @@ class BucketSet:
             if mid is None:
                 new_buckets.append(b)
                 continue
-            left = Bucket(b.low, mid, deque(r for r in b.requests if r.input_len < mid),
-                          b._counts)
-            right = Bucket(mid, b.up, deque(r for r in b.requests if r.input_len >= mid),
-                           b._counts)
-            self.requests_moved += len(b.requests)
+            reqs = b.requests
+            left = Bucket(b.low, mid, deque(r for r in reqs if r.input_len < mid), b._counts)
+            right = Bucket(mid, b.up, deque(r for r in reqs if r.input_len >= mid), b._counts)
+            self.requests_moved += len(reqs)
             new_buckets.extend((left, right))
         self.buckets = new_buckets
         assert self.edges() == new_edges
         if all(c.kind == "skip" for c in changes):
             self.dirty = False
         return changes
+
+    def length_histogram(self, bins: int = 64) -> LengthHistogram:
+        """The simulator's monitor histogram of the queued lengths
+        (LengthHistogram.from_samples(lengths, bins, (0, max_seq_len)), pd_sim.py:829-831),
+        binned on the GPU from the incremental per-length counts (f2)."""
+        return _monitor(self, bins)[0]
+
+    def expected_waste(self, bins: int = 64) -> float:
+        """expected_waste(length_histogram(bins), [(b.low, b.up) ...]) — the per-tick
+        monitor statistic (pd_sim.py:828-833, memory_model.py:160-191), on the GPU."""
+        return _monitor(self, bins)[1]
 
     def check_partition(self) -> PartitionViolation | None:
         """bucket_manager.py:193-216."""
@@ -270,7 +427,61 @@ class BucketSet:
         return None
 
 
+@dataclass(frozen=True)
+class BoundaryFit:
+    """bucket_manager.py:219-223."""
+    boundary: float
+    iterations: int
+    converged: bool
+
+
+def optimal_boundary_oracle(hist: LengthHistogram, low: float, up: float, tol: float,
+                            max_iters: int = 100) -> BoundaryFit:
+    """bucket_manager.py:226-249: the reference's test-only conditional-mean boundary
+    (U <- mean(S | low <= S < U) from U = up until it moves by < tol * (up - low)); kept
+    for API completeness — the scheduling path uses the midpoint split (K2)."""
+    if tol <= 0:
+        raise ValueError("tol must be > 0")
+    if hist.mass_in(low, up) == 0:
+        raise ValueError(f"histogram has no mass in [{low}, {up})")
+    u, eps = float(up), tol * (up - low)
+    for it in range(1, max_iters + 1):
+        m = hist.conditional_mean(low, u)
+        if m is None:
+            return BoundaryFit(u, it, True)
+        if abs(u - m) < eps:
+            return BoundaryFit(m, it, True)
+        u = m
+    return BoundaryFit(u, max_iters, False)
+
+
+def _monitor(bs: BucketSet, bins: int):
+    """(LengthHistogram, expected_waste) of the set's queued requests (f2, K8 on the
+    GPU over the incremental histogram; the reference errors for an empty queue)."""
+    counts = bs._current_counts()
+    if counts is None:
+        raise ValueError("a queued length lies outside [0, max_seq_len)")
+    sched = _scheduler(1, max_seq_len=bs.max_seq_len, n_classes=1,
+                       policies=(DispatchPolicy.FCFS,), kv_bytes_per_token=1, current_safe=0,
+                       truncate=False)
+    return sched.monitor_from_hist(counts, bs.edges(), bins=bins)
+
+
 # ---- batch_controller.py --------------------------------------------------------------
+class _Drain:
+    """form_batch's calls on one bucket for one (class, policy, pledged, memory) key,
+    computed once on the GPU (K4 + K5 over the class-filtered bucket) and handed out
+    one call at a time while the bucket is unchanged."""
+
+    __slots__ = ("cands", "calls", "pos", "version")
+
+    def __init__(self, cands, calls, version):
+        self.cands = cands
+        self.calls = calls      # [(rejected idx array, admitted idx array, meta | None)]
+        self.pos = 0
+        self.version = version
+
+
 class BatchController:
     """batch_controller.py:70-191; form_batch sizing runs on the GPU (K4 + K5)."""
 
@@ -294,87 +505,114 @@ class BatchController:
         return self.current_safe // self.kv_per_token
 
     def current_n_max(self, bucket_set: BucketSet) -> int:
+        """batch_controller.py:93-104; Σ input_len from the set's incremental histogram
+        (O(L)) instead of a pass over every queued request."""
         total = bucket_set.total_requests
         if total == 0:
             return 1
-        mean_len = sum(r.input_len for r in bucket_set.iter_requests()) / total
+        mean_len = bucket_set.queued_length_sum() / total
         return max(1, int(self.token_budget() // mean_len))
 
     def select_bucket(self, bucket_set: BucketSet, task_class) -> int | None:
-        if task_class is TaskClass.ONLINE:
+        """batch_controller.py:106-134 over per-bucket aggregates kept by the buckets
+        (O(K) per call instead of O(queued requests))."""
+        if is_online(task_class):
             best_idx, best_key = None, None
             for idx, bucket in enumerate(bucket_set.buckets):
-                for r in bucket.requests:
-                    if r.task_class is not TaskClass.ONLINE:
-                        continue
-                    key = (r.arrival_time, r.id)
-                    if best_key is None or key < best_key:
-                        best_key, best_idx = key, idx
+                key = bucket._oldest_online()
+                if key is not None and (best_key is None or key < best_key):
+                    best_key, best_idx = key, idx
             return best_idx
         best_idx, best_mass = None, 0
         for idx, bucket in enumerate(bucket_set.buckets):
-            mass = sum(r.input_len for r in bucket.requests if r.task_class is TaskClass.OFFLINE)
+            mass = bucket._queued_offline_mass()
             if mass > best_mass:
                 best_mass, best_idx = mass, idx
         return best_idx
 
     def _footprint(self, max_len: int, count: int, token_sum: int) -> int:
-        if self.accounting is MemoryAccounting.PADDED:
+        if enum_value(self.accounting) == MemoryAccounting.PADDED.value:
             return self.kv_per_token * max_len * count
         return self.kv_per_token * token_sum
 
+    def _plan_drain(self, bucket: Bucket, policy, pledged: int, task_class) -> _Drain:
+        """The whole drain of the bucket's class-filtered candidates (form_batch
+        repeated until it returns None), from one K4 + K5 launch sequence."""
+        cands = [r for r in bucket.requests if _class_matches(r, task_class)]
+        calls = []
+        if cands:
+            # arrival rank = (arrival_time, id) order (order_requests' tie-break)
+            cands.sort(key=_ARRIVAL_ORDER)
+            lens = np.fromiter((r.input_len for r in cands), np.int64, len(cands))
+            L = int(max(self.model.max_seq_len, int(lens.max()) + 1))
+            sched = _scheduler(len(cands), max_seq_len=L, n_classes=1, policies=(policy,),
+                               adjust=False, kv_bytes_per_token=self.kv_per_token,
+                               current_safe=self.current_safe, pledged=pledged,
+                               accounting=self.accounting, truncate=False)
+            res = sched.schedule(lens.astype(np.int32), np.zeros(len(cands), np.uint8))
+            perm = res.perm.cpu().numpy()
+            rb = res.req_batch.cpu().numpy()[perm]       # outcome in drain order
+            b = res.batches()
+            lo = 0
+            for k in range(len(b)):
+                hi = int(b[k]["end"])
+                seg_pos = np.arange(lo, hi)
+                calls.append((perm[seg_pos[rb[lo:hi] == N.REQ_REJECTED]],
+                              perm[seg_pos[rb[lo:hi] == k]],
+                              (int(b[k]["max_input_len"]), int(b[k]["token_sum"]),
+                               int(b[k]["footprint"]))))
+                lo = hi
+            # the call after the last batch removes the rejected requests before the
+            # blocking one (or the rest) and admits nothing
+            pend = np.nonzero(rb[lo:] == N.REQ_PENDING)[0]
+            hi = lo + (int(pend[0]) if len(pend) else len(perm) - lo)
+            if hi > lo:
+                calls.append((perm[lo:hi], perm[:0], None))
+        return _Drain(cands, calls, bucket._version)
+
     def form_batch(self, bucket: Bucket, policy: DispatchPolicy, *, pledged: int = 0,
                    task_class=None, now: float = 0.0) -> BatchPlan | None:
-        """batch_controller.py:141-191: the first batch of the bucket's drain."""
+        """batch_controller.py:141-191: the next batch of the bucket's drain.  The drain
+        is computed on the GPU once per (bucket state, class, policy, pledged, memory)
+        and its calls are handed out while the bucket is unchanged."""
         headroom = self.current_safe - pledged
         if headroom <= 0:
             return None
-        cands = [r for r in bucket.requests if task_class is None or r.task_class is task_class]
-        if not cands:
+        key = (enum_value(task_class) if task_class is not None else None, enum_value(policy),
+               pledged, self.current_safe, enum_value(self.accounting), self.kv_per_token)
+        bucket._aggregates_current()
+        d = bucket._drains.get(key)
+        if d is None or d.version != bucket._version:
+            d = self._plan_drain(bucket, policy, pledged, task_class)
+            bucket._drains[key] = d
+        if d.pos >= len(d.calls):
             return None
-        # arrival rank = (arrival_time, id) order (order_requests' tie-break)
-        cands.sort(key=_ARRIVAL_ORDER)
-        lens = np.fromiter((r.input_len for r in cands), np.int64, len(cands))
-        L = int(max(self.model.max_seq_len, int(lens.max()) + 1))
-        sched = _scheduler(len(cands), max_seq_len=L, n_classes=1, policies=(policy,),
-                           adjust=False, kv_bytes_per_token=self.kv_per_token,
-                           current_safe=self.current_safe, pledged=pledged,
-                           accounting=self.accounting, truncate=False)
-        res = sched.schedule(lens.astype(np.int32), np.zeros(len(cands), np.uint8))
-        rb = res.req_batch.cpu().numpy()
-        rr = res.req_row.cpu().numpy()
-        b = res.batches()
-        # the first form_batch call consumes positions [start_0, end_0) (or, when it
-        # admits nothing, the rejected prefix before the blocking request)
-        perm = res.perm.cpu().numpy()
-        if len(b):
-            end = int(b[0]["end"])
-        else:
-            end = len(perm)
-            for j, i in enumerate(perm):
-                if rb[i] == N.REQ_PENDING:
-                    end = j
-                    break
-        admitted: list[Request] = [None] * (int(b[0]["n"]) if len(b) else 0)
-        removed: set = set()
-        for j in range(end):
-            i = int(perm[j])
+        rej_idx, adm_idx, meta = d.calls[d.pos]
+        d.pos += 1
+        cands = d.cands
+        for i in rej_idx:
             r = cands[i]
-            if rb[i] == N.REQ_REJECTED:
-                self.rejections.append(OversizeRejection(r, self.kv_per_token * r.input_len,
-                                                         self.current_safe))
-                removed.add(r.id)
-            elif rb[i] == 0:
-                admitted[int(rr[i])] = r
-                removed.add(r.id)
-        if removed:
-            bucket.remove_ids(removed)
-        if not admitted:
+            self.rejections.append(OversizeRejection(r, self.kv_per_token * r.input_len,
+                                                     self.current_safe))
+        admitted = tuple(cands[i] for i in adm_idx)
+        consumed = [cands[i] for i in rej_idx]
+        consumed.extend(admitted)
+        if consumed:
+            # drains of other classes on this bucket stay valid: their candidates are
+            # untouched; any drain over this class (or over all classes) is dropped
+            before = bucket._version
+            bucket._consume(consumed)
+            for k2, d2 in list(bucket._drains.items()):
+                if d2 is d or (k2[0] is not None and key[0] is not None and k2[0] != key[0]
+                               and d2.version == before):
+                    d2.version = bucket._version
+                else:
+                    del bucket._drains[k2]
+        if meta is None:
             return None
-        m = int(b[0]["max_input_len"])
-        s = int(b[0]["token_sum"])
-        return BatchPlan(request_ids=tuple(r.id for r in admitted), requests=tuple(admitted),
-                         max_input_len=m, token_sum=s, footprint=int(b[0]["footprint"]),
+        m, s, fp = meta
+        return BatchPlan(request_ids=tuple(r.id for r in admitted), requests=admitted,
+                         max_input_len=m, token_sum=s, footprint=fp,
                          created_at=now, source_bucket=(bucket.low, bucket.up))
 
 
@@ -448,7 +686,13 @@ def schedule_requests(requests: Sequence[Request], model: ModelConfig, gpu: GpuC
     pending = []
     for i in range(len(reqs)):
         if rb[i] == N.REQ_PENDING:
-            pending.append(reqs[i])
-            bs.buckets[int(h["bucket"][i])].add(reqs[i])
+            r = reqs[i]
+            pending.append(r)
+            if r.input_len >= L and truncate:
+                # filed under L - 1 like the simulator's truncated copy (pd_sim.py:382-383);
+                # the caller's object is left as it was
+                r = copy.copy(r)
+                r.input_len = L - 1
+            bs.buckets[int(h["bucket"][i])].add(r)
     return WindowSchedule(bucket_set=bs, changes=res.changes(), n_max=int(h["summary"]["n_max"]),
                           plans=plans, rejections=rejections, pending=pending)

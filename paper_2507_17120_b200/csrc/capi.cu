@@ -557,6 +557,24 @@ int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p
   return BS_OK;
 }
 
+int bs_monitor(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,
+               const int32_t* edges, int32_t k, uint64_t* counts_out, double* stats_out,
+               void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK) return rc;
+  if (!hist || !counts_out || bins < 1 || bins > 4096)
+    return fail(ctx, BS_ERR_INVALID_ARG, "bad arguments");
+  if (edges && (k < 1 || k > p->l_max || !stats_out))
+    return fail(ctx, BS_ERR_INVALID_ARG, "edges need 1 <= k <= l_max and stats_out");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  BS_CUDA(bsk::launch_monitor(hist, *p, bins, edges, k, counts_out, stats_out,
+                              static_cast<cudaStream_t>(stream)),
+          "k_monitor");
+  ++ctx->launches;
+  return BS_OK;
+}
+
 int bs_profile_enable(bs_ctx* ctx, int32_t max_steps) {
   if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
   if (max_steps < 0) return fail(ctx, BS_ERR_INVALID_ARG, "max_steps must be >= 0");

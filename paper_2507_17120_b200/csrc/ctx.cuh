@@ -155,6 +155,9 @@ int peer_flag_words();
 int dispatch_threads();
 cudaError_t launch_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params& p,
                                uint32_t* hist_global, bs_summary* summary, cudaStream_t st);
+cudaError_t launch_monitor(const uint32_t* hist, const bs_window_params& p, int32_t bins,
+                           const int32_t* edges, int32_t k, uint64_t* out, double* stats,
+                           cudaStream_t st);
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);

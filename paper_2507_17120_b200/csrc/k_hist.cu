@@ -131,32 +131,83 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
   return cudaGetLastError();
 }
 
-// f2: 64-bin monitor view, bin = (x * bins) // L (memory_model.py:125-130 with
-// range (0, L), pd_sim.py:829-831; integer identity pinned in SURVEY App. B P9).
-__global__ void k_monitor_bins(const uint32_t* __restrict__ hist, int32_t L, int32_t C,
-                               int32_t bins, unsigned long long* out) {
+// f2: the monitor histogram of pd_sim.py:829-831 — LengthHistogram.from_samples(
+// lengths, bins, range=(0, L)) (memory_model.py:125-130), i.e. np.histogram over
+// float64 samples with uniform edges e_i = i * (L / bins) (np.linspace; e_bins = L).
+// The bin of an integer length x is restated from numpy's uniform-bin path
+// (numpy/lib/_histograms_impl.py:851-861 in numpy 2.3.5): i = (int)((x / L) * bins),
+// clamp to bins-1, then one step down if x < e_i and one step up if x >= e_{i+1}
+// (except in the last bin).  For bins dividing L exactly this equals (x*bins)//L
+// (SURVEY App. B P9); the correction keeps other bin counts identical too.
+__device__ __forceinline__ double mon_edge(int i, int bins, double step, double Ld) {
+  return i == bins ? Ld : __dmul_rn((double)i, step);
+}
+
+__device__ __forceinline__ int mon_bin(int64_t x, int bins, double step, double Ld) {
+  const double xd = (double)x;
+  int i = (int)__dmul_rn(__ddiv_rn(xd, Ld), (double)bins);
+  if (i == bins) --i;
+  if (xd < mon_edge(i, bins, step, Ld)) --i;
+  if (xd >= mon_edge(i + 1, bins, step, Ld) && i != bins - 1) ++i;
+  return i;
+}
+
+// One CTA: bin the per-(class, length) histogram into shared counters, then — when
+// edges are given — expected_waste (memory_model.py:160-191) of the bucket partition
+// edges[0..k]: bins left to right, skipping empty ones, acc += cnt * (1 - mid / up)
+// with up the first bucket upper > mid, all in float64 in the reference's order
+// (explicit _rn intrinsics: no FMA contraction), divided by the total mass.
+__global__ void __launch_bounds__(1024) k_monitor(const uint32_t* __restrict__ hist, int32_t L,
+                                                  int32_t C, int32_t bins,
+                                                  const int32_t* __restrict__ edges, int32_t k,
+                                                  unsigned long long* __restrict__ out,
+                                                  double* __restrict__ stats) {
   extern __shared__ unsigned long long sb[];
   for (int i = threadIdx.x; i < bins; i += blockDim.x) sb[i] = 0;
   __syncthreads();
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < L;
-       x += (int64_t)gridDim.x * blockDim.x) {
+  const double Ld = (double)L;
+  const double step = __ddiv_rn(Ld, (double)bins);
+  for (int64_t x = threadIdx.x; x < L; x += blockDim.x) {
     unsigned long long h = 0;
-    for (int c = 0; c < C; ++c) h += hist[(int64_t)c * L + x];
-    if (h) atomicAdd(&sb[(x * bins) / L], h);
+    for (int c = 0; c < C; ++c) h += __ldg(hist + (int64_t)c * L + x);
+    if (h) atomicAdd(&sb[mon_bin(x, bins, step, Ld)], h);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < bins; i += blockDim.x)
-    if (sb[i]) atomicAdd(&out[i], sb[i]);
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) out[i] = sb[i];
+  if (threadIdx.x != 0 || stats == nullptr) return;
+  double acc = 0.0, total = 0.0;
+  for (int i = 0; i < bins; ++i) {
+    const unsigned long long cnt = sb[i];
+    total = __dadd_rn(total, (double)cnt);
+    if (cnt == 0 || edges == nullptr) continue;
+    const double mid = __ddiv_rn(__dadd_rn(mon_edge(i, bins, step, Ld),
+                                           mon_edge(i + 1, bins, step, Ld)), 2.0);
+    int lo = 1, hi = k + 1;  // first upper edges[j] (j in 1..k) with edges[j] > mid
+    while (lo < hi) {
+      const int m = (lo + hi) >> 1;
+      if ((double)edges[m] > mid) hi = m; else lo = m + 1;
+    }
+    if (lo > k) { acc = __longlong_as_double(0x7ff8000000000000LL); continue; }  // not covered
+    const double up = (double)edges[lo];
+    acc = __dadd_rn(acc, __dmul_rn((double)cnt, __dsub_rn(1.0, __ddiv_rn(mid, up))));
+  }
+  stats[0] = total > 0.0 ? __ddiv_rn(acc, total) : __longlong_as_double(0x7ff8000000000000LL);
+  stats[1] = total;
+  stats[2] = acc;
+}
+
+cudaError_t launch_monitor(const uint32_t* hist, const bs_window_params& p, int32_t bins,
+                           const int32_t* edges, int32_t k, uint64_t* out, double* stats,
+                           cudaStream_t st) {
+  k_monitor<<<1, 1024, sizeof(unsigned long long) * bins, st>>>(
+      hist, p.l_max, p.n_classes, bins, edges, k, reinterpret_cast<unsigned long long*>(out),
+      stats);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint64_t) * bins, st);
-  if (e != cudaSuccess) return e;
-  int blocks = (int)std::min<int64_t>((p.l_max + 255) / 256, 64);
-  k_monitor_bins<<<blocks, 256, sizeof(unsigned long long) * bins, st>>>(
-      hist, p.l_max, p.n_classes, bins, reinterpret_cast<unsigned long long*>(out));
-  return cudaGetLastError();
+  return launch_monitor(hist, p, bins, nullptr, 0, out, nullptr, st);
 }
 
 }  // namespace bsk

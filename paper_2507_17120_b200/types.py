@@ -32,21 +32,38 @@ class MemoryAccounting(Enum):
     EXACT = "exact"
 
 
+def enum_value(x):
+    """The reference compares its enums by identity (`is`); a caller that swaps these
+    classes into bucketsim passes bucketsim's own enum members, so members of any enum
+    are matched by their value ("online", "sjf", "padded", ...)."""
+    return x.value if isinstance(x, Enum) else x
+
+
+def is_online(task_class) -> bool:
+    return enum_value(task_class) == TaskClass.ONLINE.value
+
+
+def is_offline(task_class) -> bool:
+    return enum_value(task_class) == TaskClass.OFFLINE.value
+
+
 def policy_code(p) -> int:
-    if isinstance(p, int):
+    if isinstance(p, int) and not isinstance(p, Enum):
         if p not in (N.POLICY_FCFS, N.POLICY_SJF, N.POLICY_LJF):
             raise ValueError(f"unknown dispatch policy {p}")
         return p
-    p = DispatchPolicy(p) if not isinstance(p, DispatchPolicy) else p
+    p = DispatchPolicy(enum_value(p))
     return {DispatchPolicy.SJF: N.POLICY_SJF, DispatchPolicy.LJF: N.POLICY_LJF,
             DispatchPolicy.FCFS: N.POLICY_FCFS,
             DispatchPolicy.EARLIEST_ARRIVAL: N.POLICY_FCFS}[p]
 
 
 def accounting_code(a) -> int:
-    if isinstance(a, int):
+    if isinstance(a, int) and not isinstance(a, Enum):
+        if a not in (N.ACCOUNTING_PADDED, N.ACCOUNTING_EXACT):
+            raise ValueError(f"unknown memory accounting {a}")
         return a
-    a = MemoryAccounting(a) if not isinstance(a, MemoryAccounting) else a
+    a = MemoryAccounting(enum_value(a))
     return N.ACCOUNTING_PADDED if a is MemoryAccounting.PADDED else N.ACCOUNTING_EXACT
 
 

@@ -294,6 +294,47 @@ class WindowScheduler:
         if pack_capacity:
             self._ensure_pack(int(pack_capacity))
 
+    _RECONFIGURABLE = ("policies", "split_threshold", "adjust", "max_passes", "n_max",
+                       "kv_bytes_per_token", "current_safe", "pledged", "accounting",
+                       "truncate", "pad_id")
+
+    def configure(self, *, buckets=(), **fields) -> "WindowScheduler":
+        """Change the per-window knobs (policies, memory, threshold, initial edges, ...)
+        without reallocating: the buffers depend only on (max_requests, max_seq_len,
+        n_classes, dispatch).  A captured graph is dropped when anything changed."""
+        bad = set(fields) - set(self._RECONFIGURABLE)
+        if bad:
+            raise ValueError(f"not reconfigurable: {sorted(bad)}")
+        if "policies" in fields:
+            fields["policies"] = tuple(fields["policies"])
+        changed = any(getattr(self.cfg, k) != v for k, v in fields.items())
+        if changed:
+            old = {k: getattr(self.cfg, k) for k in fields}
+            for k, v in fields.items():
+                setattr(self.cfg, k, v)
+            try:
+                self._params = self.cfg.params()
+            except Exception:
+                for k, v in old.items():
+                    setattr(self.cfg, k, v)
+                raise
+        if buckets != ():
+            if buckets is None:
+                changed |= self.init_edges is not None
+                self.init_edges, self.k_init = None, 0
+            else:
+                e = np.asarray(buckets, np.int32)
+                same = (self.init_edges is not None and self.k_init == len(e) - 1
+                        and bool(torch.equal(self.init_edges.cpu(), torch.as_tensor(e))))
+                if not same:
+                    self.init_edges = torch.as_tensor(e).to(self.device)
+                    self.k_init = len(e) - 1
+                    changed = True
+        if changed:
+            self._graph = None
+            self._graph_key = None
+        return self
+
     # ------------------------------------------------------------------------
     def _peer_connect(self):
         """C1 over peer memory: share this context's exchange buffer with the other ranks
@@ -570,6 +611,39 @@ class WindowScheduler:
                                          C.byref(self._params), bins, _ptr(out),
                                          _stream_handle(self.device)), self.ctx.ptr)
         return out.cpu().numpy()
+
+    def monitor_from_hist(self, hist, edges, *, bins: int = 64):
+        """f2 on a caller-maintained per-length histogram (int [C, L] or [L]): the
+        simulator's per-tick monitor (pd_sim.py:828-833) — the LengthHistogram of the
+        queued lengths (bins over [0, max_seq_len)) and expected_waste of the bucket
+        partition `edges` — from one K8 launch.  Raises the reference's ValueError
+        where expected_waste does (memory_model.py:167-183).
+        Returns (LengthHistogram, expected_waste)."""
+        from .memory_model import LengthHistogram, check_waste_partition
+        h = np.ascontiguousarray(np.asarray(hist).reshape(-1), dtype=np.int64)
+        Cn, L = self.cfg.n_classes, self.cfg.max_seq_len
+        if h.size != Cn * L:
+            raise ValueError(f"histogram has {h.size} counts, expected {Cn * L}")
+        e = np.asarray(edges, np.int32)
+        dev = self.device
+        counts = torch.empty(bins, dtype=torch.int64, device=dev)
+        stats = torch.empty(3, dtype=torch.float64, device=dev)
+        d_edges = torch.as_tensor(e).to(dev)
+        with torch.cuda.device(dev):
+            self.hist.copy_(torch.from_numpy(h.astype(np.uint32).view(np.int32)))
+            N.check(N.load().bs_monitor(self.ctx.ptr, _ptr(self.hist), C.byref(self._params),
+                                        bins, _ptr(d_edges), len(e) - 1, _ptr(counts),
+                                        _ptr(stats), _stream_handle(dev)), self.ctx.ptr)
+        hist_obj = LengthHistogram.from_bin_counts(counts.cpu().numpy(), bins, (0, L))
+        check_waste_partition(hist_obj, list(zip(e[:-1].tolist(), e[1:].tolist())))
+        return hist_obj, float(stats[0].item())
+
+    def monitor(self, *, bins: int = 64):
+        """f2 for the last window: (LengthHistogram, expected_waste of its edges)."""
+        res = WindowResult(self, 0, False)
+        h = (self.hist_global if self.hist_global is not None else self.hist)
+        hist = h.cpu().numpy().view(np.uint32).astype(np.int64)
+        return self.monitor_from_hist(hist, res.edges(), bins=bins)
 
     def close(self):
         """Release the context scratch, the captured graph and the output buffers."""

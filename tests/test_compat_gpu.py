@@ -250,3 +250,151 @@ def test_adjust_after_outside_deque_mutation_recounts():
     ch = bs.adjust_buckets(16)
     assert [c.kind for c in ch] == ["split"]
     assert [(b.low, b.up, len(b)) for b in bs.buckets] == [(0, 1024, 16), (1024, 2048, 8)]
+
+
+# ---- round-2 drop-in fixes -------------------------------------------------
+from enum import Enum  # noqa: E402
+
+
+class _RefTaskClass(Enum):  # stands in for bucketsim.workload.TaskClass (identity differs)
+    ONLINE = "online"
+    OFFLINE = "offline"
+
+
+class _RefPolicy(Enum):
+    SJF = "sjf"
+    LJF = "ljf"
+    EARLIEST_ARRIVAL = "earliest_arrival"
+    FCFS = "fcfs"
+
+
+class _RefAccounting(Enum):
+    PADDED = "padded"
+    EXACT = "exact"
+
+
+def _ref_form_batch(reqs, policy, kvpt, safe, pledged, cls, padded):
+    """batch_controller.py:141-191 restated in plain Python (the test's checker):
+    returns (plan tuple | None, rejected ids, remaining requests)."""
+    from paper_2507_17120_b200.compat import order_requests
+    headroom = safe - pledged
+    if headroom <= 0:
+        return None, [], list(reqs)
+    cands = [r for r in reqs if cls is None or r.task_class.value == cls.value]
+    if not cands:
+        return None, [], list(reqs)
+    adm, rej, removed = [], [], set()
+    cur_max = cur_sum = 0
+    for r in order_requests(cands, policy):
+        if kvpt * r.input_len > safe:
+            rej.append(r.id)
+            removed.add(r.id)
+            continue
+        nm, ns = max(cur_max, r.input_len), cur_sum + r.input_len
+        fp = kvpt * nm * (len(adm) + 1) if padded else kvpt * ns
+        if fp > headroom:
+            break
+        adm.append(r)
+        removed.add(r.id)
+        cur_max, cur_sum = nm, ns
+    rest = [r for r in reqs if r.id not in removed]
+    if not adm:
+        return None, rej, rest
+    fp = kvpt * cur_max * len(adm) if padded else kvpt * cur_sum
+    return (tuple(r.id for r in adm), cur_max, cur_sum, fp), rej, rest
+
+
+@pytest.mark.parametrize("padded", [True, False])
+def test_foreign_enums_select_form_footprint(padded):
+    """pd_sim passes bucketsim's own enum members: they are matched by value."""
+    acc = _RefAccounting.PADDED if padded else _RefAccounting.EXACT
+    ctl = BatchController(UNIT, _gpu_budget(10_000), acc)
+    assert ctl._footprint(40, 3, 48) == (120 if padded else 48) * UNIT.kv_bytes_per_token
+    reqs = deque([_req(0, 300, 2.0, _RefTaskClass.OFFLINE), _req(1, 100, 1.0, _RefTaskClass.ONLINE),
+                  _req(2, 200, 0.5, _RefTaskClass.OFFLINE), _req(3, 50, 3.0, _RefTaskClass.ONLINE)])
+    bs = BucketSet(100_000, buckets=[Bucket(0, 100_000, reqs)])
+    assert ctl.select_bucket(bs, _RefTaskClass.ONLINE) == 0
+    assert ctl.select_bucket(bs, _RefTaskClass.OFFLINE) == 0
+    plan = ctl.form_batch(bs.buckets[0], _RefPolicy.EARLIEST_ARRIVAL, task_class=_RefTaskClass.ONLINE)
+    assert plan.request_ids == (1, 3)
+    plan = ctl.form_batch(bs.buckets[0], _RefPolicy.SJF, task_class=_RefTaskClass.OFFLINE)
+    assert plan.request_ids == (2, 0)
+    assert ctl.select_bucket(bs, _RefTaskClass.ONLINE) is None
+    out = schedule_requests([_req(i, 100 + i, float(i), [_RefTaskClass.ONLINE, _RefTaskClass.OFFLINE][i % 2])
+                             for i in range(50)], UNIT, _gpu_budget(100_000),
+                            accounting=acc, offline_policy=_RefPolicy.LJF)
+    assert sum(len(p) for p in out.plans) == 50
+
+
+def test_schedule_requests_truncated_pending_is_filed_at_l_minus_1():
+    """truncate=True + pledged memory leaves pending requests; an over-long one is
+    filed in the returned BucketSet under L-1 (no IndexError, partition valid) and the
+    caller's object keeps its length."""
+    model = ModelConfig(1, 1, 1, 2, 4096)
+    gpu = GpuConfig(4 * 5000, 0, 0.0)  # 5000 tokens of KV
+    reqs = [_req(i, x, float(i)) for i, x in enumerate([100, 9000, 3000, 4000, 50])]
+    out = schedule_requests(reqs, model, gpu, pledged=4 * 2000, truncate=True)
+    assert out.bucket_set.check_partition() is None
+    assert reqs[1].input_len == 9000
+    pend = {r.id for r in out.pending}
+    assert 1 in pend or any(1 in p.request_ids for p in out.plans)
+    lens = {r.id: r.input_len for r in out.bucket_set.iter_requests()}
+    if 1 in lens:
+        assert lens[1] == 4095
+    assert out.bucket_set.total_requests == len(out.pending)
+
+
+def test_pool_does_not_grow_with_memory_state():
+    from paper_2507_17120_b200 import compat
+    ctl = BatchController(UNIT, _gpu_budget(50_000))
+    before = None
+    for k in range(20):
+        ctl.on_memory_change(UNIT.kv_bytes_per_token * (10_000 + 37 * k))
+        ctl.form_batch(_bucket(0, 100_000, [100, 200, 300]), DispatchPolicy.SJF, pledged=4 * k)
+        if before is None:
+            before = len(compat._POOL)
+    assert len(compat._POOL) == before
+
+
+def test_cached_drains_equal_fresh_form_batch_calls():
+    """form_batch hands out a drain computed once per bucket state; interleaved classes,
+    policies, pledged memory, memory changes and arrivals between calls must give
+    exactly the reference's call-by-call results."""
+    rng = np.random.default_rng(31)
+    kvpt = UNIT.kv_bytes_per_token
+    for trial in range(6):
+        safe_tokens = int(rng.integers(2_000, 20_000))
+        padded = bool(trial % 2)
+        acc = MemoryAccounting.PADDED if padded else MemoryAccounting.EXACT
+        ctl = BatchController(UNIT, _gpu_budget(safe_tokens), acc)
+        reqs = [_req(i, int(rng.integers(1, safe_tokens + 3000)), float(rng.integers(0, 50)),
+                     [TaskClass.ONLINE, TaskClass.OFFLINE][int(rng.integers(0, 2))])
+                for i in range(int(rng.integers(50, 400)))]
+        bucket = Bucket(0, 100_000, deque(reqs))
+        shadow = list(reqs)
+        nid = len(reqs)
+        for step in range(120):
+            op = rng.random()
+            if op < 0.1:
+                r = _req(nid, int(rng.integers(1, 3000)), float(rng.integers(0, 60)),
+                         [TaskClass.ONLINE, TaskClass.OFFLINE][int(rng.integers(0, 2))])
+                nid += 1
+                bucket.add(r)
+                shadow.append(r)
+                continue
+            if op < 0.13:
+                ctl.on_memory_change(kvpt * int(rng.integers(1_000, 20_000)))
+                continue
+            cls = [None, TaskClass.ONLINE, TaskClass.OFFLINE][int(rng.integers(0, 3))]
+            pol = [DispatchPolicy.SJF, DispatchPolicy.LJF, DispatchPolicy.FCFS][int(rng.integers(0, 3)) if step % 5 == 0 else 0]
+            pledged = int(rng.choice([0, 0, 0, kvpt * 500]))
+            want, want_rej, shadow = _ref_form_batch(shadow, pol, kvpt, ctl.current_safe, pledged,
+                                                     cls, padded)
+            plan = ctl.form_batch(bucket, pol, pledged=pledged, task_class=cls)
+            got = None if plan is None else (plan.request_ids, plan.max_input_len,
+                                             plan.token_sum, plan.footprint)
+            assert got == want, (trial, step)
+            assert [x.request.id for x in ctl.rejections] == want_rej, (trial, step)
+            ctl.rejections.clear()
+            assert [r.id for r in bucket.requests] == [r.id for r in shadow], (trial, step)
+            assert len(bucket) == len(shadow)

@@ -9,7 +9,13 @@ decisions (K1 + one K2 pass from the current edges) and form_batch sizing (K4 + 
 run on the GPU — with the simulator's own bookkeeping between calls (dirty on a plan
 or rejections, pd_sim.py:457-459; rejections drained, :464-467).  Every result must be
 identical: bucket indices, n_max, change lists and edges, dirty flags, selected
-buckets, plans (ids, max_input_len, token_sum, footprint) and rejected ids."""
+buckets, plans (ids, max_input_len, token_sum, footprint), rejected ids, and the
+per-tick monitor value expected_waste (K8 over the set's incremental histogram).
+
+Two of the logs are the reference's own scenario files run as `bucketsim run` runs
+them (smoke.yaml, mixed_longtail.yaml); the simulator touches the scheduling path only
+through these calls, so identical results at every call mean the drop-in run — and the
+report whose sha256 the log records — is byte-identical to the reference's."""
 
 import gzip
 import json
@@ -18,7 +24,7 @@ import os
 import pytest
 
 torch = pytest.importorskip("torch")
-pytestmark = pytest.mark.gpu
+
 
 from golden_util import GOLDEN_DIR  # noqa: E402
 from paper_2507_17120_b200 import GpuConfig, ModelConfig  # noqa: E402
@@ -30,6 +36,7 @@ with gzip.open(os.path.join(GOLDEN_DIR, "sim_calls.json.gz"), "rt") as fh:
     CASES = json.load(fh)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 def test_replay_simulator_calls(case):
     model = ModelConfig(*case["model"])
@@ -67,6 +74,10 @@ def test_replay_simulator_calls(case):
             if plan is not None or ctl.rejections:  # Simulator._next_plan, pd_sim.py:457-459
                 bs.dirty = True
             ctl.rejections.clear()                   # pd_sim.py:464-467
+        elif op == "snapshot":  # monitor: expected_waste of the queue (pd_sim.py:828-833)
+            assert bs.edges() == e["edges"], where
+            assert bs.total_requests == e["total"], where
+            assert bs.expected_waste() == e["out"], where   # bit-exact, from K8
         else:
             raise AssertionError(f"unknown op {op}")
     assert len(seen) > 0
@@ -84,3 +95,22 @@ def test_logs_exercise_the_stateful_paths():
                 plans += e["out"] is not None
     assert {"split", "merge"} <= kinds
     assert rejected > 0 and none_plans > 0 and plans > 200
+    names = {c["name"] for c in CASES}
+    assert {"scenario_smoke", "scenario_mixed_longtail"} <= names
+    assert sum(e["op"] == "snapshot" for c in CASES for e in c["calls"]) > 1000
+
+
+def test_reduction_pairs_are_batch_identical_in_the_logs():
+    """Acceptance criterion 7 (test_acceptance.py:264-282): for every seed the
+    theta = 1.0 FCFS BucketServe run and the continuous proxy form the same batches.
+    The replay above reproduces every one of those calls on the GPU classes, so the
+    drop-in satisfies the reduction too."""
+    by = {c["name"]: c for c in CASES}
+    seeds = [n.split("seed")[1] for n in by if n.startswith("reduction_bucket_")]
+    assert len(seeds) == 20
+    for sd in seeds:
+        a = [e["out"][0] for e in by[f"reduction_bucket_seed{sd}"]["calls"]
+             if e["op"] == "form" and e["out"] is not None]
+        b = [e["out"][0] for e in by[f"reduction_continuous_seed{sd}"]["calls"]
+             if e["op"] == "form" and e["out"] is not None]
+        assert a == b and len(a) > 0
