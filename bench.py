@@ -160,9 +160,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_2507_17120_b200 import workloads as W
-    # bounded sample per step (the full window on the CPU would take ~1 s per step)
-    cfg, lens, cls = W.make_window(args.config, n=min(args.requests, args.cpu_sample),
-                                   seed=1234)
+    # the same window as the B200 arm (one full config-sized window per step) unless a
+    # smaller --cpu-sample is forced, which the line then reports as same_config: false
+    n_ref = args.requests if args.cpu_sample is None else min(args.requests, args.cpu_sample)
+    cfg, lens, cls = W.make_window(args.config, n=n_ref, seed=1234)
     tok_off, tokens = W.token_store(lens)
     threads = os.cpu_count() or 1
     r = cpu_port_window(cfg, lens, cls, tok_off, tokens, threads)
@@ -180,7 +181,7 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded lengths, hashed token ids)", "impl": "reference",
         "config": {"workload": f"{args.config}: {cfg.note}", "requests_per_step": len(lens),
-                   "parallelism": "host threads"},
+                   "parallelism": "host threads", "same_config": len(lens) == args.requests},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{args.config} distribution, {len(lens)}-request window per "
                                    "step incl. pack (reference composition restated in C, "
@@ -188,6 +189,43 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _spawn_ranks(args):
+    """`--gpus N` without a launcher: re-run this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1.  More ranks than visible GPUs only with
+    --share-gpus (gloo process group, ranks share GPUs round-robin, collective 'torch'
+    or 'peer'); otherwise a one-line JSON refusal."""
+    import torch
+    n_dev = torch.cuda.device_count()
+    env = dict(os.environ)
+    argv = list(sys.argv[1:])
+    if args.gpus > n_dev:
+        if not args.share_gpus:
+            print(json.dumps({"metric": METRIC, "impl": args.impl, "n_gpus": args.gpus,
+                              "unavailable": f"{args.gpus} GPUs requested, {n_dev} visible; "
+                                             "pass --share-gpus to run the ranks on the visible "
+                                             "GPUs (gloo, functional check only)"}), flush=True)
+            return
+        env["BS_DIST_BACKEND"] = "gloo"
+        if args.collective == "nccl":  # NCCL needs one GPU per rank
+            argv += ["--collective", "torch"]
+    if args.gpus > 1 and args.impl == "b200":
+        env.setdefault("NCCL_DEBUG", "INFO")           # communicator lines on stderr
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    rc = subprocess.call(cmd, env=env)
+    if rc:
+        sys.exit(rc)
 
 
 def main():
@@ -202,19 +240,29 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the window kernels "
                     "individually instead of replaying one CUDA graph per window")
-    ap.add_argument("--cpu-sample", type=int, default=131_072)
+    ap.add_argument("--cpu-sample", type=int, default=None, help="requests per window of the "
+                    "CPU arms (default: the full window for --impl reference, 131,072 for the "
+                    "cpu_baseline leg of the B200 line)")
+    ap.add_argument("--share-gpus", action="store_true", help="with --gpus N larger than the "
+                    "visible GPUs: run the N ranks on the visible ones (gloo process group, "
+                    "collective 'torch') instead of refusing")
     ap.add_argument("--dispatch", action="store_true", help="also compute the simulator's "
                     "global dispatch order (K7, SURVEY f3) inside every window")
-    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
-                    help="C1 for N > 1: torch.distributed all-reduce (NCCL over NVLink) or the "
-                         "device-side exchange over CUDA-IPC peer memory (bs_peer_*), which "
-                         "keeps the whole window inside one CUDA graph")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "torch", "peer"],
+                    help="C1 for N > 1: 'nccl' = the library's own NCCL communicator, the "
+                         "histogram all-reduce issued between K1 and K2 inside the window's CUDA "
+                         "graph (NVLink / NVSwitch); 'torch' = torch.distributed.all_reduce "
+                         "between an eager K1 and the graph of K2..K6; 'peer' = device-side "
+                         "exchange over CUDA-IPC peer memory (bs_peer_*)")
     ap.add_argument("--inflight", type=int, default=0, help="windows in flight: consecutive "
                     "windows alternate over this many schedulers (own scratch, outputs and CUDA "
                     "stream), so the latency-bound scheduling of one window overlaps the "
                     "HBM-bound pack of the previous ones; 0 = as many as HBM holds, up to 4")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _spawn_ranks(args)
+        return
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -287,6 +335,18 @@ def main():
     stage_ms, prof_steps = sched.ctx.profile_read()
     stage_ms = {k: v / max(prof_steps, 1) for k, v in stage_ms.items()}
     sched.ctx.profile_enable(0)
+    c1_ms = stage_ms.get("exchange", 0.0) if world > 1 else None
+    if world > 1 and args.collective == "torch":  # C1 outside the library: time it here
+        from paper_2507_17120_b200.sharding import allreduce_histogram
+        for _ in range(3):
+            allreduce_histogram(sched.hist_global, pg)
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record()
+        for _ in range(20):
+            allreduce_histogram(sched.hist_global, pg)
+        e_b.record()
+        torch.cuda.synchronize(dev)
+        c1_ms = e_a.elapsed_time(e_b) / 20
     # windows in flight: scheduler k (own context, outputs, stream) takes windows k, k+I, ...
     inflight = args.inflight
     if inflight <= 0:  # auto: every scheduler holds its own scratch + packed output
@@ -374,7 +434,11 @@ def main():
     peak, peak_src = _peaks()
     admitted = int(s["admitted_tokens"])
     n_adm = n - int(s["n_rejected"]) - int(s["n_pending"])
-    pack_bytes = 4 * admitted + 24 * n_adm + 5 * int(s["packed_elems"])
+    # SURVEY §8(d) algorithmic bytes: per admitted request 4*len (tokens) + 8 (offset)
+    # read; per batch n * max_input_len * (4 + 1) written (int32 token + u8 mask)
+    pack_bytes = 4 * admitted + 8 * n_adm + 5 * int(s["padded_tokens"])
+    # what K6 actually moves: rows padded to the 32-token pitch, + perm / row map / len
+    pack_bytes_pitch = 4 * admitted + 24 * n_adm + 5 * int(s["packed_elems"])
     pack_ms = stage_ms["pack"]
     pack_gbs = pack_bytes / (pack_ms / 1e3) / 1e9 if pack_ms > 0 else None
     sched_bytes = 17 * n
@@ -439,7 +503,8 @@ def main():
 
     cpu_base = None
     if not args.no_cpu_baseline and world == 1:
-        cpu_base = cpu_baseline(args.config, min(args.cpu_sample, n))
+        # the same window as the timed one (capped at 1M requests of host memory)
+        cpu_base = cpu_baseline(args.config, min(args.cpu_sample or (1 << 20), n))
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -455,9 +520,11 @@ def main():
             "l_max": cfg.l_max, "classes": cfg.n_classes,
             "kv_bytes_per_token": cfg.kvpt, "safe_memory_bytes": cfg.current_safe,
             "accounting": "padded" if cfg.accounting == 0 else "exact",
-            "parallelism": f"dp{world} (request shards, " + (
-                "histogram exchange over CUDA-IPC peer memory)" if args.collective == "peer"
-                else f"{os.environ.get('BS_DIST_BACKEND', 'nccl').upper()} histogram all-reduce)"),
+            "parallelism": f"dp{world}" if world == 1 else f"dp{world} (request shards, " + {
+                "peer": "histogram exchange over CUDA-IPC peer memory inside the window graph)",
+                "nccl": "NCCL histogram all-reduce inside the window graph)",
+                "torch": f"torch.distributed ({os.environ.get('BS_DIST_BACKEND', 'nccl')}) "
+                         "histogram all-reduce between K1 and K2)"}[args.collective],
             "pipeline": f"{inflight} windows in flight (one scheduler context + CUDA stream each); "
                         "ms_per_step = timed region / steps",
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
@@ -466,7 +533,10 @@ def main():
         "roofline": {"bound": "hbm", "kernel": _pack_kernel(cfg.l_max), "achieved": pack_gbs, "peak": peak,
                      "unit": "GB/s", "frac": (pack_gbs / peak) if pack_gbs else None,
                      "traffic": _profile_traffic(args.config, _pack_kernel(cfg.l_max)), "algorithmic_bytes": pack_bytes,
-                     "avg_launch_ms": pack_ms, "peak_source": peak_src},
+                     "avg_launch_ms": pack_ms, "peak_source": peak_src,
+                     "pitch_overhead": {"bytes_moved": pack_bytes_pitch,
+                                        "frac_incl_pitch": (pack_bytes_pitch / (pack_ms / 1e3) / 1e9 / peak)
+                                        if pack_ms > 0 else None}},
         "stages_ms": stage_ms,
         "schedule_roofline": {"bytes": sched_bytes, "ms": sched_ms,
                               "achieved_gbs": sched_bytes / (sched_ms / 1e3) / 1e9 if sched_ms else None},
@@ -479,6 +549,10 @@ def main():
         "cuda_graph": use_graph,
         "inflight": inflight,
         "window_latency_ms": window_latency_ms,
+        "c1": None if c1_ms is None else {
+            "collective": args.collective, "ms_per_window": c1_ms,
+            "bytes": 4 * cfg.l_max * cfg.n_classes,
+            "what": "all-reduce (sum) of the uint32 [classes x l_max] length histogram"},
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -241,10 +241,11 @@ int bs_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg_off, int64_
 
 /* ---- fused window ------------------------------------------------------------------
  * K1..K6 (+ K7 when p->dispatch) in one call on one stream.  Single rank: the local
- * histogram is the global one.  Sharded window: either call bs_histogram, all-reduce
- * the histogram across ranks (NCCL) and then bs_window_from_hist on every rank, or
- * connect the contexts once (bs_peer_*) and call bs_window_schedule, which then reduces
- * the ranks' histograms over peer memory into io->hist_global on the device. */
+ * histogram is the global one.  Sharded window: attach NCCL once (bs_nccl_connect /
+ * bs_set_nccl) or connect the contexts' peer memory once (bs_peer_*) and call
+ * bs_window_schedule, which runs C1 between K1 and K2 into io->hist_global; or call
+ * bs_histogram, all-reduce the histogram with any collective, then
+ * bs_window_from_hist on every rank. */
 typedef struct bs_window_io {
   /* inputs */
   const int32_t* len;         /* [n]  */
@@ -300,6 +301,26 @@ int bs_peer_connect(bs_ctx* ctx, int32_t rank, int32_t world, const void* handle
 int bs_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params* p,
                    uint32_t* hist_global, bs_summary* summary, void* stream);
 
+/* ---- C1 over NCCL (the library's own communicator, SURVEY §8b "bs_set_nccl") --------
+ * Attaching a communicator makes bs_window_schedule run C1 itself: after K1 it
+ * all-reduces (sum) io->hist into io->hist_global (required, distinct) with
+ * ncclAllReduce on the window's stream, then K2..K6 on the global histogram — every
+ * rank gets the same edges.  The whole window is then one stream
+ * sequence a CUDA graph can capture.  libnccl.so.2 is resolved at run time (the
+ * instance already loaded in the process is reused; BS_NCCL_LIB overrides).
+ *   bs_nccl_unique_id: ncclGetUniqueId into 128 opaque bytes (rank 0; the caller
+ *                      broadcasts them over any host transport);
+ *   bs_nccl_connect:   ncclCommInitRank on ctx's device; ctx owns the communicator;
+ *   bs_set_nccl:       attach a caller-owned ncclComm_t instead (NULL detaches);
+ *   bs_nccl_allreduce: C1 alone, for callers composing bs_histogram /
+ *                      bs_window_from_hist themselves. */
+#define BS_NCCL_ID_BYTES 128
+int bs_nccl_unique_id(void* id_out);
+int bs_nccl_connect(bs_ctx* ctx, int32_t rank, int32_t world, const void* unique_id);
+int bs_set_nccl(bs_ctx* ctx, void* nccl_comm, int32_t rank, int32_t world);
+int bs_nccl_allreduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params* p,
+                      uint32_t* hist_global, void* stream);
+
 /* ---- monitor statistics ------------------------------------------
  * Bin counts only (= bs_monitor without edges): out[b] for the window histogram,
  * summed over classes; out is uint64[bins]. */
@@ -354,9 +375,10 @@ int  bs_trace_read_bst(const char* path, bs_trace* out);
  * sets (0 disarms); bs_profile_read synchronises the recorded events, writes the
  * summed milliseconds per stage (BS_STAGES floats) and the number of recorded
  * steps, and resets the ring.  bs_launch_count: kernels launched by ctx so far. */
-#define BS_STAGES 10  /* 0 histogram, 1 boundaries, 2 order, 3 size.prep, 4 size.next,
-                         5 size.chain, 6 size.describe(+offsets), 7 size.outcome,
-                         8 dispatch (when p->dispatch), 9 pack */
+#define BS_STAGES 11  /* 0 histogram, 1 exchange (C1: NCCL / peer all-reduce), 2 boundaries,
+                         3 order, 4 size.prep, 5 size.next, 6 size.chain,
+                         7 size.describe(+offsets), 8 size.outcome,
+                         9 dispatch (when p->dispatch), 10 pack */
 int bs_profile_enable(bs_ctx* ctx, int32_t max_steps);
 int bs_profile_read(bs_ctx* ctx, float* stage_ms, int32_t* steps_out);
 int64_t bs_launch_count(const bs_ctx* ctx);

@@ -35,6 +35,7 @@ FLAG_BAD_EDGES = 0x80
 FLAG_DISPATCH_RANGE = 0x100
 FLAG_PEER_TIMEOUT = 0x200
 PEER_HANDLE_BYTES = 64
+NCCL_ID_BYTES = 128
 
 POLICY_FCFS, POLICY_SJF, POLICY_LJF = 0, 1, 2
 ACCOUNTING_PADDED, ACCOUNTING_EXACT = 0, 1
@@ -49,8 +50,9 @@ EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "
            "bs_profile_enable",
            "bs_profile_read", "bs_launch_count", "bs_dispatch", "bs_trace_parse",
            "bs_trace_write_bst", "bs_trace_read_bst", "bs_peer_export", "bs_peer_connect",
-           "bs_peer_reduce")
-STAGES = ("histogram", "boundaries", "order", "size.prep", "size.next", "size.chain",
+           "bs_peer_reduce", "bs_nccl_unique_id", "bs_nccl_connect", "bs_set_nccl",
+           "bs_nccl_allreduce")
+STAGES = ("histogram", "exchange", "boundaries", "order", "size.prep", "size.next", "size.chain",
           "size.describe", "size.outcome", "dispatch", "pack")
 
 
@@ -132,6 +134,10 @@ def load():
         "bs_peer_export": (C.c_int, [vp, vp]),
         "bs_peer_connect": (C.c_int, [vp, i32, i32, vp]),
         "bs_peer_reduce": (C.c_int, [vp, vp, P, vp, vp, vp]),
+        "bs_nccl_unique_id": (C.c_int, [vp]),
+        "bs_nccl_connect": (C.c_int, [vp, i32, i32, vp]),
+        "bs_set_nccl": (C.c_int, [vp, vp, i32, i32]),
+        "bs_nccl_allreduce": (C.c_int, [vp, vp, P, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -78,7 +78,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
-    res = subprocess.run(base + ["-shared", "-o", LIB + ".tmp"] + [o for _, o, _ in results],
+    res = subprocess.run(base + ["-shared", "-o", LIB + ".tmp"] + [o for _, o, _ in results] + ["-ldl"],
                          capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -241,6 +241,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
 int bs_destroy(bs_ctx* ctx) {
   if (!ctx) return BS_OK;
   cudaSetDevice(ctx->device);
+  if (ctx->nccl_owned) bsk::nccl_comm_destroy(ctx->nccl_comm);
   for (void* m : ctx->peer_mapped)
     if (m) cudaIpcCloseMemHandle(m);
   if (ctx->peer_ptrs) cudaFree(ctx->peer_ptrs);
@@ -455,14 +456,14 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                             io->init_edges, io->k_init, io->edges, io->changes, io->changes_cap,
                             io->seg_off, io->summary, st)) != BS_OK)
     return rc;
-  bsk::prof_mark(ctx, 2, st);
+  bsk::prof_mark(ctx, 3, st);
   BS_CUDA(bsk::launch_order(ctx, io->len, io->cls, io->n, *p, io->perm, io->bucket, io->summary, st),
           "k_sort_pass");
-  bsk::prof_mark(ctx, 3, st);
+  bsk::prof_mark(ctx, 4, st);
   BS_CUDA(bsk::launch_size(ctx, io->len, io->perm, io->seg_off, io->n, *p, io->batches,
                            io->batches_cap, io->req_batch, io->req_row, io->summary, st),
           "k_size");
-  bsk::prof_mark(ctx, 8, st);
+  bsk::prof_mark(ctx, 9, st);
   if (p->dispatch) {
     if (!io->emit_order || !io->batch_emit)
       return fail(ctx, BS_ERR_INVALID_ARG, "dispatch needs emit_order and batch_emit");
@@ -471,7 +472,7 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                                  io->batch_emit, io->summary, st),
             "k_dispatch");
   }
-  bsk::prof_mark(ctx, 9, st);
+  bsk::prof_mark(ctx, 10, st);
   if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
     if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
       return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
@@ -482,7 +483,7 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
                              io->out_capacity, io->summary, st),
             "k_pack");
   }
-  bsk::prof_mark(ctx, 10, st);
+  bsk::prof_mark(ctx, 11, st);
   return BS_OK;
 }
 
@@ -512,9 +513,22 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
   ++ctx->launches;
   BS_CUDA(bsk::launch_histogram(ctx, io->len, io->cls, io->n, *p, io->hist, io->summary, st),
           "k_histogram");
+  bsk::prof_mark(ctx, 1, st);
   bs_window_io local = *io;
   local.hist_global = io->hist;
-  if (ctx->peer_world > 1) {  // C1 over peer memory (bs_peer_connect): io->hist_global required
+  if (ctx->nccl_comm) {  // C1 over NCCL, on this stream (capturable)
+    if (!io->hist_global || io->hist_global == io->hist) {
+      ctx->prof_in_window = false;
+      return fail(ctx, BS_ERR_INVALID_ARG, "an NCCL-attached context needs io->hist_global");
+    }
+    std::string why;
+    if (bsk::nccl_allreduce_hist(ctx, io->hist, const_cast<uint32_t*>(io->hist_global),
+                                 (size_t)p->l_max * p->n_classes, st, &why)) {
+      ctx->prof_in_window = false;
+      return fail(ctx, BS_ERR_CUDA, why);
+    }
+    local.hist_global = io->hist_global;
+  } else if (ctx->peer_world > 1) {  // C1 over peer memory (bs_peer_connect): io->hist_global required
     if (!io->hist_global || io->hist_global == io->hist) {
       ctx->prof_in_window = false;
       return fail(ctx, BS_ERR_INVALID_ARG, "a peer-connected context needs io->hist_global");
@@ -524,7 +538,7 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
             "k_peer_reduce");
     local.hist_global = io->hist_global;
   }
-  bsk::prof_mark(ctx, 1, st);
+  bsk::prof_mark(ctx, 2, st);
   rc = window_from_hist_impl(ctx, &local, p, st);
   ctx->prof_in_window = false;
   return rc;
@@ -538,11 +552,64 @@ int bs_window_from_hist(bs_ctx* ctx, const bs_window_io* io, const bs_window_par
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ctx->prof_in_window = true;
-  bsk::prof_mark(ctx, 0, st);  // K1 ran in bs_histogram; its stage reads as ~0 here
+  bsk::prof_mark(ctx, 0, st);  // K1 and C1 ran before this call; their stages read as ~0
   bsk::prof_mark(ctx, 1, st);
+  bsk::prof_mark(ctx, 2, st);
   rc = window_from_hist_impl(ctx, io, p, st);
   ctx->prof_in_window = false;
   return rc;
+}
+
+int bs_nccl_unique_id(void* id_out) {
+  bs_ctx* ctx = nullptr;
+  if (!id_out) return fail(ctx, BS_ERR_INVALID_ARG, "NULL argument");
+  std::string why;
+  if (bsk::nccl_unique_id(id_out, &why)) return fail(ctx, BS_ERR_CUDA, why);
+  return BS_OK;
+}
+
+int bs_nccl_connect(bs_ctx* ctx, int32_t rank, int32_t world, const void* unique_id) {
+  if (!ctx || !unique_id) return fail(ctx, BS_ERR_INVALID_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ctx, BS_ERR_INVALID_ARG, "bad rank/world");
+  if (ctx->nccl_comm) return fail(ctx, BS_ERR_INVALID_ARG, "context already has a communicator");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::string why;
+  void* comm = nullptr;
+  if (bsk::nccl_comm_init(&comm, world, unique_id, rank, &why)) return fail(ctx, BS_ERR_CUDA, why);
+  ctx->nccl_comm = comm;
+  ctx->nccl_owned = true;
+  ctx->nccl_rank = rank;
+  ctx->nccl_world = world;
+  return BS_OK;
+}
+
+int bs_set_nccl(bs_ctx* ctx, void* nccl_comm, int32_t rank, int32_t world) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  if (nccl_comm && (world < 1 || rank < 0 || rank >= world))
+    return fail(ctx, BS_ERR_INVALID_ARG, "bad rank/world");
+  std::string why;
+  if (nccl_comm && bsk::nccl_status(&why)) return fail(ctx, BS_ERR_NOT_BUILT, why);
+  if (ctx->nccl_owned) bsk::nccl_comm_destroy(ctx->nccl_comm);
+  ctx->nccl_comm = nccl_comm;
+  ctx->nccl_owned = false;
+  ctx->nccl_rank = nccl_comm ? rank : -1;
+  ctx->nccl_world = nccl_comm ? world : 0;
+  return BS_OK;
+}
+
+int bs_nccl_allreduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params* p,
+                      uint32_t* hist_global, void* stream) {
+  if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
+  int rc;
+  if ((rc = check_params(ctx, p)) != BS_OK) return rc;
+  if (!hist_local || !hist_global) return fail(ctx, BS_ERR_INVALID_ARG, "NULL buffer");
+  if (!ctx->nccl_comm) return fail(ctx, BS_ERR_INVALID_ARG, "no communicator attached");
+  BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::string why;
+  if (bsk::nccl_allreduce_hist(ctx, hist_local, hist_global, (size_t)p->l_max * p->n_classes,
+                               static_cast<cudaStream_t>(stream), &why))
+    return fail(ctx, BS_ERR_CUDA, why);
+  return BS_OK;
 }
 
 int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int32_t bins,

@@ -90,6 +90,10 @@ struct bs_ctx {
   int peer_rank = -1, peer_world = 0;
   std::vector<void*> peer_mapped;    // IPC mappings of the other ranks' exchange buffers
   uint32_t** peer_ptrs = nullptr;    // device table [world] of exchange-buffer base pointers
+  // C1 over NCCL (bs_nccl_connect / bs_set_nccl)
+  void* nccl_comm = nullptr;         // ncclComm_t
+  bool nccl_owned = false;           // created by bs_nccl_connect (destroyed with the ctx)
+  int nccl_rank = -1, nccl_world = 0;
   int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
                                  //        [66] n_batches, [67] pack rows cursor, [69] long chains,
                                  //        [70] long-segment count
@@ -161,5 +165,12 @@ cudaError_t launch_monitor(const uint32_t* hist, const bs_window_params& p, int3
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);
+// nccl_c1.cu (libnccl resolved with dlopen)
+int nccl_status(std::string* why);
+int nccl_unique_id(void* id_out, std::string* why);
+int nccl_comm_init(void** comm, int world, const void* id, int rank, std::string* why);
+void nccl_comm_destroy(void* comm);
+int nccl_allreduce_hist(bs_ctx* ctx, const uint32_t* hist_local, uint32_t* hist_global,
+                        size_t count, cudaStream_t st, std::string* why);
 
 }  // namespace bsk

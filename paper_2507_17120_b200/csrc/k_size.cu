@@ -887,7 +887,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   cudaError_t e;
   const int64_t H = p.current_safe - p.pledged;
   if (n == 0 || H <= 0)
-    for (int s = 4; s <= 7; ++s) prof_mark(ctx, s, st);
+    for (int s = 5; s <= 8; ++s) prof_mark(ctx, s, st);
   if (n == 0) return cudaSuccess;
   if (H <= 0) {  // form_batch returns None before touching the queue (:150-152)
     k_fill_pending<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4LL * ctx->num_sms), 256, 0,
@@ -918,12 +918,12 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                        ctx->bmin, ctx->bcnt, ctx->bsum, ctx->sorted_keys,
                                        ctx->slot_len);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  prof_mark(ctx, 4, st);
+  prof_mark(ctx, 5, st);
   k_size_next<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmask,
                                        ctx->bmax, ctx->bcnt, ctx->bsum, ctx->J, ctx->is_start,
                                        misc, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  prof_mark(ctx, 5, st);
+  prof_mark(ctx, 6, st);
   {
     int r_cap = ctx->r_cap;
     const int32_t* ki = ctx->kinfo;
@@ -959,7 +959,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                     dim3(cblocks), dim3(wide ? 1024 : 512), args, 0, st);
     if (e != cudaSuccess) return e;
   }
-  prof_mark(ctx, 6, st);
+  prof_mark(ctx, 7, st);
   k_size_describe<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax,
                                            ctx->bmin, ctx->bcnt, ctx->bsum, ctx->J, ctx->listA,
                                            ctx->listB, ctx->node_batch, misc, batches,
@@ -970,7 +970,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary,
                                      ctx->piece_tok);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  prof_mark(ctx, 7, st);
+  prof_mark(ctx, 8, st);
   // outcome arrays beyond 32 MB (4M requests) are scattered in request-id ranges of
   // <= 32 MB (C3, 16M requests: 4 passes, 0.60 vs 0.72 ms; 3 passes of 43 MB gain
   // nothing, every extra pass re-reads the positions, ~0.1 ms at 16M)

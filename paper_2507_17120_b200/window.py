@@ -261,11 +261,16 @@ class WindowScheduler:
         self.hist = torch.zeros(Cn * L, **i32)
         self.hist_global = torch.zeros(Cn * L, **i32) if process_group is not None else None
         self.process_group = process_group
-        if collective not in ("nccl", "peer"):
-            raise ValueError("collective must be 'nccl' (torch.distributed all-reduce) or 'peer'")
-        self.collective = collective if process_group is not None else "nccl"
+        if collective not in ("nccl", "torch", "peer"):
+            raise ValueError("collective must be 'nccl' (the library's NCCL communicator, C1 "
+                             "inside the window), 'torch' (torch.distributed all-reduce between "
+                             "K1 and K2) or 'peer' (CUDA-IPC peer memory)")
+        self.collective = collective if process_group is not None else "none"
+        self._nccl = False
         if self.collective == "peer":
             self._peer_connect()
+        elif self.collective == "nccl":
+            self._nccl_connect()
         self.edges = torch.zeros(L + 1, **i32)
         self.changes_cap = int(changes_cap if changes_cap is not None else 4 * L + 64)
         self.changes = torch.zeros(4 * self.changes_cap, **i32)
@@ -350,6 +355,41 @@ class WindowScheduler:
         allh = (C.c_ubyte * (N.PEER_HANDLE_BYTES * world)).from_buffer_copy(b"".join(got))
         N.check(lib.bs_peer_connect(self.ctx.ptr, rank, world, allh), self.ctx.ptr)
 
+    def _nccl_connect(self):
+        """C1 over the library's own NCCL communicator: rank 0 makes the unique id, the
+        process group carries it to the other ranks, every rank attaches it to its
+        context (bs_nccl_connect); bs_window_schedule then all-reduces the histogram
+        between K1 and K2 on the window's stream — inside the window's CUDA graph."""
+        import torch.distributed as dist
+        rank = dist.get_rank(self.process_group)
+        world = dist.get_world_size(self.process_group)
+        uid = bytearray(N.NCCL_ID_BYTES)
+        if rank == 0:
+            uid = self.nccl_unique_id()
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(self.process_group, 0)
+                                   if self.process_group is not dist.group.WORLD else 0,
+                                   group=self.process_group)
+        self.attach_nccl(rank, world, obj[0])
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_ubyte * N.NCCL_ID_BYTES)()
+        N.check(N.load().bs_nccl_unique_id(buf), None)
+        return bytes(buf)
+
+    def attach_nccl(self, rank: int, world: int, unique_id: bytes):
+        """Attach an NCCL communicator (ncclCommInitRank over `unique_id`) to this
+        scheduler's context; every window then runs C1 itself (also with world = 1)."""
+        buf = (C.c_ubyte * N.NCCL_ID_BYTES).from_buffer_copy(bytes(unique_id))
+        with torch.cuda.device(self.device):
+            N.check(N.load().bs_nccl_connect(self.ctx.ptr, int(rank), int(world), buf), self.ctx.ptr)
+        self._nccl = True
+        self.collective = "nccl"
+        if self.hist_global is None:
+            self.hist_global = torch.zeros_like(self.hist)
+        self._graph = None
+
     def _ensure_pack(self, cap: int):
         if cap <= self.pack_capacity:
             return
@@ -414,8 +454,9 @@ class WindowScheduler:
         store (`tok_off` int64[n+1], `tokens` int32[...]) enables packing.
 
         Sharded windows: with a process group (constructor) the local histogram is
-        all-reduced over it (C1); `hist_reduce(hist)` may instead transform the
-        local histogram in place into the global one (e.g. in single-GPU tests).
+        all-reduced across the ranks (C1: collective 'nccl' inside the fused call, or
+        'peer', or 'torch' between K1 and K2); `hist_reduce(hist)` may instead transform
+        the local histogram in place into the global one (e.g. in single-GPU tests).
 
         graph=True replays the whole fused window (16-20 kernels) as one CUDA graph,
         captured on the first call for these input buffers (serving loops reuse
@@ -435,8 +476,9 @@ class WindowScheduler:
         if pack and n == 0:
             self._ensure_pack(64)  # nothing to pack; keep the result shape uniform
         two_phase = pack and self.pack_capacity == 0
-        sharded = self.process_group is not None or hist_reduce is not None
-        fused = not sharded or (self.collective == "peer" and hist_reduce is None)
+        sharded = self.process_group is not None or hist_reduce is not None or self._nccl
+        # C1 inside the fused call: the library's NCCL communicator or peer memory
+        fused = not sharded or (self.collective in ("nccl", "peer") and hist_reduce is None)
         if graph and fused and not two_phase:
             key = (lens.data_ptr(), cls.data_ptr(), n,
                    tok_off.data_ptr() if pack else 0, tokens.data_ptr() if pack else 0,
@@ -447,7 +489,7 @@ class WindowScheduler:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     io_g = self._io(lens, cls, n, tok_off, tokens, pack)
-                    if sharded:  # peer-connected context: C1 runs inside the fused call
+                    if sharded:  # NCCL / peer context: C1 runs inside the fused call
                         io_g.hist_global = _ptr(self.hist_global)
                     N.check(lib.bs_window_schedule(self.ctx.ptr, C.byref(io_g), C.byref(p),
                                                    _stream_handle(dev)), self.ctx.ptr)

@@ -48,7 +48,7 @@ def _worker(rank, world, port, out_dir):
                                kv_bytes_per_token=cfg.kvpt, current_safe=cfg.current_safe,
                                device=dev, process_group=dist.group.WORLD, collective=collective)
 
-    ref = mk("nccl").schedule(*t).to_host()
+    ref = mk("torch").schedule(*t).to_host()
     peer = mk("peer")
     outs = [peer.schedule(*t).to_host()]
     for _ in range(4):  # several epochs through both exchange slots, as one CUDA graph each
