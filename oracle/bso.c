@@ -404,6 +404,51 @@ int bso_pack(const int32_t* len, const int32_t* perm, const int32_t* req_batch,
   return (int)fl;
 }
 
+/* Checksum of the packed output without materialising it (parity at full sizes: C3's
+ * 16M-request pack is ~37 GB).  Element e (offset from the first batch's out_offset) of
+ * the packed token / mask streams contributes tok[e] * w1(e) and mask[e] * w2(e),
+ * w_k(e) = e * A_k + B_k, all mod 2^64 — position-sensitive, so a token in the wrong
+ * slot changes the sum.  Tokens come from `tokens` or, when it is NULL, are regenerated
+ * from the synthetic store's hash (token at store slot q = ((q * mul + seed) mod 2^32)
+ * mod vocab, workloads.token_store).  Covers the real tokens and the padding of every
+ * row of every batch.  out[0] = token sum, out[1] = mask sum. */
+#define CK_A1 0x9E3779B97F4A7C15ull
+#define CK_B1 0x632BE59BD9B4E019ull
+#define CK_A2 0xD6E8FEB86659FD93ull
+#define CK_B2 0xA0761D6478BD642Full
+void bso_pack_checksum(const int32_t* len, const int32_t* perm, const int32_t* req_batch,
+                       const int32_t* req_row, const int64_t* tok_off, const int32_t* tokens,
+                       uint32_t mul, uint32_t seed, uint32_t vocab, const bso_params* p,
+                       const bso_batch* batches, int64_t nb, uint64_t* out) {
+  int64_t fl = 0;
+  uint64_t st = 0, sm = 0;
+  const int64_t base = nb > 0 ? batches[0].out_offset : 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : st, sm) reduction(| : fl)
+  for (int64_t b = 0; b < nb; ++b) {
+    const bso_batch* B = &batches[b];
+    for (int64_t j = B->start; j < B->end; ++j) {
+      const int32_t r = perm[j];
+      if (req_batch[r] != (int32_t)b) continue;
+      const int64_t x = eff_len(len[r], p, &fl);
+      const uint64_t e0 = (uint64_t)(B->out_offset - base + (int64_t)req_row[r] * B->pitch);
+      for (int64_t t = 0; t < B->pitch; ++t) {
+        const uint64_t e = e0 + (uint64_t)t;
+        uint32_t tok;
+        if (t < x) {
+          const uint64_t q = (uint64_t)tok_off[r] + (uint64_t)t;
+          tok = tokens ? (uint32_t)tokens[q] : (uint32_t)(((uint32_t)q * mul + seed) % vocab);
+          sm += e * CK_A2 + CK_B2;
+        } else {
+          tok = (uint32_t)p->pad_id;
+        }
+        st += (uint64_t)tok * (e * CK_A1 + CK_B1);
+      }
+    }
+  }
+  out[0] = st;
+  out[1] = sm;
+}
+
 /* f2 monitor view: LengthHistogram.from_samples(lengths, bins, range=(0, L))
  * (memory_model.py:125-130, pd_sim.py:829-831) equals bincount((len*bins)//L). */
 void bso_monitor_bins(const uint32_t* hist, const bso_params* p, int32_t bins, uint64_t* out) {

@@ -182,6 +182,60 @@ def window(spec: WindowSpec, lens, cls, tok_off=None, tokens=None, threads: int 
                         summary=summary, out_tokens=out_tokens, out_mask=out_mask)
 
 
+def boundaries(spec: WindowSpec, hist) -> tuple[np.ndarray, np.ndarray, dict]:
+    """K2 alone on a given (global) per-(class, length) histogram: (edges, change log,
+    summary) of bso_boundaries (BucketSet.adjust_buckets to the fixpoint on the counts;
+    n_max from the histogram's moments unless spec.n_max is set)."""
+    L = lib()
+    h = np.ascontiguousarray(np.asarray(hist).reshape(-1), dtype=np.uint32)
+    p = spec.params()
+    edges = np.zeros(spec.l_max + 1, np.int32)
+    k = C.c_int32(0)
+    cap = 4 * spec.l_max + 64
+    changes = np.zeros((cap, 4), np.int32)
+    init = None if spec.init_edges is None else np.ascontiguousarray(spec.init_edges, np.int32)
+    s = Summary()
+    rc = L.bso_boundaries(_ptr(h), C.byref(p), _ptr(init), C.c_int32(0 if init is None else len(init) - 1),
+                          _ptr(edges), C.byref(k), _ptr(changes), C.c_int32(cap), C.byref(s))
+    if rc != 0:
+        raise ValueError("malformed init edges")
+    summary = {f: getattr(s, f) for f, _ in Summary._fields_ if f != "reserved"}
+    return edges[:k.value + 1].copy(), changes[:min(int(s.n_changes), cap)].copy(), summary
+
+
+CK = (0x9E3779B97F4A7C15, 0x632BE59BD9B4E019, 0xD6E8FEB86659FD93, 0xA0761D6478BD642F)
+HASH_MUL = 2654435761
+
+
+def pack_checksum(spec: WindowSpec, lens, res: WindowResult, tok_off, tokens=None,
+                  seed: int = 0, vocab: int = 32000) -> tuple[int, int]:
+    """(token sum, mask sum) of the window's packed output (bso_pack_checksum) from the
+    oracle's own plan, without materialising it; tokens=None regenerates the synthetic
+    store's ids from its hash (workloads.token_store)."""
+    L = lib()
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    p = spec.params()
+    out = np.zeros(2, np.uint64)
+    tok_off = np.ascontiguousarray(tok_off, dtype=np.int64)
+    tk = None if tokens is None else np.ascontiguousarray(tokens, dtype=np.int32)
+    b = np.ascontiguousarray(res.batches)
+    L.bso_pack_checksum(_ptr(lens), _ptr(res.perm), _ptr(res.req_batch), _ptr(res.req_row),
+                        _ptr(tok_off), _ptr(tk), C.c_uint32(HASH_MUL), C.c_uint32(seed & 0xFFFFFFFF),
+                        C.c_uint32(vocab), C.byref(p), _ptr(b), C.c_int64(len(b)), _ptr(out))
+    return int(out[0]), int(out[1])
+
+
+def checksum_arrays(out_tokens, out_mask, m: int) -> tuple[int, int]:
+    """The same checksum over materialised packed arrays (numpy, for cross-checks)."""
+    e = np.arange(m, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        w1 = e * np.uint64(CK[0]) + np.uint64(CK[1])
+        w2 = e * np.uint64(CK[2]) + np.uint64(CK[3])
+        st = np.sum(out_tokens[:m].astype(np.uint32).astype(np.uint64) * w1, dtype=np.uint64)
+        sm = np.sum(out_mask[:m].astype(np.uint64) * w2, dtype=np.uint64)
+    return int(st), int(sm)
+
+
 def n_max(total: int, sum_len: int, current_safe: int, kvpt: int) -> int:
     fl = C.c_int64(0)
     return int(lib().bso_n_max(total, sum_len, current_safe, kvpt, C.byref(fl)))

@@ -154,13 +154,98 @@ def test_c3_four_class_4m():
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True, sample_rows=2000)
 
 
-def test_c3_full_16m_schedule_bit_exact():
-    """BASELINE configs[2] at its full 16M size: edges, drain order, batches and every
-    request's outcome bit-exact vs the oracle, which also drives K5c's pointer-doubling
-    path (C3 has chains beyond the serial walk).  The pack at this size is checked on
-    sampled rows by test_c3_four_class_4m (a 16M packed copy is ~35 GB on the host)."""
+def _compare_at_scale(spec, lens, cls, seed=0):
+    """Full-size window with the packed output checked too: the GPU packs from a token
+    store generated on the device (workloads.token_store_device, the bench's store);
+    the oracle computes its plan, then the checksum of the packed stream it would write
+    (tokens regenerated from the store's hash, bso_pack_checksum); the device checksum
+    of the GPU's packed buffer must be identical (tests/pack_checksum.py).  Every
+    request's outcome, the drain order and every batch descriptor are compared bit-exact
+    as well."""
+    from pack_checksum import device_checksum
+    n = len(lens)
+    dev = torch.device("cuda", 0)
+    d_lens = torch.as_tensor(lens).to(dev)
+    d_off, d_tok = W.token_store_device(d_lens, seed=seed)
+    sched = _sched(spec, n)
+    res = sched.schedule(d_lens, torch.as_tensor(cls).to(dev), d_off, d_tok)
+    summ = res.summary()
+    m = int(summ["packed_elems"])
+    got_ck = device_checksum(sched.out_tokens, sched.out_mask, m)
+    g = dict(perm=res.perm.cpu().numpy(), req_batch=res.req_batch.cpu().numpy(),
+             req_row=res.req_row.cpu().numpy(), bucket=res.bucket.cpu().numpy(),
+             edges=res.edges(), batches=res.batches(), seg_off=res.seg_off())
+    tok_off = d_off.cpu().numpy()
+    del d_tok
+    sched.close()
+    torch.cuda.empty_cache()
+    o = _oracle(spec, lens, cls)
+    for k in ("perm", "req_batch", "req_row", "bucket", "edges", "seg_off"):
+        assert np.array_equal(g[k], getattr(o, k)), k
+    for f in o.batches.dtype.names:
+        if f == "waste":
+            assert np.array_equal(g["batches"][f].view(np.uint64), o.batches[f].view(np.uint64))
+        else:
+            assert np.array_equal(g["batches"][f], o.batches[f]), f
+    assert m == int(o.summary["packed_elems"])
+    want_ck = cpu.pack_checksum(_oracle_spec(spec), lens, o, tok_off, None, seed=seed)
+    assert got_ck == want_ck, (got_ck, want_ck)
+    return summ
+
+
+def _oracle_spec(spec):
+    return cpu.WindowSpec(l_max=spec["l_max"], n_classes=spec["n_classes"],
+                          policies=spec["policies"], theta=spec["theta"], adjust=spec["adjust"],
+                          max_passes=spec["max_passes"], kvpt=spec["kvpt"],
+                          current_safe=spec["current_safe"], pledged=spec["pledged"],
+                          accounting=spec["accounting"], truncate=spec["truncate"],
+                          init_edges=spec["init_edges"])
+
+
+def test_c3_full_16m_bit_exact_with_pack():
+    """BASELINE configs[2] at its full, benchmarked 16M size (4 classes): edges, drain
+    order, batches and every request's outcome bit-exact vs the oracle, which also
+    drives K5c's pointer-doubling path (C3 has chains beyond the serial walk), and the
+    whole ~37 GB packed output through the position-weighted checksum."""
     cfg, lens, cls = W.make_window("c3", seed=1234)
-    _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=False)
+    s = _compare_at_scale(_cfg_spec(cfg), lens, cls)
+    assert s["packed_elems"] > 7_000_000_000
+
+
+def test_c4_benchmarked_262k_bit_exact_with_pack():
+    """BASELINE configs[3] at the benchmarked 262,144 requests (128k-token tail, TMA pack
+    path): schedule bit-exact and the packed output through the checksum."""
+    cfg, lens, cls = W.make_window("c4", seed=1234)
+    assert len(lens) == 262_144
+    _compare_at_scale(_cfg_spec(cfg), lens, cls)
+
+
+def test_c2_benchmarked_window_checksum_and_seed():
+    """The bench's own C2 window (seed 1234, device token store with a nonzero hash
+    seed) through the same full-size check."""
+    cfg, lens, cls = W.make_window("c2", seed=1234)
+    _compare_at_scale(_cfg_spec(cfg), lens, cls, seed=7)
+
+
+def test_checksum_agrees_with_materialised_pack():
+    """The device checksum, the oracle's streaming checksum (tokens regenerated from the
+    hash) and a checksum of the materialised packed arrays agree on a window small
+    enough to hold on the host."""
+    from pack_checksum import device_checksum
+    cfg, lens, cls = W.make_window("c2", n=40_000, seed=9)
+    spec = _cfg_spec(cfg)
+    tok_off, tokens = W.token_store(lens, seed=5)
+    sched = _sched(spec, len(lens))
+    dev = torch.device("cuda", 0)
+    res = sched.schedule(torch.as_tensor(lens).to(dev), torch.as_tensor(cls).to(dev),
+                         torch.as_tensor(tok_off).to(dev), torch.as_tensor(tokens).to(dev))
+    m = int(res.summary()["packed_elems"])
+    a = device_checksum(sched.out_tokens, sched.out_mask, m)
+    o = _oracle(spec, lens, cls, tok_off, tokens)
+    b = cpu.checksum_arrays(o.out_tokens, o.out_mask, m)
+    c = cpu.pack_checksum(_oracle_spec(spec), lens, o, tok_off, None, seed=5)
+    assert a == b == c
+    sched.close()
 
 
 def test_c4_long_context_pack():
@@ -410,3 +495,110 @@ def test_outcome_in_request_id_ranges(parts, monkeypatch):
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
     for name in ("reject_heavy_acc0", "pledged_acc1", "zero_headroom", "four_class_exact"):
         test_gpu_matches_reference_fixture(name)
+
+
+def _adversarial_moments(rng, budget, L, count):
+    """(N, sum_len) pairs whose mean puts token_budget / mean on or next to an integer,
+    where float rounding of the mean decides CPython's floor division."""
+    out = []
+    while len(out) < count:
+        n = int(rng.choice([1, 2, 3, 7, 1000, 999_983, int(rng.integers(1, 1 << 26))]))
+        k = int(rng.integers(1, 5000))
+        s0 = budget * n // k
+        for s in (s0 - 1, s0, s0 + 1, -(-budget * n // k)):
+            if n <= s <= n * (L - 1):
+                out.append((n, s))
+    return out
+
+
+def test_device_n_max_matches_cpython_on_adversarial_histograms():
+    """current_n_max on the device (K2, batch_controller.py:93-104: CPython int // float
+    of token_budget by the float mean) on histograms built to put the quotient on an
+    integer boundary; expected values from the literal Python expression."""
+    rng = np.random.default_rng(44)
+    for L, kvpt, safe in ((4096, 524288, 160_417_028_505), (131072, 131072, 147_600_000_000),
+                          (4096, 819200, 13_529_146_982), (1000, 2, 10 ** 6 + 1)):
+        spec = dict(l_max=L, n_classes=1, policies=(0,), theta=0.5, adjust=True, max_passes=1,
+                    init_edges=None, kvpt=kvpt, current_safe=safe, pledged=0, accounting=0,
+                    truncate=True)
+        s = _sched(spec, 1)
+        budget = safe // kvpt
+        for n, sl in _adversarial_moments(rng, budget, L, 150):
+            a = sl // n                       # counts at a and a + 1 give mean sl / n
+            hi = sl - n * a
+            h = np.zeros(L, np.int64)
+            h[a] += n - hi
+            if hi:
+                h[a + 1] += hi
+            want = max(1, int(budget // (sl / n)))
+            _, _, summ = s.boundaries_from_hist(h, n_max=None, max_passes=1)
+            assert summ["n_max"] == want, (L, n, sl)
+            assert summ["total_global"] == n and summ["sum_len_global"] == sl
+        s.close()
+
+
+@pytest.fixture(scope="module")
+def c5_trace():
+    cfg, lens, cls = W.make_window("c5", seed=1234)   # the 64M-request trace bench.py shards
+    return cfg, lens, cls
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c5_64m_sharded_edges_and_drains(world, c5_trace):
+    """BASELINE configs[4]: the 64M-request trace split into `world` contiguous
+    arrival-order shards, run one after another on this GPU the way each
+    rank runs: K1 per shard, the shard histograms summed (what C1's all-reduce
+    produces), K2..K5 on every shard from the global histogram.  Every shard's edges /
+    n_max / change log equal the single-window oracle's on the whole 64M trace, and each
+    shard's drain (order, batches, outcomes) equals the oracle's drain of that shard on
+    the global edges (App. C.5).  At 4 and 8 shards the last shard is also packed and
+    checked by checksum."""
+    from paper_2507_17120_b200.sharding import shard_range
+    from pack_checksum import device_checksum
+    cfg, lens, cls = c5_trace
+    spec = _cfg_spec(cfg)
+    L, Cn = cfg.l_max, cfg.n_classes
+    hist = np.bincount(cls.astype(np.int64) * L + lens, minlength=Cn * L)
+    full_edges, full_changes, full_s = cpu.boundaries(_oracle_spec(spec), hist)
+    dev = torch.device("cuda", 0)
+    big = max(b - a for a, b in (shard_range(len(lens), r, world) for r in range(world)))
+    s = _sched(spec, big)
+    glob = torch.zeros(Cn * L, dtype=torch.int64, device=dev)
+    for r in range(world):
+        a, b = shard_range(len(lens), r, world)
+        glob += s.histogram(torch.as_tensor(lens[a:b]).to(dev),
+                            torch.as_tensor(cls[a:b]).to(dev)).reshape(-1).to(torch.int64)
+    assert np.array_equal(glob.cpu().numpy(), hist)
+    glob32 = glob.to(torch.int32)
+    shard_spec = dict(spec, adjust=False, init_edges=tuple(int(e) for e in full_edges))
+    for r in range(world):
+        a, b = shard_range(len(lens), r, world)
+        l, c = lens[a:b], cls[a:b]
+        d_l = torch.as_tensor(l).to(dev)
+        pack = r == world - 1 and world >= 4   # <= 16M requests: store + output < 80 GB
+        d_off = d_tok = None
+        if pack:
+            d_off, d_tok = W.token_store_device(d_l, seed=r)
+        res = s.schedule(d_l, torch.as_tensor(c).to(dev), d_off, d_tok,
+                         hist_reduce=lambda h: h.copy_(glob32))
+        summ = res.summary()
+        assert np.array_equal(res.edges(), full_edges), r
+        assert summ["n_max"] == full_s["n_max"] and summ["total_global"] == len(lens)
+        assert np.array_equal(res.changes_array(), full_changes)
+        o = _oracle(shard_spec, l, c)
+        assert np.array_equal(res.perm.cpu().numpy(), o.perm)
+        assert np.array_equal(res.req_batch.cpu().numpy(), o.req_batch)
+        assert np.array_equal(res.req_row.cpu().numpy(), o.req_row)
+        gb = res.batches()
+        for f in ("segment", "start", "end", "n", "max_input_len", "token_sum", "footprint",
+                  "out_offset"):
+            assert np.array_equal(gb[f], o.batches[f]), f
+        if pack:
+            m = int(summ["packed_elems"])
+            got = device_checksum(s.out_tokens, s.out_mask, m)
+            want = cpu.pack_checksum(_oracle_spec(shard_spec), l, o, d_off.cpu().numpy(), None,
+                                     seed=r)
+            assert got == want
+            del d_tok
+    s.close()
+    torch.cuda.empty_cache()

@@ -81,6 +81,21 @@ def test_n_max_matches_python_float_semantics():
         assert cpu.n_max(total, sum_len, safe, kvpt) == _py_n_max(total, sum_len, safe, kvpt)
 
 
+def test_n_max_on_integer_boundaries():
+    """Means chosen so token_budget / mean sits on or next to an integer (the cases where
+    float rounding of the mean decides the floor); the oracle vs the literal Python."""
+    rng = np.random.default_rng(4)
+    for kvpt, safe in ((524288, 160_417_028_505), (131072, 147_600_000_000), (819200, 13_529_146_982)):
+        budget = safe // kvpt
+        for _ in range(3000):
+            n = int(rng.choice([1, 3, 7, 999_983, int(rng.integers(1, 1 << 26))]))
+            k = int(rng.integers(1, 5000))
+            s0 = budget * n // k
+            for s in (s0 - 1, s0, s0 + 1, -(-budget * n // k)):
+                if s >= n:
+                    assert cpu.n_max(n, s, safe, kvpt) == _py_n_max(n, s, safe, kvpt)
+
+
 def test_baseline_config_constants():
     assert W.CONFIGS["c2"].current_safe == 160_417_028_505
     assert W.CONFIGS["c2"].kvpt == 524_288
