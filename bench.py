@@ -50,10 +50,9 @@ def _peaks():
 def _pack_kernel(l_max):
     """the K6 kernel the library launches by default (k_pack.cu: launch_pack)."""
     v = int(os.environ.get("BS_PACK_VARIANT", "0") or 0)
-    if v == 0:
+    if v not in (5, 21):
         v = 5 if l_max > 16384 else 21
-    return {5: "k_pack_tma", 6: "k_pack_ring", 18: "k_pack_stream", 20: "k_pack_stream",
-            21: "k_pack_stream", 22: "k_pack_stream"}.get(v, "k_pack")
+    return {5: "k_pack_tma", 21: "k_pack_stream"}[v]
 
 
 def _profile_traffic(cfg_name, kernel):

@@ -137,6 +137,11 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_PACK_VARIANT")) ctx->pack_variant = atoi(v);
   if (const char* v = getenv("BS_HIST_AGG")) ctx->hist_agg = atoi(v);
   if (const char* v = getenv("BS_CHAIN_WIDE")) ctx->chain_wide = atoi(v);
+  ctx->hist_maxb = 2 * ctx->num_sms;
+  if (const char* v = getenv("BS_HIST_EPT")) ctx->hist_ept = std::max(1, atoi(v));
+  if (const char* v = getenv("BS_HIST_MAXB")) ctx->hist_maxb = std::max(1, atoi(v));
+  if (const char* v = getenv("BS_SORT_ITEMS")) ctx->sort_items = atoi(v);
+  if (const char* v = getenv("BS_CHAIN_CTAS")) ctx->chain_ctas = std::max(1, atoi(v));
   int r = 1;
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;
@@ -234,6 +239,14 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
     ctx->disp_blocks = std::max(1, std::min(per_sm * ctx->num_sms, atoi(v)));
   A(disp_agg, 2 * ctx->disp_blocks);
 #undef A
+  // per-device kernel attributes (checked): every context sets them on its own device
+  if ((e = bsk::hist_prepare(ctx)) != cudaSuccess || (e = bsk::bounds_prepare(ctx)) != cudaSuccess ||
+      (e = bsk::pack_prepare(ctx)) != cudaSuccess) {
+    int rc = cuda_fail(ctx, e, "kernel attributes");
+    free_all(ctx);
+    delete ctx;
+    return rc;
+  }
   *out = ctx;
   return BS_OK;
 }

@@ -22,6 +22,13 @@ struct bs_ctx {
   int32_t piece_tok = 2048;  // K6 piece size of the last sized window (piece_tokens_for)
   int64_t pack_pieces = 0;   // upper bound on its K6 pieces: n * ceil(l_max / piece_tok)
   int chain_wide = -1;      // K5c: -1 = by window size, 0/1 = 512/1024 threads (env BS_CHAIN_WIDE)
+  // tuning hooks, read from the environment once per context by bs_create (per-device
+  // state such as shared-memory opt-ins and occupancy lives here too, not in statics)
+  int hist_ept = 4;         // K1 elements per thread (BS_HIST_EPT)
+  int hist_maxb = 0;        // K1 CTA cap (BS_HIST_MAXB; default 2 per SM)
+  int sort_items = 0;       // K4 keys per thread: 0 = by window size, 8 | 16 (BS_SORT_ITEMS)
+  int chain_ctas = 0;       // K5c CTA cap, 0 = one per SM (BS_CHAIN_CTAS)
+  int pack_tma_blocks = 0;  // K6 TMA grid: co-resident CTAs per SM x SMs
   std::string err;
   // stage profiler: ring of (BS_STAGES+1) events per recorded step
   std::vector<cudaEvent_t> prof_events;
@@ -165,6 +172,10 @@ cudaError_t launch_monitor(const uint32_t* hist, const bs_window_params& p, int3
 cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
                                 uint64_t* out, cudaStream_t st);
 cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);
+// per-context, per-device setup run by bs_create (shared-memory opt-ins, occupancy)
+cudaError_t hist_prepare(bs_ctx* ctx);
+cudaError_t bounds_prepare(bs_ctx* ctx);
+cudaError_t pack_prepare(bs_ctx* ctx);
 // nccl_c1.cu (libnccl resolved with dlopen)
 int nccl_status(std::string* why);
 int nccl_unique_id(void* id_out, std::string* why);

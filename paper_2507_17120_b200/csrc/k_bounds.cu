@@ -729,6 +729,33 @@ SortPlan sort_plan(int32_t l_max, int32_t n_classes) {
   return SortPlan{passes, per};
 }
 
+// dynamic shared memory of the K2 kernels for a window of l_max L
+static size_t bounds_small_smem(int32_t L) {
+  const int W = (L + 1 + 31) / 32;
+  const int NW = ((1 << kMaxDepth) + 31) / 32;
+  return sizeof(uint32_t) * ((size_t)(L + 1) + W + NW + (L + 1));
+}
+static size_t bounds_big_smem(int32_t L) {
+  const int ntiles = (L + kTileX - 1) / kTileX;
+  const int W = (L + 1 + 31) / 32;
+  return sizeof(uint32_t) * ((size_t)W + ntiles + (L + 1 <= kEcap ? kEcap : 0));
+}
+
+// per-context setup on the context's device (bs_create): opt the K2 kernels into the
+// shared memory the largest window of this context (l_max <= l_cap) needs
+cudaError_t bounds_prepare(bs_ctx* ctx) {
+  const int32_t Ls = std::min<int32_t>(ctx->l_cap, kSmallL);
+  size_t sm = bounds_small_smem(Ls);
+  cudaError_t e = cudaSuccess;
+  if (sm > 48 * 1024)
+    e = cudaFuncSetAttribute(k_bounds_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess || ctx->l_cap <= kSmallL) return e;
+  sm = bounds_big_smem(ctx->l_cap);
+  if (sm > 48 * 1024)
+    e = cudaFuncSetAttribute(k_boundaries, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  return e;
+}
+
 cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uint32_t* hist_global,
                               const bs_window_params& p, const int32_t* init_edges, int32_t k_init,
                               int32_t* edges_out, int32_t* changes_out, int32_t changes_cap,
@@ -736,14 +763,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
   const SortPlan sp = sort_plan(p.l_max, p.n_classes);
   const int32_t L = p.l_max, C = p.n_classes;
   if (L <= kSmallL) {
-    const int W = (L + 1 + 31) / 32;
-    const int NW = ((1 << kMaxDepth) + 31) / 32;
-    const size_t smem = sizeof(uint32_t) * ((size_t)(L + 1) + W + NW + (L + 1));
-    static size_t attr_small = 0;
-    if (smem > 48 * 1024 && smem > attr_small) {
-      cudaFuncSetAttribute(k_bounds_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr_small = smem;
-    }
+    const size_t smem = bounds_small_smem(L);
     k_bounds_small<<<1, kSmallBT, smem, st>>>(hist_local, hist_global ? hist_global : hist_local, p,
                                          sp.bits, sp.passes, init_edges, k_init, edges_out,
                                          changes_out, changes_cap, seg_off_out, ctx->PcL, ctx->E,
@@ -766,13 +786,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
                                           reinterpret_cast<unsigned long long*>(ctx->tile_slen));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int W = (L + 1 + 31) / 32;
-  const size_t smem = sizeof(uint32_t) * ((size_t)W + ntiles + (L + 1 <= kEcap ? kEcap : 0));
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(k_boundaries, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  const size_t smem = bounds_big_smem(L);
   k_boundaries<<<1, kBT, smem, st>>>(ctx->P, ctx->PcL, ctx->tile_tot,
                                      reinterpret_cast<const unsigned long long*>(ctx->tile_slen),
                                      ntiles, p, init_edges, k_init, edges_out, changes_out,

@@ -90,6 +90,16 @@ cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// per-context setup on the context's device (bs_create): 64 KB of privatised counters
+cudaError_t hist_prepare(bs_ctx* ctx) {
+  cudaError_t e = cudaFuncSetAttribute(k_histogram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       64 * 1024);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_histogram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             64 * 1024);
+  return e;
+}
+
 cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
                              const bs_window_params& p, uint32_t* hist, bs_summary* summary,
                              cudaStream_t st) {
@@ -99,23 +109,11 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
   // privatised head: <= 64 KB of shared counters per CTA (3 CTAs / SM)
   const int32_t H = (int32_t)std::min<int64_t>(L, (64 * 1024 / 4) / C);
   const size_t smem = sizeof(uint32_t) * (size_t)C * H;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_histogram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_histogram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr_set = true;
-  }
   const int threads = 512;
   // >= ept elements per thread and at most 2 CTAs per SM: the per-CTA zero/flush of the
   // privatised bins stays well below the elements each CTA reads
   const int agg = ctx->hist_agg;
-  static int ept = 0, maxb = 0;
-  if (ept == 0) {  // tuning hooks
-    const char* v = getenv("BS_HIST_EPT");
-    ept = v ? atoi(v) : 4;
-    const char* m = getenv("BS_HIST_MAXB");
-    maxb = m ? atoi(m) : 2 * ctx->num_sms;
-  }
+  const int ept = ctx->hist_ept, maxb = ctx->hist_maxb;  // tuning hooks read by bs_create
   int64_t blocks = (n + (int64_t)ept * threads - 1) / ((int64_t)ept * threads);
   blocks = std::min<int64_t>(blocks, maxb);
   blocks = std::max<int64_t>(blocks, 1);

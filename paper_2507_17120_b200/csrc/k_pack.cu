@@ -16,9 +16,8 @@
 // 3.6x slower).  The lanes fetch the 32 pieces' metadata in parallel (batch by
 // binary search, row map -> request -> token offset / length), then the warp copies
 // them with 128-bit streaming loads (ld.global.nc.L1::no_allocate, 4 in flight per
-// lane) and evict-first 128-bit stores (st.global.cs).  Default kernel:
-// k_pack_stream with the uniform-group fast path (L <= 16384), k_pack_tma above;
-// the other variants are tuning hooks (launch_pack, bottom of this file).
+// lane) and evict-first 128-bit stores (st.global.cs).  Kernels: k_pack_stream with
+// the uniform-group fast path (L <= 16384), k_pack_tma above (launch_pack, bottom).
 #include "ctx.cuh"
 
 namespace bsk {
@@ -92,89 +91,16 @@ __device__ __forceinline__ void copy_row_range(const int32_t* src, int32_t* dst,
   }
 }
 
-template <int kPackU, int kMinBlocks>
-__global__ void __launch_bounds__(kPackThreads, kMinBlocks)
-    k_pack(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
-           const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
-           const int64_t* __restrict__ tok_off, const int32_t* __restrict__ tokens, int32_t L,
-           int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
-           int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
-           int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
-           bs_summary* sum, int32_t ptok) {
-  const unsigned FULL = 0xffffffffu;
-  int64_t b_end = b_end_arg;
-  if (b_end < 0) {
-    b_end = sum_in->n_batches;
-    if (b_end > batches_cap) b_end = batches_cap;
-  }
-  if (b_begin >= b_end) return;
-  const int64_t base_off = batches[b_begin].out_offset;
-  const bs_batch last = batches[b_end - 1];
-  if (last.out_offset + (int64_t)last.n * last.pitch - base_off > out_cap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
-    return;
-  }
-  const int64_t t0 = task_base[b_begin], t1 = task_base[b_end];
-  const int lane = threadIdx.x & 31;
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned fl = 0;
-  // groups of 32 consecutive tasks, round-robin over warps: concurrently active warps
-  // work on neighbouring rows (DRAM-page and TLB locality), every task <= kPiece tokens
-  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
-    const int64_t t = gt + lane;
-    const int32_t* src = nullptr;
-    int32_t* dst = nullptr;
-    uint8_t* mdst = nullptr;
-    int32_t x = 0, vb = 0, ve = 0;
-    if (t < t1) {
-      int64_t lo = b_begin, hi = b_end;  // batch of task t: last b with task_base[b] <= t
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (task_base[mid] <= t) lo = mid; else hi = mid;
-      }
-      const bs_batch B = batches[lo];
-      const int32_t pieces = (B.pitch + ptok - 1) / ptok;
-      const int64_t local = t - task_base[lo];
-      const int64_t row = local / pieces;
-      const int32_t piece = (int32_t)(local - row * pieces);
-      const int64_t rstart = (B.out_offset - base_off) + row * (int64_t)B.pitch;
-      const int32_t r = perm[rowpos[B.row_base + row]];
-      x = eff_len(len[r], L, truncate, fl);
-      src = tokens + tok_off[r];
-      dst = out_tokens + rstart;
-      mdst = out_mask ? out_mask + rstart : nullptr;
-      vb = piece * (ptok / 4);
-      const int32_t c1 = (piece + 1) * ptok < B.pitch ? (piece + 1) * ptok : B.pitch;
-      ve = c1 >> 2;
-    }
-    const int nv = __popc(__ballot_sync(FULL, t < t1));
-    for (int i = 0; i < nv; ++i) {
-      const int32_t* s_i = reinterpret_cast<const int32_t*>(
-          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(src), i));
-      int32_t* d_i = reinterpret_cast<int32_t*>(
-          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(dst), i));
-      uint8_t* m_i = reinterpret_cast<uint8_t*>(
-          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(mdst), i));
-      const int32_t x_i = __shfl_sync(FULL, x, i);
-      const int32_t vb_i = __shfl_sync(FULL, vb, i);
-      const int32_t ve_i = __shfl_sync(FULL, ve, i);
-      copy_row_range<kPackU>(s_i, d_i, m_i, x_i, vb_i, ve_i, lane, pad_id);
-    }
-  }
-  if (fl) latch_flags(sum, fl);
-}
-
 // ---------------------------------------------------------------------------------
 // Flattened variant: the 16-byte token vectors of the warp's 32 pieces form one
 // stream (exclusive scan of the per-piece vector counts), and every iteration moves
-// 32 * kU consecutive vectors of that stream, whichever pieces they belong to.  With
-// k_pack a short row (C2's median is 245 tokens = 62 vectors) leaves most of the
+// 32 * kU consecutive vectors of that stream, whichever pieces they belong to.  Copying
+// row by row, a short row (C2's median is 245 tokens = 62 vectors) leaves most of the
 // 4 x 32 vector slots of its iteration empty and every row costs one load round trip;
 // here each round trip carries a full 32 * kU * 16 bytes.  A lane finds the piece of
 // stream position q by a 5-step binary search over the lanes' scan values (shuffles);
 // rows whose source is not 16-byte aligned take copy_row_range's scalar path after
-// the stream.  The mask is written per piece as in k_pack.  kUni adds the fast path
+// the stream.  The mask is written per piece.  kUni adds the fast path
 // for uniform groups — 32 consecutive one-piece rows of equal pitch, i.e. nearly every
 // group inside a batch: their output rows are contiguous, so a vector's row is q / V
 // (one multiply, no search), tokens and mask go out as two contiguous streams and only
@@ -550,6 +476,19 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
   if (fl) latch_flags(sum, fl);
 }
 
+// per-context setup on the context's device (bs_create): the dynamic shared-memory
+// opt-in of the TMA kernel and its co-resident CTAs per SM
+cudaError_t pack_prepare(bs_ctx* ctx) {
+  const int smem = kTmaWarps * kTmaSlots * kTmaSlotBytes;
+  cudaError_t e = cudaFuncSetAttribute(k_pack_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_tma, kTmaWarps * 32, smem);
+  if (e != cudaSuccess) return e;
+  ctx->pack_tma_blocks = std::max(1, per_sm) * ctx->num_sms;
+  return cudaSuccess;
+}
+
 static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                    const int64_t* tok_off, const int32_t* tokens,
                                    const bs_window_params& p, const bs_batch* batches,
@@ -557,14 +496,7 @@ static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_
                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                    bs_summary* summary, cudaStream_t st) {
   const size_t smem = (size_t)kTmaWarps * kTmaSlots * kTmaSlotBytes;
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(k_pack_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_tma, kTmaWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
-  k_pack_tma<<<blocks, kTmaWarps * 32, smem, st>>>(
+  k_pack_tma<<<(unsigned)ctx->pack_tma_blocks, kTmaWarps * 32, smem, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
       summary, ctx->piece_tok);
@@ -572,240 +504,19 @@ static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------------
-// Ring variant: the warp streams its 32 pieces as a flat sequence of chunks (one
-// chunk = 32 lanes x kU 16-byte vectors of one piece).  Loads are cp.async (16 B per
-// lane, L1 bypass) into a per-warp shared-memory ring of kNS chunks, so kNS-1 chunks
-// stay in flight while the oldest is written out — bytes in flight are bounded by
-// shared memory instead of registers.  Each lane reads back only the vectors it
-// fetched itself, so cp.async.wait_group is the only synchronisation.
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int kU, int kNS, int kWarps>
-__global__ void __launch_bounds__(kWarps * 32)
-    k_pack_ring(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
-                const int32_t* __restrict__ rowpos, const int64_t* __restrict__ task_base,
-                const int64_t* __restrict__ tok_off, const int32_t* __restrict__ tokens,
-                int32_t L, int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
-                int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
-                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
-                bs_summary* sum, int32_t ptok) {
-  constexpr int kChunkV = 32 * kU;  // vectors per chunk
-  extern __shared__ __align__(128) uint8_t ring_smem[];
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  int4* ring = reinterpret_cast<int4*>(ring_smem) + (size_t)wib * kNS * kChunkV;
-  int64_t b_end = b_end_arg;
-  if (b_end < 0) {
-    b_end = sum_in->n_batches;
-    if (b_end > batches_cap) b_end = batches_cap;
-  }
-  if (b_begin >= b_end) return;
-  const int64_t base_off = batches[b_begin].out_offset;
-  const bs_batch last = batches[b_end - 1];
-  if (last.out_offset + (int64_t)last.n * last.pitch - base_off > out_cap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
-    return;
-  }
-  const int64_t t0 = task_base[b_begin], t1 = task_base[b_end];
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int4 pad4 = make_int4(pad_id, pad_id, pad_id, pad_id);
-  unsigned fl = 0;
-  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
-    const int64_t t = gt + lane;
-    PieceMeta my{nullptr, nullptr, nullptr, 0, 0, 0};
-    int32_t my_chunks = 0;
-    if (t < t1) {
-      int64_t lo = b_begin, hi = b_end;
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (task_base[mid] <= t) lo = mid; else hi = mid;
-      }
-      const bs_batch B = batches[lo];
-      const int32_t pieces = (B.pitch + ptok - 1) / ptok;
-      const int64_t local = t - task_base[lo];
-      const int64_t row = local / pieces;
-      const int32_t piece = (int32_t)(local - row * pieces);
-      const int64_t rstart = (B.out_offset - base_off) + row * (int64_t)B.pitch;
-      const int32_t r = perm[rowpos[B.row_base + row]];
-      my.x = eff_len(len[r], L, truncate, fl);
-      my.src = tokens + tok_off[r];
-      my.dst = out_tokens + rstart;
-      my.mdst = out_mask ? out_mask + rstart : nullptr;
-      my.vb = piece * (ptok / 4);
-      const int32_t c1 = (piece + 1) * ptok < B.pitch ? (piece + 1) * ptok : B.pitch;
-      my.ve = c1 >> 2;
-      my_chunks = (my.ve - my.vb + kChunkV - 1) / kChunkV;
-      if (((reinterpret_cast<uintptr_t>(my.src) | reinterpret_cast<uintptr_t>(my.dst)) & 15) != 0)
-        my_chunks = -my_chunks;  // unaligned row: scalar copy, no ring traffic
-    }
-    // flat chunk sequence over the group's pieces: chunk k of piece i
-    const int32_t ch_abs = my_chunks < 0 ? -my_chunks : my_chunks;
-    const int32_t ch_incl = warp_incl_scan(ch_abs);
-    const int32_t total = __shfl_sync(FULL, ch_incl, 31);
-    const int32_t ch_excl = ch_incl - ch_abs;
-    auto get = [&](int i) {
-      PieceMeta m;
-      m.src = reinterpret_cast<const int32_t*>(
-          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.src), i));
-      m.dst = reinterpret_cast<int32_t*>(
-          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.dst), i));
-      m.mdst = reinterpret_cast<uint8_t*>(
-          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(my.mdst), i));
-      m.x = __shfl_sync(FULL, my.x, i);
-      m.vb = __shfl_sync(FULL, my.vb, i);
-      m.ve = __shfl_sync(FULL, my.ve, i);
-      return m;
-    };
-    // piece owning flat chunk c (lanes hold inclusive chunk prefixes)
-    auto owner = [&](int32_t c) { return __popc(__ballot_sync(FULL, ch_incl <= c)); };
-    auto issue = [&](int32_t c) {
-      if (c < total) {
-        const int i = owner(c);
-        const PieceMeta m = get(i);
-        const int32_t ci = c - __shfl_sync(FULL, ch_excl, i);
-        const bool al = __shfl_sync(FULL, my_chunks, i) > 0;
-        if (al) {
-          const int32_t full = m.x >> 2;
-          const int32_t hi = full < m.ve ? full : m.ve;
-          int4* slot = ring + (c % kNS) * kChunkV;
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int32_t v = m.vb + ci * kChunkV + u * 32 + lane;
-            if (v < hi) cp_async16(slot + u * 32 + lane, m.src + 4 * v);
-          }
-        }
-      }
-      cp_async_commit();  // one group per chunk slot, empty past the end
-    };
-#pragma unroll
-    for (int c = 0; c < kNS - 1; ++c) issue(c);
-    for (int32_t c = 0; c < total; ++c) {
-      issue(c + kNS - 1);
-      cp_async_wait<kNS - 1>();  // chunk c has landed (groups complete in order)
-      const int i = owner(c);
-      const PieceMeta m = get(i);
-      const int32_t ci = c - __shfl_sync(FULL, ch_excl, i);
-      const bool al = __shfl_sync(FULL, my_chunks, i) > 0;
-      const int32_t cb = m.vb + ci * kChunkV;
-      const int32_t ce = cb + kChunkV < m.ve ? cb + kChunkV : m.ve;
-      if (al) {
-        const int32_t full = m.x >> 2, rem = m.x & 3;
-        const int4* slot = ring + (c % kNS) * kChunkV;
-        int4* d4 = reinterpret_cast<int4*>(m.dst);
-        uint32_t* m4 = reinterpret_cast<uint32_t*>(m.mdst);
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int32_t v = cb + u * 32 + lane;
-          if (v < ce) {
-            int4 val = v < full ? slot[u * 32 + lane] : pad4;
-            if (v == full && rem) {
-              val.x = m.src[4 * v];
-              if (rem > 1) val.y = m.src[4 * v + 1];
-              if (rem > 2) val.z = m.src[4 * v + 2];
-            }
-            st_stream_v4(d4 + v, val);
-            if (m4) st_stream_u32(m4 + v, mask_word(m.x - 4 * v));
-          }
-        }
-      } else {
-        for (int32_t tt = 4 * cb + lane; tt < 4 * ce; tt += 32) {
-          m.dst[tt] = tt < m.x ? m.src[tt] : pad_id;
-          if (m.mdst) m.mdst[tt] = tt < m.x ? 1 : 0;
-        }
-      }
-    }
-    cp_async_wait<0>();
-  }
-  if (fl) latch_flags(sum, fl);
-}
-
-template <int kU, int kNS, int kWarps>
-static cudaError_t launch_pack_ring(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
-                                    const int64_t* tok_off, const int32_t* tokens,
-                                    const bs_window_params& p, const bs_batch* batches,
-                                    int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
-                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
-                                    bs_summary* summary, cudaStream_t st) {
-  const size_t smem = (size_t)kWarps * kNS * 32 * kU * 16;
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(k_pack_ring<kU, kNS, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_ring<kU, kNS, kWarps>,
-                                                  kWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
-  k_pack_ring<kU, kNS, kWarps><<<blocks, kWarps * 32, smem, st>>>(
-      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
-      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary, ctx->piece_tok);
-  ++ctx->launches;
-  return cudaGetLastError();
-}
-
-// non-persistent form: one 32-piece group per warp (grid from an upper bound on the
-// pieces), so CTAs retire as they finish and kernels of other streams can interleave
-template <int kU, int kMinB>
-static cudaError_t launch_pack_flat(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
-                                    const int64_t* tok_off, const int32_t* tokens,
-                                    const bs_window_params& p, const bs_batch* batches,
-                                    int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
-                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
-                                    bs_summary* summary, cudaStream_t st) {
-  const int64_t groups = (ctx->pack_pieces + 31) / 32;  // bound from the last sized window
-  const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
-  k_pack<kU, kMinB><<<(unsigned)blocks, kPackThreads, 0, st>>>(
-      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
-      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary, ctx->piece_tok);
-  ++ctx->launches;
-  return cudaGetLastError();
-}
-
-// non-persistent: one 32-piece group per warp
-template <int kU, int kMinB, bool kUni = false>
+// non-persistent: one 32-piece group per warp (grid from an upper bound on the pieces of
+// the last sized window), so CTAs retire as they finish and the scheduling kernels of
+// other windows in flight interleave with this pack
+template <int kU, int kMinB, bool kUni>
 static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                       const int64_t* tok_off, const int32_t* tokens,
                                       const bs_window_params& p, const bs_batch* batches,
                                       int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
                                       int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                       bs_summary* summary, cudaStream_t st) {
-  const int64_t groups = (ctx->pack_pieces + 31) / 32;  // bound from the last sized window
+  const int64_t groups = (ctx->pack_pieces + 31) / 32;
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
   k_pack_stream<kU, kMinB, kUni><<<(unsigned)blocks, kPackThreads, 0, st>>>(
-      len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
-      batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary, ctx->piece_tok);
-  ++ctx->launches;
-  return cudaGetLastError();
-}
-
-template <int kU, int kMinB>
-static cudaError_t launch_pack_v(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
-                                 const int64_t* tok_off, const int32_t* tokens,
-                                 const bs_window_params& p, const bs_batch* batches,
-                                 int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
-                                 int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
-                                 bs_summary* summary, cudaStream_t st) {
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack<kU, kMinB>, kPackThreads, 0);
-    if (per_sm > kMinB) per_sm = kMinB;  // kMinB CTAs per SM: the rest of the SM stays free
-    if (per_sm < 1) per_sm = 1;
-  }
-  const unsigned blocks = (unsigned)(per_sm * ctx->num_sms);
-  k_pack<kU, kMinB><<<blocks, kPackThreads, 0, st>>>(
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
       summary, ctx->piece_tok);
@@ -818,57 +529,22 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const bs_batch* batches, int64_t batch_begin, int64_t batch_end,
                         int32_t batches_cap, int32_t* out_tokens, uint8_t* out_mask,
                         int64_t out_capacity, bs_summary* summary, cudaStream_t st) {
-#define BS_PACK_V(U, MB)                                                                  \
-  return launch_pack_v<U, MB>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,   \
-                              batch_end, batches_cap, out_tokens, out_mask, out_capacity, \
-                              summary, st)
-  int v = ctx->pack_variant;
-  // default: the TMA staging variant for long-context windows (rows of many KB: C4 at
-  // 90-91 % of the copy peak with windows in flight; the register stream packs faster
+  // The TMA staging kernel for long-context windows (rows of many KB: C4 at 89-91 % of
+  // the copy peak with windows in flight; the register stream packs a C4 window faster
   // alone, 96 %, but fills every SM and slows the windows in flight), the flattened
   // 128-bit register stream with the uniform-group fast path otherwise (C2 758 vs 786
-  // us, C3 11.11 vs 11.45 ms against the stream without it), on a non-persistent grid
-  // (CTAs retire as they finish, so the scheduling kernels of the windows in flight
-  // interleave with this pack; persistent grids of 3-4 CTAs per SM measured 2-8 %
-  // slower per window).  Tuning hook BS_PACK_VARIANT (all bit-identical):
-  //   1  k_pack, persistent grid (6 CTAs/SM)             5  TMA bulk-copy staging
-  //   2  k_pack, 8 vectors per lane, 4 CTAs/SM           6  cp.async shared-memory ring
-  //   17 k_pack, non-persistent grid                     18 k_pack_stream, 5 CTAs/SM bound
-  //   20 k_pack_stream, 4 CTAs/SM, no uniform fast path  22 as 21, 8 vectors per lane
-  //   21 k_pack_stream, 4 CTAs/SM + uniform-group fast path (default for l_max <= 16384)
-  if (v == 0) v = p.l_max > 16384 ? 5 : 21;
-  switch (v) {
-    case 1: BS_PACK_V(4, 6);
-    case 2: BS_PACK_V(8, 4);
-    case 5:
-      return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
-                             batches_cap, out_tokens, out_mask, out_capacity, summary, st);
-    case 18:
-      return launch_pack_stream<4, 5>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
-                                      batch_end, batches_cap, out_tokens, out_mask, out_capacity,
-                                      summary, st);
-    case 21:
-      return launch_pack_stream<4, 4, true>(ctx, len, perm, tok_off, tokens, p, batches,
-                                            batch_begin, batch_end, batches_cap, out_tokens,
-                                            out_mask, out_capacity, summary, st);
-    case 22:
-      return launch_pack_stream<8, 3, true>(ctx, len, perm, tok_off, tokens, p, batches,
-                                            batch_begin, batch_end, batches_cap, out_tokens,
-                                            out_mask, out_capacity, summary, st);
-    case 20:
-      return launch_pack_stream<4, 4>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
-                                      batch_end, batches_cap, out_tokens, out_mask, out_capacity,
-                                      summary, st);
-    case 6:
-      return launch_pack_ring<4, 4, 8>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
-                                       batch_end, batches_cap, out_tokens, out_mask,
-                                       out_capacity, summary, st);
-    default:
-      return launch_pack_flat<4, 6>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
-                                    batch_end, batches_cap, out_tokens, out_mask, out_capacity,
-                                    summary, st);
-  }
-#undef BS_PACK_V
+  // us, C3 11.11 vs 11.45 ms against the stream without it).  ctx->pack_variant
+  // (BS_PACK_VARIANT at bs_create) forces one: 5 = TMA, 21 = register stream; both are
+  // bit-identical.  The slower forms measured in round 1 (per-row k_pack, persistent
+  // grids, a cp.async shared-memory ring, 8 vectors per lane) are recorded in DESIGN.md.
+  int v = ctx->pack_variant;
+  if (v != 5 && v != 21) v = p.l_max > 16384 ? 5 : 21;
+  if (v == 5)
+    return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
+                           batches_cap, out_tokens, out_mask, out_capacity, summary, st);
+  return launch_pack_stream<4, 4, true>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin,
+                                        batch_end, batches_cap, out_tokens, out_mask, out_capacity,
+                                        summary, st);
 }
 
 }  // namespace bsk

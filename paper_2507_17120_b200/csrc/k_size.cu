@@ -948,11 +948,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                     (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
     const bool wide = ctx->chain_wide >= 0 ? ctx->chain_wide != 0 : n > kChainWide;
     // small windows: fewer CTAs (a grid barrier over 148 CTAs costs more than the work)
-    static int cap = -1;
-    if (cap < 0) {  // tuning hook
-      const char* v = getenv("BS_CHAIN_CTAS");
-      cap = v ? std::max(1, atoi(v)) : ctx->chain_blocks;
-    }
+    const int cap = ctx->chain_ctas > 0 ? ctx->chain_ctas : ctx->chain_blocks;  // tuning hook
     const unsigned cblocks = (unsigned)std::min<int64_t>(
         std::min(ctx->chain_blocks, cap), std::max<int64_t>(1, (n + 4095) / 4096));
     e = cudaLaunchCooperativeKernel(wide ? (void*)k_chain<1024, 1> : (void*)k_chain<512, 3>,

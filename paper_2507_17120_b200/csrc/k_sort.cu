@@ -238,11 +238,7 @@ cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, in
   (void)summary;
   if (n == 0) return cudaSuccess;
   const SortPlan sp = sort_plan(p.l_max, p.n_classes);
-  static int force = -1;
-  if (force < 0) {  // tuning hook: BS_SORT_ITEMS=8|16
-    const char* v = getenv("BS_SORT_ITEMS");
-    force = v ? atoi(v) : 0;
-  }
+  const int force = ctx->sort_items;  // tuning hook BS_SORT_ITEMS=8|16 (read by bs_create)
   if (force == 8 || (force != 16 && n < (int64_t)4 << 20))
     return order_passes<kItemsSmall>(ctx, len, cls, n, p, perm_out, bucket_out, sp, st);
   return order_passes<kItemsLarge>(ctx, len, cls, n, p, perm_out, bucket_out, sp, st);
