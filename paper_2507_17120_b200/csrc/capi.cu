@@ -142,6 +142,8 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_HIST_MAXB")) ctx->hist_maxb = std::max(1, atoi(v));
   if (const char* v = getenv("BS_SORT_ITEMS")) ctx->sort_items = atoi(v);
   if (const char* v = getenv("BS_CHAIN_CTAS")) ctx->chain_ctas = std::max(1, atoi(v));
+  if (const char* v = getenv("BS_CHAIN_WALK")) ctx->chain_walk = std::max(1, atoi(v));
+  if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
   int r = 1;
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;
@@ -274,7 +276,7 @@ int bs_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (summary) {
-    BS_CUDA(bsk::launch_init_summary(summary, n, st), "init_summary");
+    BS_CUDA(bsk::launch_init_summary(ctx, summary, n, st), "init_summary");
     ++ctx->launches;
   }
   BS_CUDA(bsk::launch_histogram(ctx, len, cls, n, *p, hist_out, summary, st), "k_histogram");
@@ -513,6 +515,16 @@ static int check_io(bs_ctx* ctx, const bs_window_io* io) {
   return BS_OK;
 }
 
+namespace {
+struct WindowScope {
+  bs_ctx* c;
+  ~WindowScope() {
+    c->window_zeroed = false;
+    c->prof_in_window = false;
+  }
+};
+}  // namespace
+
 int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
                        void* stream) {
   if (!ctx) return fail(nullptr, BS_ERR_INVALID_ARG, "ctx is NULL");
@@ -521,11 +533,18 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ctx->prof_in_window = true;
+  WindowScope scope{ctx};  // clears window_zeroed / prof_in_window on every return
   bsk::prof_mark(ctx, 0, st);
-  BS_CUDA(bsk::launch_init_summary(io->summary, io->n, st), "init_summary");
-  ++ctx->launches;
-  BS_CUDA(bsk::launch_histogram(ctx, io->len, io->cls, io->n, *p, io->hist, io->summary, st),
-          "k_histogram");
+  BS_CUDA(bsk::launch_window_init(ctx, io->summary, io->n, io->hist,
+                                  (int64_t)p->l_max * p->n_classes,
+                                  bsk::sort_status_words(ctx, io->n, *p), st),
+          "k_window_init");
+  ctx->window_zeroed = true;  // the launchers below skip their memsets
+  cudaError_t ek = bsk::launch_histogram(ctx, io->len, io->cls, io->n, *p, io->hist, io->summary, st);
+  if (ek != cudaSuccess) {
+    ctx->window_zeroed = ctx->prof_in_window = false;
+    return cuda_fail(ctx, ek, "k_histogram");
+  }
   bsk::prof_mark(ctx, 1, st);
   bs_window_io local = *io;
   local.hist_global = io->hist;
@@ -554,6 +573,7 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
   bsk::prof_mark(ctx, 2, st);
   rc = window_from_hist_impl(ctx, &local, p, st);
   ctx->prof_in_window = false;
+  ctx->window_zeroed = false;
   return rc;
 }
 
@@ -632,7 +652,7 @@ int bs_monitor_bins(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p
   if ((rc = check_params(ctx, p)) != BS_OK) return rc;
   if (!hist || !out || bins < 1 || bins > 4096) return fail(ctx, BS_ERR_INVALID_ARG, "bad arguments");
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  BS_CUDA(bsk::launch_monitor_bins(hist, *p, bins, out, static_cast<cudaStream_t>(stream)),
+  BS_CUDA(bsk::launch_monitor_bins(ctx, hist, *p, bins, out, static_cast<cudaStream_t>(stream)),
           "k_monitor_bins");
   return BS_OK;
 }
@@ -648,7 +668,7 @@ int bs_monitor(bs_ctx* ctx, const uint32_t* hist, const bs_window_params* p, int
   if (edges && (k < 1 || k > p->l_max || !stats_out))
     return fail(ctx, BS_ERR_INVALID_ARG, "edges need 1 <= k <= l_max and stats_out");
   BS_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  BS_CUDA(bsk::launch_monitor(hist, *p, bins, edges, k, counts_out, stats_out,
+  BS_CUDA(bsk::launch_monitor(ctx, hist, *p, bins, edges, k, counts_out, stats_out,
                               static_cast<cudaStream_t>(stream)),
           "k_monitor");
   ++ctx->launches;

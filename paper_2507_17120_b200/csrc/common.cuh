@@ -19,6 +19,19 @@ constexpr uint32_t kStatAgg = 1u << 30;
 constexpr uint32_t kStatPrefix = 2u << 30;
 constexpr uint32_t kStatMask = (1u << 30) - 1;
 
+// Programmatic dependent launch (sm_90+).  The window's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (ctx.cuh: launch_k), so a kernel may
+// be scheduled while its predecessor on the stream is still running.  Every kernel calls
+// pdl_prologue() first: griddepcontrol.wait blocks until the predecessor grid has
+// completed and its writes are visible (a no-op for a normal launch) — so completion is
+// still transitive along the stream — and launch_dependents lets the successor's CTAs be
+// scheduled as soon as every CTA of this grid has started, hiding its launch latency
+// behind this grid's run time.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

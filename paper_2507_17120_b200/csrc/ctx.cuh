@@ -2,6 +2,7 @@
 #pragma once
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -28,7 +29,11 @@ struct bs_ctx {
   int hist_maxb = 0;        // K1 CTA cap (BS_HIST_MAXB; default 2 per SM)
   int sort_items = 0;       // K4 keys per thread: 0 = by window size, 8 | 16 (BS_SORT_ITEMS)
   int chain_ctas = 0;       // K5c CTA cap, 0 = one per SM (BS_CHAIN_CTAS)
+  int chain_walk = 0;       // K5c serial-walk limit, 0 = default (BS_CHAIN_WALK)
   int pack_tma_blocks = 0;  // K6 TMA grid: co-resident CTAs per SM x SMs
+  int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
+  bool window_zeroed = false;  // inside a fused window call whose k_window_init zeroed the
+                               // accumulators (the launchers then skip their memsets)
   std::string err;
   // stage profiler: ring of (BS_STAGES+1) events per recorded step
   std::vector<cudaEvent_t> prof_events;
@@ -128,6 +133,41 @@ inline void prof_mark(bs_ctx* ctx, int stage, cudaStream_t st) {
   if (stage == BS_STAGES) ++ctx->prof_recorded;
 }
 
+// Kernel launch for the window path: cudaLaunchKernelEx with programmatic stream
+// serialization when ctx->pdl (see pdl_prologue in common.cuh), and the cooperative
+// attribute for grid-synchronising kernels.  If the driver refuses the combination of a
+// cooperative launch with PDL, the kernel is launched cooperatively without it.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(const bs_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                            size_t smem, cudaStream_t st, bool cooperative, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  unsigned na = 0;
+  if (cooperative) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  if (ctx->pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess && cooperative && ctx->pdl) {
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;  // cooperative only
+    e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  }
+  return e;
+}
+
 struct SortPlan {
   int passes;  // radix passes
   int bits;    // digit bits per pass (<= 8)
@@ -166,12 +206,15 @@ int peer_flag_words();
 int dispatch_threads();
 cudaError_t launch_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_params& p,
                                uint32_t* hist_global, bs_summary* summary, cudaStream_t st);
-cudaError_t launch_monitor(const uint32_t* hist, const bs_window_params& p, int32_t bins,
-                           const int32_t* edges, int32_t k, uint64_t* out, double* stats,
-                           cudaStream_t st);
-cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
-                                uint64_t* out, cudaStream_t st);
-cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st);
+cudaError_t launch_monitor(const bs_ctx* ctx, const uint32_t* hist, const bs_window_params& p,
+                           int32_t bins, const int32_t* edges, int32_t k, uint64_t* out,
+                           double* stats, cudaStream_t st);
+cudaError_t launch_monitor_bins(const bs_ctx* ctx, const uint32_t* hist, const bs_window_params& p,
+                                int32_t bins, uint64_t* out, cudaStream_t st);
+cudaError_t launch_init_summary(const bs_ctx* ctx, bs_summary* s, int64_t n, cudaStream_t st);
+cudaError_t launch_window_init(bs_ctx* ctx, bs_summary* s, int64_t n, uint32_t* hist,
+                               int64_t hist_words, int64_t status_words, cudaStream_t st);
+int64_t sort_status_words(const bs_ctx* ctx, int64_t n, const bs_window_params& p);
 // per-context, per-device setup run by bs_create (shared-memory opt-ins, occupancy)
 cudaError_t hist_prepare(bs_ctx* ctx);
 cudaError_t bounds_prepare(bs_ctx* ctx);

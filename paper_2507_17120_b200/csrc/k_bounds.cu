@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(1024)
     k_prefix_tiles(const uint32_t* __restrict__ hist_local, const uint32_t* __restrict__ hist_global,
                    int32_t L, int32_t C, uint32_t* __restrict__ P, uint32_t* __restrict__ PcL,
                    uint32_t* __restrict__ tile_tot, unsigned long long* __restrict__ tile_slen) {
+  pdl_prologue();
   __shared__ uint32_t s32[33];
   __shared__ uint64_t s64[33];
   const int t = blockIdx.x;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kBT, 1)
                  int32_t* __restrict__ gE, uint32_t* __restrict__ gbm, uint32_t* __restrict__ gwp,
                  int32_t* __restrict__ seg_base, uint32_t* __restrict__ tile_carry,
                  uint32_t* __restrict__ bins_cnt, int32_t* __restrict__ kinfo, bs_summary* sum) {
+  pdl_prologue();
   extern __shared__ uint32_t dyn[];
   __shared__ BoundsShared sh;
   const int32_t L = p.l_max, C = p.n_classes;
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(256)
              int32_t* __restrict__ lut, uint32_t* __restrict__ slot_lut,
              uint32_t* __restrict__ bins_cnt, int32_t* __restrict__ slot_seg,
              int32_t* __restrict__ slot_len) {
+  pdl_prologue();
   __shared__ uint32_t sbins[4 * 256];
   const int32_t L = p.l_max, C = p.n_classes;
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) sbins[i] = 0;
@@ -439,6 +442,7 @@ __global__ void __launch_bounds__(kSmallBT, kSmallBTMin)
                    uint32_t* __restrict__ slot_lut, uint32_t* __restrict__ bins_cnt,
                    int32_t* __restrict__ kinfo, bs_summary* sum, int32_t* __restrict__ slot_seg,
                    uint32_t* __restrict__ gbm, uint32_t* __restrict__ gwp) {
+  pdl_prologue();
   extern __shared__ uint32_t dyn[];
   __shared__ BoundsShared sh;
   __shared__ int32_t s_flag;
@@ -764,7 +768,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
   const int32_t L = p.l_max, C = p.n_classes;
   if (L <= kSmallL) {
     const size_t smem = bounds_small_smem(L);
-    k_bounds_small<<<1, kSmallBT, smem, st>>>(hist_local, hist_global ? hist_global : hist_local, p,
+    launch_k(ctx, k_bounds_small, dim3(1), dim3(kSmallBT), smem, st, false, hist_local, hist_global ? hist_global : hist_local, p,
                                          sp.bits, sp.passes, init_edges, k_init, edges_out,
                                          changes_out, changes_cap, seg_off_out, ctx->PcL, ctx->E,
                                          ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
@@ -774,7 +778,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
     const int64_t cells = (int64_t)C * L;
     const unsigned tb = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((cells + 255) / 256, 4LL * ctx->num_sms));
-    k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
+    launch_k(ctx, k_tables, dim3(tb), dim3(256), 0, st, false, hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
                                  ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
                                  ctx->slot_seg, ctx->slot_len);
     ctx->launches += 2;
@@ -782,12 +786,12 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
   }
   const int ntiles = (L + kTileX - 1) / kTileX;
   const uint32_t* hg = hist_global ? hist_global : hist_local;
-  k_prefix_tiles<<<ntiles, 1024, 0, st>>>(hist_local, hg, L, C, ctx->P, ctx->PcL, ctx->tile_tot,
+  launch_k(ctx, k_prefix_tiles, dim3(ntiles), dim3(1024), 0, st, false, hist_local, hg, L, C, ctx->P, ctx->PcL, ctx->tile_tot,
                                           reinterpret_cast<unsigned long long*>(ctx->tile_slen));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = bounds_big_smem(L);
-  k_boundaries<<<1, kBT, smem, st>>>(ctx->P, ctx->PcL, ctx->tile_tot,
+  launch_k(ctx, k_boundaries, dim3(1), dim3(kBT), smem, st, false, ctx->P, ctx->PcL, ctx->tile_tot,
                                      reinterpret_cast<const unsigned long long*>(ctx->tile_slen),
                                      ntiles, p, init_edges, k_init, edges_out, changes_out,
                                      changes_cap, seg_off_out, ctx->E, ctx->bmw, ctx->wp,
@@ -797,7 +801,7 @@ cudaError_t launch_boundaries(bs_ctx* ctx, const uint32_t* hist_local, const uin
   const int64_t cells = (int64_t)C * L;
   const unsigned tb = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((cells + 1023) / 1024, 4LL * ctx->num_sms));
-  k_tables<<<tb, 256, 0, st>>>(hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
+  launch_k(ctx, k_tables, dim3(tb), dim3(256), 0, st, false, hist_local, p, sp.bits, sp.passes, ctx->E, ctx->bmw, ctx->wp,
                                ctx->seg_base, ctx->lut, ctx->slot_lut, ctx->bins_cnt,
                                ctx->slot_seg, ctx->slot_len);
   ctx->launches += 3;

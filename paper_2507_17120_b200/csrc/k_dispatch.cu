@@ -538,6 +538,7 @@ __device__ void unreached(const DispArgs& a, const uint32_t* V, int M, int64_t w
 }  // namespace
 
 __global__ void __launch_bounds__(kKT, 1) k_dispatch(DispArgs a) {
+  pdl_prologue();
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* sk0 = reinterpret_cast<uint64_t*>(smem + kOffK0);
   uint64_t* sk1 = reinterpret_cast<uint64_t*>(smem + kOffK1);
@@ -751,9 +752,7 @@ cudaError_t launch_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg
   a.req_batch = req_batch;
   a.req_row = req_row;
   a.sum = summary;
-  void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_dispatch, dim3(ctx->disp_blocks), dim3(kKT),
-                                              args, kSmem, st);
+  cudaError_t e = launch_k(ctx, k_dispatch, dim3(ctx->disp_blocks), dim3(kKT), kSmem, st, true, a);
   ++ctx->launches;
   return e;
 }

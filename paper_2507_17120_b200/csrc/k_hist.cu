@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(512) k_histogram(const int32_t* __restrict__ l
                                                    int32_t L, int32_t C, int32_t truncate,
                                                    int32_t H, int vec_ok,
                                                    uint32_t* __restrict__ hist, bs_summary* sum) {
+  pdl_prologue();
   extern __shared__ uint32_t sh[];  // [C][H]
   for (int i = threadIdx.x; i < C * H; i += blockDim.x) sh[i] = 0;
   __syncthreads();
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(512) k_histogram(const int32_t* __restrict__ l
 }
 
 __global__ void k_init_summary(bs_summary* s, int64_t n) {
+  pdl_prologue();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     bs_summary z = {};
     z.n_requests = n;
@@ -85,8 +87,39 @@ __global__ void k_init_summary(bs_summary* s, int64_t n) {
   }
 }
 
-cudaError_t launch_init_summary(bs_summary* s, int64_t n, cudaStream_t st) {
-  k_init_summary<<<1, 32, 0, st>>>(s, n);
+cudaError_t launch_init_summary(const bs_ctx* ctx, bs_summary* s, int64_t n, cudaStream_t st) {
+  launch_k(ctx, k_init_summary, dim3(1), dim3(32), 0, st, false, s, n);
+  return cudaGetLastError();
+}
+
+// The fused window's first kernel: the summary plus every buffer the window's kernels
+// accumulate into (K1 histogram, K4 look-back status words and tile counters, K5 misc
+// counters) zeroed in one grid instead of memset nodes, which would cut the chain of
+// programmatically dependent launches.
+__global__ void k_window_init(bs_summary* s, int64_t n, uint32_t* hist, int64_t hist_words,
+                              uint32_t* status, int64_t status_words, uint32_t* tile_ctr,
+                              int32_t* misc) {
+  pdl_prologue();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0 && s) {
+    bs_summary z = {};
+    z.n_requests = n;
+    *s = z;
+  }
+  if (tid < 4) tile_ctr[tid] = 0;
+  if (tid < 128) misc[tid] = 0;
+  for (int64_t i = tid; i < hist_words; i += stride) hist[i] = 0;
+  for (int64_t i = tid; i < status_words; i += stride) status[i] = 0;
+}
+
+cudaError_t launch_window_init(bs_ctx* ctx, bs_summary* s, int64_t n, uint32_t* hist,
+                               int64_t hist_words, int64_t status_words, cudaStream_t st) {
+  const int64_t words = std::max<int64_t>(hist_words, status_words);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((words + 1023) / 1024, 4LL * ctx->num_sms));
+  launch_k(ctx, k_window_init, dim3((unsigned)blocks), dim3(256), 0, st, false, s, n, hist,
+           hist_words, ctx->status, status_words, ctx->tile_ctr, ctx->misc);
+  ++ctx->launches;
   return cudaGetLastError();
 }
 
@@ -104,7 +137,8 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
                              const bs_window_params& p, uint32_t* hist, bs_summary* summary,
                              cudaStream_t st) {
   const int32_t L = p.l_max, C = p.n_classes;
-  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)L * C, st);
+  cudaError_t e = cudaSuccess;
+  if (!ctx->window_zeroed) e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)L * C, st);
   if (e != cudaSuccess || n == 0) return e;
   // privatised head: <= 64 KB of shared counters per CTA (3 CTAs / SM)
   const int32_t H = (int32_t)std::min<int64_t>(L, (64 * 1024 / 4) / C);
@@ -120,10 +154,10 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
   const int vec_ok = ((reinterpret_cast<uintptr_t>(len) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(cls) & 3) == 0);
   if (agg)
-    k_histogram<true><<<(unsigned)blocks, threads, smem, st>>>(len, cls, n, L, C, p.truncate, H,
+    launch_k(ctx, k_histogram<true>, dim3((unsigned)blocks), dim3(threads), smem, st, false, len, cls, n, L, C, p.truncate, H,
                                                              vec_ok, hist, summary);
   else
-    k_histogram<false><<<(unsigned)blocks, threads, smem, st>>>(len, cls, n, L, C, p.truncate, H,
+    launch_k(ctx, k_histogram<false>, dim3((unsigned)blocks), dim3(threads), smem, st, false, len, cls, n, L, C, p.truncate, H,
                                                               vec_ok, hist, summary);
   ++ctx->launches;
   return cudaGetLastError();
@@ -160,6 +194,7 @@ __global__ void __launch_bounds__(1024) k_monitor(const uint32_t* __restrict__ h
                                                   const int32_t* __restrict__ edges, int32_t k,
                                                   unsigned long long* __restrict__ out,
                                                   double* __restrict__ stats) {
+  pdl_prologue();
   extern __shared__ unsigned long long sb[];
   for (int i = threadIdx.x; i < bins; i += blockDim.x) sb[i] = 0;
   __syncthreads();
@@ -194,18 +229,18 @@ __global__ void __launch_bounds__(1024) k_monitor(const uint32_t* __restrict__ h
   stats[2] = acc;
 }
 
-cudaError_t launch_monitor(const uint32_t* hist, const bs_window_params& p, int32_t bins,
-                           const int32_t* edges, int32_t k, uint64_t* out, double* stats,
-                           cudaStream_t st) {
-  k_monitor<<<1, 1024, sizeof(unsigned long long) * bins, st>>>(
+cudaError_t launch_monitor(const bs_ctx* ctx, const uint32_t* hist, const bs_window_params& p,
+                           int32_t bins, const int32_t* edges, int32_t k, uint64_t* out,
+                           double* stats, cudaStream_t st) {
+  launch_k(ctx, k_monitor, dim3(1), dim3(1024), sizeof(unsigned long long) * bins, st, false, 
       hist, p.l_max, p.n_classes, bins, edges, k, reinterpret_cast<unsigned long long*>(out),
       stats);
   return cudaGetLastError();
 }
 
-cudaError_t launch_monitor_bins(const uint32_t* hist, const bs_window_params& p, int32_t bins,
-                                uint64_t* out, cudaStream_t st) {
-  return launch_monitor(hist, p, bins, nullptr, 0, out, nullptr, st);
+cudaError_t launch_monitor_bins(const bs_ctx* ctx, const uint32_t* hist, const bs_window_params& p,
+                                int32_t bins, uint64_t* out, cudaStream_t st) {
+  return launch_monitor(ctx, hist, p, bins, nullptr, 0, out, nullptr, st);
 }
 
 }  // namespace bsk

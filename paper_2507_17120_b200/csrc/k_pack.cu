@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
                   int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in,
                   int32_t batches_cap, int32_t* __restrict__ out_tokens,
                   uint8_t* __restrict__ out_mask, int64_t out_cap, bs_summary* sum, int32_t ptok) {
+  pdl_prologue();
   const unsigned FULL = 0xffffffffu;
   int64_t b_end = b_end_arg;
   if (b_end < 0) {
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
                int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
                bs_summary* sum, int32_t ptok) {
+  pdl_prologue();
   extern __shared__ __align__(128) uint8_t tma_smem[];
   __shared__ __align__(8) uint64_t bars[kTmaWarps][kTmaSlots];
   const unsigned FULL = 0xffffffffu;
@@ -496,7 +498,7 @@ static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_
                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                    bs_summary* summary, cudaStream_t st) {
   const size_t smem = (size_t)kTmaWarps * kTmaSlots * kTmaSlotBytes;
-  k_pack_tma<<<(unsigned)ctx->pack_tma_blocks, kTmaWarps * 32, smem, st>>>(
+  launch_k(ctx, k_pack_tma, dim3((unsigned)ctx->pack_tma_blocks), dim3(kTmaWarps * 32), smem, st, false, 
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
       summary, ctx->piece_tok);
@@ -516,7 +518,7 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
                                       bs_summary* summary, cudaStream_t st) {
   const int64_t groups = (ctx->pack_pieces + 31) / 32;
   const int64_t blocks = std::max<int64_t>(1, (groups + kPackThreads / 32 - 1) / (kPackThreads / 32));
-  k_pack_stream<kU, kMinB, kUni><<<(unsigned)blocks, kPackThreads, 0, st>>>(
+  launch_k(ctx, k_pack_stream<kU, kMinB, kUni>, dim3((unsigned)blocks), dim3(kPackThreads), 0, st, false, 
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
       summary, ctx->piece_tok);

@@ -40,6 +40,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 
 __global__ void k_peer_copy(const uint32_t* __restrict__ hist, int64_t words, uint32_t* xbuf,
                             int64_t slot_words, const int64_t* flags) {
+  pdl_prologue();
   const int64_t e = flags[1] + 1;  // the epoch this window publishes
   uint32_t* slot = xbuf + (e & 1) * slot_words;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
@@ -48,6 +49,7 @@ __global__ void k_peer_copy(const uint32_t* __restrict__ hist, int64_t words, ui
 }
 
 __global__ void k_peer_flag(int64_t* flags) {
+  pdl_prologue();
   const int64_t e = flags[1] + 1;
   flags[1] = e;
   __threadfence_system();  // the slot written by k_peer_copy is visible system-wide
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(256)
     k_peer_reduce(uint32_t* const* __restrict__ peers, int world, int64_t words,
                   int64_t slot_words, const int64_t* own_flags, uint32_t* __restrict__ out,
                   bs_summary* sum) {
+  pdl_prologue();
   __shared__ int s_ok;
   const int64_t e = own_flags[1];
   const int64_t slot = (e & 1) * slot_words;
@@ -92,9 +95,9 @@ cudaError_t launch_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs
   int64_t* flags = reinterpret_cast<int64_t*>(ctx->xbuf + 2 * slot_words);
   const unsigned blocks = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>((words + 255) / 256, 2LL * ctx->num_sms));
-  k_peer_copy<<<blocks, 256, 0, st>>>(hist_local, words, ctx->xbuf, slot_words, flags);
-  k_peer_flag<<<1, 1, 0, st>>>(flags);
-  k_peer_reduce<<<blocks, 256, 0, st>>>(ctx->peer_ptrs, ctx->peer_world, words, slot_words, flags,
+  launch_k(ctx, k_peer_copy, dim3(blocks), dim3(256), 0, st, false, hist_local, words, ctx->xbuf, slot_words, flags);
+  launch_k(ctx, k_peer_flag, dim3(1), dim3(1), 0, st, false, flags);
+  launch_k(ctx, k_peer_reduce, dim3(blocks), dim3(256), 0, st, false, ctx->peer_ptrs, ctx->peer_world, words, slot_words, flags,
                                         hist_global, summary);
   ctx->launches += 3;
   return cudaGetLastError();

@@ -50,6 +50,7 @@ struct SizeArgs {
   int32_t C;         // classes (segment s holds class s % C)
   int32_t sjf_mask;  // bit c: class c drains SJF (lengths ascending in its segments)
   int32_t ljf_mask;  // bit c: class c drains LJF (lengths descending)
+  int32_t walk;      // K5c: chain calls followed serially before pointer doubling is used
 };
 
 struct Stat {
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(256)
                 int32_t* __restrict__ bmax, int32_t* __restrict__ bmin,
                 int32_t* __restrict__ bcnt, int32_t* __restrict__ bsum,
                 const uint32_t* __restrict__ skeys, const int32_t* __restrict__ slot_len) {
+  pdl_prologue();
   const int lane = threadIdx.x & 31;
   const int64_t groups = (a.n + 31) >> 5;
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(256)
                 const int32_t* __restrict__ bsum, int32_t* __restrict__ J0,
                 uint8_t* __restrict__ is_start, int32_t* __restrict__ alive,
                 const uint32_t* __restrict__ skeys, const int32_t* __restrict__ slot_seg) {
+  pdl_prologue();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int32_t n_segs = kinfo[2];
@@ -412,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             const int32_t* __restrict__ bcnt, int32_t* __restrict__ Rg, int32_t* btot,
             int32_t* segw, int32_t batches_cap, bs_summary* sum, int32_t* dseg, int32_t* dmin,
             int64_t* dsum) {
+  pdl_prologue();
   cg::grid_group grid = cg::this_grid();
   __shared__ ChainShared sh;
   const int64_t n = a.n;
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         for (;;) {
           const int32_t y = J[pos];
           if (y == kEnd) break;
-          if (++k >= kWalk) { lng = 1; break; }
+          if (++k >= a.walk) { lng = 1; break; }
           listB[st + k] = y;
           pos = y;
         }
@@ -645,6 +649,7 @@ __global__ void __launch_bounds__(256)
                     const int32_t* __restrict__ misc, bs_batch* __restrict__ batches,
                     int32_t batches_cap, bs_summary* sum, const uint32_t* __restrict__ skeys,
                     const int32_t* __restrict__ slot_seg) {
+  pdl_prologue();
   const int M = misc[64];
   const int32_t n_segs = kinfo[2];
   const int32_t* list = misc[68] ? listB : listA;
@@ -726,6 +731,7 @@ __global__ void __launch_bounds__(256)
                    int32_t* __restrict__ rowpos, bs_summary* sum,
                    const int32_t* __restrict__ slen, int32_t* __restrict__ dmin,
                    int64_t* __restrict__ dsum, int32_t r_lo, int32_t r_hi, int first) {
+  pdl_prologue();
   const int M = misc[64];
   const int32_t* list = misc[68] ? listB : listA;
   const int lane = threadIdx.x & 31;
@@ -817,6 +823,7 @@ __global__ void __launch_bounds__(1024)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
                    const int32_t* __restrict__ misc, int64_t* __restrict__ task_base,
                    bs_summary* sum, int32_t ptok) {
+  pdl_prologue();
   __shared__ int64_t s_l[33];
   __shared__ double s_d[32];
   __shared__ int64_t s_a[32], s_p[32], s_pk[32];
@@ -872,6 +879,7 @@ __global__ void __launch_bounds__(1024)
 }
 
 __global__ void k_fill_pending(int64_t n, int32_t* req_batch, int32_t* req_row, bs_summary* sum) {
+  pdl_prologue();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     req_batch[i] = BS_REQ_PENDING;
@@ -890,8 +898,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     for (int s = 5; s <= 8; ++s) prof_mark(ctx, s, st);
   if (n == 0) return cudaSuccess;
   if (H <= 0) {  // form_batch returns None before touching the queue (:150-152)
-    k_fill_pending<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4LL * ctx->num_sms), 256, 0,
-                     st>>>(n, req_batch, req_row, summary);
+    launch_k(ctx, k_fill_pending, dim3((unsigned)std::min<int64_t>((n + 255) / 256, 4LL * ctx->num_sms)), dim3(256), 0, st, false, n, req_batch, req_row, summary);
     ++ctx->launches;
     return cudaGetLastError();
   }
@@ -905,21 +912,24 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   a.truncate = p.truncate;
   a.C = p.n_classes;
   a.sjf_mask = a.ljf_mask = 0;
+  a.walk = ctx->chain_walk > 0 ? ctx->chain_walk : kWalk;
   for (int c = 0; c < p.n_classes; ++c) {
     if (p.policy[c] == BS_POLICY_SJF) a.sjf_mask |= 1 << c;
     if (p.policy[c] == BS_POLICY_LJF) a.ljf_mask |= 1 << c;
   }
   int32_t* misc = ctx->misc;
-  e = cudaMemsetAsync(misc, 0, sizeof(int32_t) * 128, st);
-  if (e != cudaSuccess) return e;
+  if (!ctx->window_zeroed) {  // the fused window zeroes misc in k_window_init
+    e = cudaMemsetAsync(misc, 0, sizeof(int32_t) * 128, st);
+    if (e != cudaSuccess) return e;
+  }
   const int64_t groups = (n + 31) >> 5;
   const unsigned wblocks = (unsigned)std::min<int64_t>((groups + 7) / 8, 16LL * ctx->num_sms);
-  k_size_prep<<<wblocks, 256, 0, st>>>(len, perm, a, ctx->sorted_len, ctx->bmask, ctx->bmax,
+  launch_k(ctx, k_size_prep, dim3(wblocks), dim3(256), 0, st, false, len, perm, a, ctx->sorted_len, ctx->bmask, ctx->bmax,
                                        ctx->bmin, ctx->bcnt, ctx->bsum, ctx->sorted_keys,
                                        ctx->slot_len);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 5, st);
-  k_size_next<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmask,
+  launch_k(ctx, k_size_next, dim3(wblocks), dim3(256), 0, st, false, a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmask,
                                        ctx->bmax, ctx->bcnt, ctx->bsum, ctx->J, ctx->is_start,
                                        misc, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -943,27 +953,30 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     int32_t* dseg = p.dispatch ? ctx->disp_cseg : nullptr;
     int32_t* dmin = p.dispatch ? ctx->disp_cmin : nullptr;
     int64_t* dsum = p.dispatch ? ctx->disp_csum : nullptr;
-    void* args[] = {&a,    (void*)&ki, (void*)&so, &J,   &r_cap, (void*)&is_start, &alive,
-                    &la,   &lb,        &nbp,       &nj0, &misc,  (void*)&sl,       (void*)&bm,
-                    (void*)&bc, &rg,   &bt,        &sw,  &bcap, &sm, &dseg, &dmin, &dsum};
     const bool wide = ctx->chain_wide >= 0 ? ctx->chain_wide != 0 : n > kChainWide;
     // small windows: fewer CTAs (a grid barrier over 148 CTAs costs more than the work)
     const int cap = ctx->chain_ctas > 0 ? ctx->chain_ctas : ctx->chain_blocks;  // tuning hook
     const unsigned cblocks = (unsigned)std::min<int64_t>(
         std::min(ctx->chain_blocks, cap), std::max<int64_t>(1, (n + 4095) / 4096));
-    e = cudaLaunchCooperativeKernel(wide ? (void*)k_chain<1024, 1> : (void*)k_chain<512, 3>,
-                                    dim3(cblocks), dim3(wide ? 1024 : 512), args, 0, st);
+    if (wide)
+      e = launch_k(ctx, k_chain<1024, 1>, dim3(cblocks), dim3(1024), 0, st, true, a, ki, so, J,
+                   r_cap, is_start, alive, la, lb, nbp, nj0, misc, sl, bm, bc, rg, bt, sw, bcap,
+                   sm, dseg, dmin, dsum);
+    else
+      e = launch_k(ctx, k_chain<512, 3>, dim3(cblocks), dim3(512), 0, st, true, a, ki, so, J,
+                   r_cap, is_start, alive, la, lb, nbp, nj0, misc, sl, bm, bc, rg, bt, sw, bcap,
+                   sm, dseg, dmin, dsum);
     if (e != cudaSuccess) return e;
   }
   prof_mark(ctx, 7, st);
-  k_size_describe<<<wblocks, 256, 0, st>>>(a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax,
+  launch_k(ctx, k_size_describe, dim3(wblocks), dim3(256), 0, st, false, a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax,
                                            ctx->bmin, ctx->bcnt, ctx->bsum, ctx->J, ctx->listA,
                                            ctx->listB, ctx->node_batch, misc, batches,
                                            batches_cap, summary, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ctx->piece_tok = piece_tokens_for(n);
   ctx->pack_pieces = n * (((int64_t)p.l_max + ctx->piece_tok - 1) / ctx->piece_tok);
-  k_size_offsets<<<1, 1024, 0, st>>>(batches, batches_cap, misc, ctx->task_base, summary,
+  launch_k(ctx, k_size_offsets, dim3(1), dim3(1024), 0, st, false, batches, batches_cap, misc, ctx->task_base, summary,
                                      ctx->piece_tok);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 8, st);
@@ -976,7 +989,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                               : (int)std::max<int64_t>(1, (n * 8 + (32LL << 20) - 1) / (32LL << 20));
   const int64_t span = (n + parts - 1) / parts;
   for (int q = 0; q < parts; ++q) {
-    k_size_outcome<<<wblocks, 256, 0, st>>>(
+    launch_k(ctx, k_size_outcome, dim3(wblocks), dim3(256), 0, st, false, 
         a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB, ctx->node_batch, ctx->node_j0, misc,
         batches, batches_cap, req_batch, req_row, ctx->rowpos, summary, ctx->sorted_len,
         p.dispatch ? ctx->disp_cmin : nullptr, p.dispatch ? ctx->disp_csum : nullptr,

@@ -40,6 +40,7 @@ constexpr int kSortMinBlocks8 = BS_SORT_MINB8;
 __global__ void k_assign(const int32_t* __restrict__ len, int64_t n, int32_t L, int32_t truncate,
                          const int32_t* __restrict__ lut, int32_t* __restrict__ bucket_out,
                          bs_summary* sum) {
+  pdl_prologue();
   unsigned fl = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 
                 const int32_t* __restrict__ lut, int32_t* __restrict__ bucket_out, int shift,
                 int bits, const uint32_t* __restrict__ bins_cnt, uint32_t* __restrict__ status,
                 uint32_t* __restrict__ tile_ctr) {
+  pdl_prologue();
   constexpr int kTile = kSortThreads * kItems;
   __shared__ uint32_t s_cnt[kSortWarps][256];
   __shared__ uint32_t s_keys[kTile];
@@ -184,7 +186,7 @@ cudaError_t launch_assign(bs_ctx* ctx, const int32_t* len, int64_t n, const bs_w
                           int32_t* bucket_out, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 8LL * ctx->num_sms);
-  k_assign<<<(unsigned)blocks, 256, 0, st>>>(len, n, p.l_max, p.truncate, ctx->lut, bucket_out,
+  launch_k(ctx, k_assign, dim3((unsigned)blocks), dim3(256), 0, st, false, len, n, p.l_max, p.truncate, ctx->lut, bucket_out,
                                               nullptr);
   ++ctx->launches;
   return cudaGetLastError();
@@ -197,10 +199,13 @@ static cudaError_t order_passes(bs_ctx* ctx, const int32_t* len, const uint8_t* 
   constexpr int kTile = kSortThreads * kItems;
   const int64_t tiles = (n + kTile - 1) / kTile;
   const size_t stat_words = (size_t)tiles * 256;
-  cudaError_t e = cudaMemsetAsync(ctx->status, 0, sizeof(uint32_t) * stat_words * sp.passes, st);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(ctx->tile_ctr, 0, sizeof(uint32_t) * 4, st);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (!ctx->window_zeroed) {  // the fused window zeroes these in k_window_init
+    e = cudaMemsetAsync(ctx->status, 0, sizeof(uint32_t) * stat_words * sp.passes, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ctx->tile_ctr, 0, sizeof(uint32_t) * 4, st);
+    if (e != cudaSuccess) return e;
+  }
   const uint32_t* kin = nullptr;
   const uint32_t* vin = nullptr;
   uint32_t* kbuf[2] = {ctx->keysA, ctx->keysB};
@@ -214,7 +219,7 @@ static cudaError_t order_passes(bs_ctx* ctx, const int32_t* len, const uint8_t* 
     uint32_t* tc = ctx->tile_ctr + q;
     const int shift = q * sp.bits;
 #define BS_SORT_LAUNCH(F, LST)                                                                \
-  k_sort_pass<F, LST, kItems><<<(unsigned)tiles, kSortThreads, 0, st>>>(                      \
+  launch_k(ctx, k_sort_pass<F, LST, kItems>, dim3((unsigned)tiles), dim3(kSortThreads), 0, st, false,                       \
       len, cls, kin, vin, kout, vout, n, p.l_max, p.n_classes, p.truncate, ctx->slot_lut,     \
       ctx->lut, bucket_out, shift, sp.bits, bb, stt, tc)
     if (first && last) BS_SORT_LAUNCH(true, true);
@@ -230,6 +235,16 @@ static cudaError_t order_passes(bs_ctx* ctx, const int32_t* len, const uint8_t* 
   }
   ctx->sorted_keys = kin;
   return cudaSuccess;
+}
+
+// words of look-back status (all passes) launch_order zeroes for a window of n requests
+int64_t sort_status_words(const bs_ctx* ctx, int64_t n, const bs_window_params& p) {
+  if (n == 0) return 0;
+  const SortPlan sp = sort_plan(p.l_max, p.n_classes);
+  const int force = ctx->sort_items;
+  const int items = (force == 8 || (force != 16 && n < (int64_t)4 << 20)) ? kItemsSmall : kItemsLarge;
+  const int64_t tiles = (n + (int64_t)kSortThreads * items - 1) / ((int64_t)kSortThreads * items);
+  return tiles * 256 * sp.passes;
 }
 
 cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, int64_t n,
