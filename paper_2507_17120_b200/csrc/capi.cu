@@ -83,7 +83,7 @@ void free_all(bs_ctx* c) {
                   c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->task_base, c->segw,
                   c->disp_cseg, c->disp_cmin, c->disp_csum, c->disp_keys0, c->disp_keys1,
                   c->disp_vals0, c->disp_vals1, c->disp_hist8, c->disp_agg, c->disp_status, c->disp_tctr, c->disp_nulls, c->disp_runs, c->disp_misc,
-                  c->misc};
+                  c->misc, c->small_rows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -144,6 +144,8 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_CHAIN_CTAS")) ctx->chain_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("BS_CHAIN_WALK")) ctx->chain_walk = std::max(1, atoi(v));
   if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
+  if (const char* v = getenv("BS_SMALL")) ctx->small_path = atoi(v) != 0;
+  if (const char* v = getenv("BS_SMALL_TIMING")) ctx->small_timing = atoi(v) != 0;
   int r = 1;
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;
@@ -189,6 +191,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(rowpos, N + 1);
   A(task_base, N + 2);
   A(misc, 128);
+  A(small_rows, 2048 * 32);  // bsk::kSmallN SmallRow records
   // K7 dispatch order
   A(disp_cseg, N + 1); A(disp_cmin, N + 1); A(disp_csum, N + 1);
   A(disp_keys0, N + 1); A(disp_keys1, N + 1); A(disp_vals0, N + 1); A(disp_vals1, N + 1);
@@ -243,7 +246,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
 #undef A
   // per-device kernel attributes (checked): every context sets them on its own device
   if ((e = bsk::hist_prepare(ctx)) != cudaSuccess || (e = bsk::bounds_prepare(ctx)) != cudaSuccess ||
-      (e = bsk::pack_prepare(ctx)) != cudaSuccess) {
+      (e = bsk::pack_prepare(ctx)) != cudaSuccess || (e = bsk::small_prepare(ctx)) != cudaSuccess) {
     int rc = cuda_fail(ctx, e, "kernel attributes");
     free_all(ctx);
     delete ctx;
@@ -464,6 +467,21 @@ int bs_peer_reduce(bs_ctx* ctx, const uint32_t* hist_local, const bs_window_para
   return BS_OK;
 }
 
+static int pack_impl(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
+                     cudaStream_t st) {
+  if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
+    if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
+      return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
+    if (io->out_mask && (reinterpret_cast<uintptr_t>(io->out_mask) & 3))
+      return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
+    BS_CUDA(bsk::launch_pack(ctx, io->len, io->perm, io->tok_off, io->tokens, *p, io->batches,
+                             0, -1, io->batches_cap, io->out_tokens, io->out_mask,
+                             io->out_capacity, io->summary, st),
+            "k_pack");
+  }
+  return BS_OK;
+}
+
 static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_window_params* p,
                                  cudaStream_t st) {
   int rc;
@@ -488,16 +506,7 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
             "k_dispatch");
   }
   bsk::prof_mark(ctx, 10, st);
-  if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
-    if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
-      return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
-    if (io->out_mask && (reinterpret_cast<uintptr_t>(io->out_mask) & 3))
-      return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
-    BS_CUDA(bsk::launch_pack(ctx, io->len, io->perm, io->tok_off, io->tokens, *p, io->batches,
-                             0, -1, io->batches_cap, io->out_tokens, io->out_mask,
-                             io->out_capacity, io->summary, st),
-            "k_pack");
-  }
+  if ((rc = pack_impl(ctx, io, p, st)) != BS_OK) return rc;
   bsk::prof_mark(ctx, 11, st);
   return BS_OK;
 }
@@ -535,6 +544,25 @@ int bs_window_schedule(bs_ctx* ctx, const bs_window_io* io, const bs_window_para
   ctx->prof_in_window = true;
   WindowScope scope{ctx};  // clears window_zeroed / prof_in_window on every return
   bsk::prof_mark(ctx, 0, st);
+  if (!ctx->nccl_comm && ctx->peer_world <= 1 &&
+      bsk::small_window_ok(ctx, io->n, *p, io->init_edges ? io->k_init : 0)) {
+    // K0: the whole schedule of a small window in one CTA (its time reads as stage 0)
+    if (io->init_edges && (io->k_init < 1 || io->k_init > p->l_max))
+      return fail(ctx, BS_ERR_INVALID_ARG, "k_init out of range");
+    BS_CUDA(bsk::launch_window_small(ctx, io, *p, st), "k_window_small");
+    for (int s = 1; s <= 10; ++s) bsk::prof_mark(ctx, s, st);
+    if (io->tok_off && io->tokens && io->out_tokens && io->n > 0) {
+      if (reinterpret_cast<uintptr_t>(io->out_tokens) & 15)
+        return fail(ctx, BS_ERR_INVALID_ARG, "out_tokens must be 16-byte aligned");
+      if (io->out_mask && (reinterpret_cast<uintptr_t>(io->out_mask) & 3))
+        return fail(ctx, BS_ERR_INVALID_ARG, "out_mask must be 4-byte aligned");
+      BS_CUDA(bsk::launch_pack_rows(ctx, io->tokens, *p, (int32_t)io->n, io->out_tokens,
+                                    io->out_mask, io->out_capacity, io->summary, st),
+              "k_pack_rows");
+    }
+    bsk::prof_mark(ctx, 11, st);
+    return BS_OK;
+  }
   BS_CUDA(bsk::launch_window_init(ctx, io->summary, io->n, io->hist,
                                   (int64_t)p->l_max * p->n_classes,
                                   bsk::sort_status_words(ctx, io->n, *p), st),

@@ -55,6 +55,24 @@ __device__ __forceinline__ int32_t eff_cls(uint32_t c, int32_t C, unsigned& fl) 
   return (int32_t)c;
 }
 
+// CPython float floor division (Objects/floatobject.c, _float_div_mod): the operation
+// behind `self.token_budget() // mean_len` in current_n_max (batch_controller.py:104)
+__device__ __forceinline__ double py_floordiv(double vx, double wx) {
+  double mod = fmod(vx, wx);
+  double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
+  if (mod != 0.0) {
+    if ((wx < 0) != (mod < 0)) { mod = __dadd_rn(mod, wx); div = __dsub_rn(div, 1.0); }
+  }
+  double fd;
+  if (div != 0.0) {
+    fd = floor(div);
+    if (__dsub_rn(div, fd) > 0.5) fd = __dadd_rn(fd, 1.0);
+  } else {
+    fd = copysign(0.0, __ddiv_rn(vx, wx));
+  }
+  return fd;
+}
+
 __device__ __forceinline__ void latch_flags(bs_summary* s, unsigned fl) {
   if (fl && s) atomicOr(reinterpret_cast<unsigned long long*>(&s->flags), (unsigned long long)fl);
 }
@@ -137,6 +155,37 @@ __device__ __forceinline__ T block_excl_scan(T v, T* scratch, T* total) {
   *total = scratch[32];
   __syncthreads();
   return r;
+}
+
+// Block-wide exclusive scan of K values per thread with one pair of barriers (instead of
+// K separate scans).  `scratch` needs K * 33 elements of T in shared memory.  v[k] is
+// replaced by its exclusive prefix; total[k] receives the block sum.  All threads call.
+template <int K, typename T>
+__device__ __forceinline__ void block_excl_scan_k(T (&v)[K], T (&total)[K], T* scratch) {
+  const int lane = lane_id(), wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  T incl[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    incl[k] = warp_incl_scan(v[k]);
+    if (lane == 31) scratch[k * 33 + wid] = incl[k];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      T w = lane < nw ? scratch[k * 33 + lane] : T(0);
+      T wi = warp_incl_scan(w);
+      if (lane < nw) scratch[k * 33 + lane] = wi - w;
+      if (lane == nw - 1) scratch[k * 33 + 32] = wi;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k] = scratch[k * 33 + wid] + incl[k] - v[k];
+    total[k] = scratch[k * 33 + 32];
+  }
+  __syncthreads();
 }
 
 }  // namespace bsk

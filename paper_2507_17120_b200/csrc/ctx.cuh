@@ -32,6 +32,9 @@ struct bs_ctx {
   int chain_walk = 0;       // K5c serial-walk limit, 0 = default (BS_CHAIN_WALK)
   int pack_tma_blocks = 0;  // K6 TMA grid: co-resident CTAs per SM x SMs
   int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
+  int small_path = 1;       // K0 single-CTA path for small windows (BS_SMALL=0 disables)
+  int small_smem_max = 0;   // its dynamic shared-memory opt-in (bytes)
+  int small_timing = 0;     // K0 phase timestamps into summary.reserved (BS_SMALL_TIMING)
   bool window_zeroed = false;  // inside a fused window call whose k_window_init zeroed the
                                // accumulators (the launchers then skip their memsets)
   std::string err;
@@ -106,12 +109,21 @@ struct bs_ctx {
   void* nccl_comm = nullptr;         // ncclComm_t
   bool nccl_owned = false;           // created by bs_nccl_connect (destroyed with the ctx)
   int nccl_rank = -1, nccl_world = 0;
+  unsigned char* small_rows = nullptr;  // [kSmallN] K0 -> k_pack_rows copy jobs (SmallRow)
   int32_t* misc = nullptr;       // [128]: [0..63] alive flags per level, [64] M, [65] R_top,
                                  //        [66] n_batches, [67] pack rows cursor, [69] long chains,
                                  //        [70] long-segment count
 };
 
 namespace bsk {
+
+// one admitted row of a small window: the copy job K0 hands to k_pack_rows
+struct SmallRow {
+  int64_t src;    // token-store offset of the request (tok_off)
+  int64_t dst;    // element offset of the row in the packed buffers
+  int32_t x;      // real tokens
+  int32_t pitch;  // row pitch (tokens + padding)
+};
 
 constexpr int kTileX = 4096;  // lengths per K2a tile
 constexpr int kPiece = 2048;  // K6 work unit: at most this many tokens of one row
@@ -219,6 +231,13 @@ int64_t sort_status_words(const bs_ctx* ctx, int64_t n, const bs_window_params& 
 cudaError_t hist_prepare(bs_ctx* ctx);
 cudaError_t bounds_prepare(bs_ctx* ctx);
 cudaError_t pack_prepare(bs_ctx* ctx);
+cudaError_t small_prepare(bs_ctx* ctx);
+bool small_window_ok(const bs_ctx* ctx, int64_t n, const bs_window_params& p, int32_t k_init);
+cudaError_t launch_window_small(bs_ctx* ctx, const bs_window_io* io, const bs_window_params& p,
+                                cudaStream_t st);
+cudaError_t launch_pack_rows(bs_ctx* ctx, const int32_t* tokens, const bs_window_params& p,
+                             int32_t n, int32_t* out_tokens, uint8_t* out_mask,
+                             int64_t out_capacity, bs_summary* summary, cudaStream_t st);
 // nccl_c1.cu (libnccl resolved with dlopen)
 int nccl_status(std::string* why);
 int nccl_unique_id(void* id_out, std::string* why);

@@ -43,23 +43,6 @@ __device__ __forceinline__ int policy_of(const bs_window_params& p, int c) {
   return pol;
 }
 
-// CPython _float_div_mod floor quotient (Objects/floatobject.c)
-__device__ double py_floordiv(double vx, double wx) {
-  double mod = fmod(vx, wx);
-  double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
-  if (mod != 0.0) {
-    if ((wx < 0) != (mod < 0)) { mod = __dadd_rn(mod, wx); div = __dsub_rn(div, 1.0); }
-  }
-  double fd;
-  if (div != 0.0) {
-    fd = floor(div);
-    if (__dsub_rn(div, fd) > 0.5) fd = __dadd_rn(fd, 1.0);
-  } else {
-    fd = copysign(0.0, __ddiv_rn(vx, wx));
-  }
-  return fd;
-}
-
 // ---------------------------------------------------------------------------- K2a
 __global__ void __launch_bounds__(1024)
     k_prefix_tiles(const uint32_t* __restrict__ hist_local, const uint32_t* __restrict__ hist_global,

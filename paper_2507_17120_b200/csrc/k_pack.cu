@@ -478,6 +478,42 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
   if (fl) latch_flags(sum, fl);
 }
 
+// ---------------------------------------------------------------------------------
+// Small windows (K0 path): K0 leaves one copy job per admitted row (source offset,
+// destination offset, length, pitch), so the pack is a single dependent load per row
+// before its vectors stream — one warp per row, no batch search / row-map walk.
+__global__ void __launch_bounds__(256)
+    k_pack_rows(const SmallRow* __restrict__ rows, const int32_t* __restrict__ nrows,
+                const int32_t* __restrict__ tokens, int32_t pad_id,
+                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask,
+                int64_t out_cap, bs_summary* sum) {
+  pdl_prologue();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (sum->packed_elems > out_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
+    return;
+  }
+  const int32_t nr = *nrows;
+  for (int64_t r = w; r < nr; r += nw) {
+    const SmallRow rw = rows[r];
+    copy_row_range<4>(tokens + rw.src, out_tokens + rw.dst, out_mask ? out_mask + rw.dst : nullptr,
+                      rw.x, 0, rw.pitch >> 2, lane, pad_id);
+  }
+}
+
+cudaError_t launch_pack_rows(bs_ctx* ctx, const int32_t* tokens, const bs_window_params& p,
+                             int32_t n, int32_t* out_tokens, uint8_t* out_mask,
+                             int64_t out_capacity, bs_summary* summary, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::max(1, (n + 7) / 8);  // a warp per row
+  launch_k(ctx, k_pack_rows, dim3(blocks), dim3(256), 0, st, false,
+           reinterpret_cast<const SmallRow*>(ctx->small_rows), ctx->misc, tokens, p.pad_id,
+           out_tokens, out_mask, out_capacity, summary);
+  ++ctx->launches;
+  return cudaGetLastError();
+}
+
 // per-context setup on the context's device (bs_create): the dynamic shared-memory
 // opt-in of the TMA kernel and its co-resident CTAs per SM
 cudaError_t pack_prepare(bs_ctx* ctx) {

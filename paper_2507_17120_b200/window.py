@@ -555,6 +555,7 @@ class WindowScheduler:
                 # first packed window: size the reusable output buffer from the plan
                 need = int(self.summary[96:104].cpu().view(torch.int64).item())  # packed_elems
                 self._ensure_pack(max(need, 64))
+            if two_phase and tokens.numel() > 0:  # an empty store: every row is padding-free
                 N.check(lib.bs_pack(self.ctx.ptr, _ptr(lens), _ptr(self.perm), _ptr(tok_off),
                                     _ptr(tokens), C.byref(p), _ptr(self.batches_raw), 0, -1,
                                     _ptr(self.out_tokens), _ptr(self.out_mask),

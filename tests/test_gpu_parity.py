@@ -631,3 +631,76 @@ def _compare_with_oracle_on(spec, lens, cls, dev):
     assert np.array_equal(h["out_tokens"][:m], o.out_tokens[:m])
     assert np.array_equal(h["out_mask"][:m], o.out_mask[:m])
     sched.close()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("BS_SMALL_CONFIGS", "40"))))
+def test_small_window_kernel_equals_multi_kernel_path(seed, monkeypatch):
+    """K0 (one CTA: K1..K5 of windows <= 2048 requests, l_max <= 8192) against the
+    multi-kernel path (BS_SMALL=0) and the oracle on random configurations: every
+    output bit-exact — histogram, edges, change log, bucket ids, drain order, segment
+    offsets, batches (incl. waste, offsets, row bases), outcomes, packed bytes — and the
+    summary's integer fields."""
+    rng = np.random.default_rng(7000 + seed)
+    L = int(rng.choice([2, 7, 64, 100, 1000, 4096, 8192]))
+    C = int(rng.integers(1, max(2, min(8, 16384 // L)) + 1))
+    C = min(C, 8, max(1, 16384 // L))
+    n = int(rng.choice([0, 1, 2, 31, 33, 500, 1000, 2047, 2048, 3000, int(rng.integers(1, 2049))]))
+    pol = tuple(int(v) for v in rng.integers(0, 3, size=C))
+    kvpt = int(rng.choice([2, 6, 524288]))
+    lens = np.clip(np.rint(rng.lognormal(np.log(max(L, 2) / 6) + 0.1, 1.2, size=n)), 0,
+                   L + 5).astype(np.int32)
+    cls = rng.integers(0, C, size=n).astype(np.uint8)
+    budget = int(rng.integers(1, 30 * L + 2))
+    init = None
+    if rng.random() < 0.3 and L > 2:
+        inner = sorted(set(int(v) for v in rng.integers(1, L, size=int(rng.integers(1, 20)))))
+        init = tuple([0] + inner + [L])
+    spec = dict(l_max=L, n_classes=C, policies=pol, theta=float(rng.choice([0.29, 0.5, 0.7, 1.0])),
+                adjust=bool(rng.random() < 0.85), max_passes=int(rng.choice([0, 0, 1, 3])),
+                init_edges=init, kvpt=kvpt,
+                current_safe=kvpt * budget + int(rng.integers(0, kvpt)),
+                pledged=int(rng.choice([0, 0, kvpt * int(rng.integers(0, budget + 1))])),
+                accounting=int(rng.integers(0, 2)), truncate=True)
+    tok_off, tokens = W.token_store(np.minimum(lens, L - 1))
+    dev = torch.device("cuda", 0)
+    outs = []
+    for small in ("1", "0"):
+        monkeypatch.setenv("BS_SMALL", small)
+        s = _sched(spec, max(n, 1))
+        l0 = s.ctx.launches
+        try:
+            res = s.schedule(torch.as_tensor(lens).to(dev), torch.as_tensor(cls).to(dev),
+                             torch.as_tensor(tok_off).to(dev), torch.as_tensor(tokens).to(dev))
+        except (ValueError, ZeroDivisionError) as err:  # the reference's errors, both paths
+            outs.append(type(err))
+            s.close()
+            continue
+        h = res.to_host()
+        h["launches"] = s.ctx.launches - l0
+        outs.append(h)
+        s.close()
+    a, b = outs
+    if isinstance(a, type) or isinstance(b, type):
+        assert a == b
+        return
+    if n <= 2048 and L <= 8192 and C * L <= 16384:
+        assert a["launches"] <= 2, a["launches"]  # K0 (+ K6)
+    for k in ("hist", "edges", "changes", "bucket", "perm", "seg_off", "req_batch", "req_row"):
+        assert np.array_equal(a[k], b[k]), k
+    for f in a["batches"].dtype.names:
+        va, vb = a["batches"][f], b["batches"][f]
+        if f == "waste":
+            va, vb = va.view(np.uint64), vb.view(np.uint64)
+        assert np.array_equal(va, vb), f
+    for f, v in a["summary"].items():
+        if f in ("sort_passes", "waste_sum"):
+            continue
+        assert v == b["summary"][f], f
+    wa, wb = a["summary"]["waste_sum"], b["summary"]["waste_sum"]
+    assert (np.isnan(wa) and np.isnan(wb)) or abs(wa - wb) <= 1e-9 * max(1.0, abs(wb))
+    m = int(a["summary"]["packed_elems"])
+    assert np.array_equal(a["out_tokens"][:m], b["out_tokens"][:m])
+    assert np.array_equal(a["out_mask"][:m], b["out_mask"][:m])
+    o = _oracle(spec, lens, cls, tok_off, tokens)
+    assert np.array_equal(a["perm"], o.perm) and np.array_equal(a["req_batch"], o.req_batch)
+    assert np.array_equal(a["edges"], o.edges) and np.array_equal(a["changes"], o.changes)
