@@ -47,12 +47,12 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _pack_kernel(l_max):
-    """the K6 kernel the library launches by default (k_pack.cu: launch_pack)."""
+def _pack_kernel(l_max, max_n):
+    """the K6 kernel(s) the library launches by default (k_pack.cu: launch_pack)."""
     v = int(os.environ.get("BS_PACK_VARIANT", "0") or 0)
-    if v not in (5, 21):
-        v = 5 if l_max > 16384 else 21
-    return {5: "k_pack_tma", 21: "k_pack_stream"}[v]
+    if v not in (1, 5, 21):
+        v = 1 if max_n <= (4 << 20) else (5 if l_max > 16384 else 21)
+    return {1: "k_pack_bulk", 5: "k_pack_tma", 21: "k_pack_stream"}[v]
 
 
 def _profile_traffic(cfg_name, kernel):
@@ -431,6 +431,7 @@ def main():
 
     # ---------------- pack roofline ------------------------------------------------
     peak, peak_src = _peaks()
+    pk_name = _pack_kernel(cfg.l_max, n)
     admitted = int(s["admitted_tokens"])
     n_adm = n - int(s["n_rejected"]) - int(s["n_pending"])
     # SURVEY §8(d) algorithmic bytes: per admitted request 4*len (tokens) + 8 (offset)
@@ -529,9 +530,10 @@ def main():
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
                   % (tokens.numel() * 4 / 1e9, int(s["packed_elems"]) * 5 / 1e9),
         },
-        "roofline": {"bound": "hbm", "kernel": _pack_kernel(cfg.l_max), "achieved": pack_gbs, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": pk_name + (" (+ k_pack_rowprep)" if pk_name == "k_pack_bulk" else ""),
+                     "achieved": pack_gbs, "peak": peak,
                      "unit": "GB/s", "frac": (pack_gbs / peak) if pack_gbs else None,
-                     "traffic": _profile_traffic(args.config, _pack_kernel(cfg.l_max)), "algorithmic_bytes": pack_bytes,
+                     "traffic": _profile_traffic(args.config, pk_name), "algorithmic_bytes": pack_bytes,
                      "avg_launch_ms": pack_ms, "peak_source": peak_src,
                      "pitch_overhead": {"bytes_moved": pack_bytes_pitch,
                                         "frac_incl_pitch": (pack_bytes_pitch / (pack_ms / 1e3) / 1e9 / peak)

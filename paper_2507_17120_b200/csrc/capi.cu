@@ -80,7 +80,7 @@ void free_all(bs_ctx* c) {
                   c->tile_tot, c->tile_slen, c->tile_carry, c->bmw, c->wp, c->kinfo,
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
                   c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
-                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->task_base, c->segw,
+                  c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->rowdesc, c->chunk_row, c->task_base, c->segw,
                   c->disp_cseg, c->disp_cmin, c->disp_csum, c->disp_keys0, c->disp_keys1,
                   c->disp_vals0, c->disp_vals1, c->disp_hist8, c->disp_agg, c->disp_status, c->disp_tctr, c->disp_nulls, c->disp_runs, c->disp_misc,
                   c->misc, c->small_rows};
@@ -144,6 +144,13 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_CHAIN_CTAS")) ctx->chain_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("BS_CHAIN_WALK")) ctx->chain_walk = std::max(1, atoi(v));
   if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
+  if (const char* v = getenv("BS_PACK_REVERSE")) ctx->pack_reverse = atoi(v) != 0;
+  if (const char* v = getenv("BS_BULK_WARPS")) ctx->pack_bulk_warps = atoi(v) == 8 ? 8 : 16;
+  if (const char* v = getenv("BS_BULK_OPT")) ctx->pack_bulk_opt = atoi(v) & 14;
+  if (const char* v = getenv("BS_PACK_FREE_SMS")) ctx->pack_free_sms = std::max(0, atoi(v));
+  if (const char* v = getenv("BS_PACK_EXCL")) ctx->pack_excl = atoi(v) != 0;
+  ctx->carveout_uniform = max_n <= (4 << 20);
+  if (const char* v = getenv("BS_CARVEOUT")) ctx->carveout_uniform = atoi(v) != 0;
   if (const char* v = getenv("BS_SMALL")) ctx->small_path = atoi(v) != 0;
   if (const char* v = getenv("BS_SMALL_TIMING")) ctx->small_timing = atoi(v) != 0;
   int r = 1;
@@ -190,6 +197,10 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(segw, 7 * (L * C + 1));
   A(rowpos, N + 1);
   A(task_base, N + 2);
+  A(rowdesc, N + 1);
+  // K6 output chunks: one per kPackChunk tokens of the largest packed window
+  ctx->chunk_cap = (N * (((int64_t)L + 31) / 32 * 32) + bsk::kPackChunk - 1) / bsk::kPackChunk + 2;
+  A(chunk_row, ctx->chunk_cap);
   A(misc, 128);
   A(small_rows, 2048 * 32);  // bsk::kSmallN SmallRow records
   // K7 dispatch order

@@ -31,6 +31,16 @@ struct bs_ctx {
   int chain_ctas = 0;       // K5c CTA cap, 0 = one per SM (BS_CHAIN_CTAS)
   int chain_walk = 0;       // K5c serial-walk limit, 0 = default (BS_CHAIN_WALK)
   int pack_tma_blocks = 0;  // K6 TMA grid: co-resident CTAs per SM x SMs
+  int pack_reverse = 1;     // K6 takes its 32-piece groups last batch first (BS_PACK_REVERSE=0: in order)
+  int pack_bulk_blocks = 0; // K6 bulk-staged grid: co-resident CTAs per SM x SMs (pack_prepare)
+  int pack_bulk_warps = 16; // warps per CTA of the bulk-staged pack (BS_BULK_WARPS: 8 | 16)
+  int pack_free_sms = 0;    // SMs the bulk-staged pack leaves to other kernels (BS_PACK_FREE_SMS)
+  int pack_excl = 0;        // bulk-staged pack CTAs claim a whole SM's shared memory (BS_PACK_EXCL)
+  int pack_smem_excl = 0;   //   that request (bytes)
+  int carveout_uniform = 0; // every kernel at the maximum shared-memory carveout (launch_k;
+                            // bs_create: max_n <= 4M, BS_CARVEOUT overrides)
+  int pack_bulk_opt = 2;    // its options (BS_BULK_OPT): bit 1 async row tails, bit 2 register stores, bit 3 contiguous chunk ranges
+  int64_t last_n = 0;       // requests of the last sized window (grid bound of the K6 row prep)
   int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
   int small_path = 1;       // K0 single-CTA path for small windows (BS_SMALL=0 disables)
   int small_smem_max = 0;   // its dynamic shared-memory opt-in (bytes)
@@ -76,6 +86,9 @@ struct bs_ctx {
   int32_t* Rg = nullptr;         // [max_n/32+1] exclusive prefix of bcnt
   int32_t* btot = nullptr;       // [chain_blocks] per-block partials of the Rg scan
   int32_t* rowpos = nullptr;     // [max_n] admitted window row -> drain position (K6)
+  ulonglong2* rowdesc = nullptr; // [max_n] K6 row descriptors {src | x << 40, dst | pitch << 40}
+  int32_t* chunk_row = nullptr;  // [chunk_cap] K6 output chunk -> the row holding its first element
+  int64_t chunk_cap = 0;
   int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
                                  //   <= kPiece tokens; exclusive prefix, K5f)
   int32_t* node_j0 = nullptr;    // [max_n + 1] first admissible position at/after each chain node
@@ -127,6 +140,7 @@ struct SmallRow {
 
 constexpr int kTileX = 4096;  // lengths per K2a tile
 constexpr int kPiece = 2048;  // K6 work unit: at most this many tokens of one row
+constexpr int kPackChunk = 1024;  // K6 bulk-staged pack: output chunk (tokens) per work unit
 // K6 piece size for a window of n requests: kPiece from 64k requests up; smaller windows
 // use proportionally smaller pieces (>= 32 tokens, one 128-byte line) so the pack still
 // spreads over every SM (C1's 1k requests: 32 pieces of 2048 tokens would be 32 warps)
@@ -157,8 +171,18 @@ inline cudaError_t launch_k(const bs_ctx* ctx, void (*kernel)(KArgs...), dim3 gr
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   unsigned na = 0;
+  if (ctx->carveout_uniform) {
+    // every kernel of the window at the maximum shared-memory carveout: an SM only runs
+    // CTAs of one L1 / shared-memory split at a time, so with mixed splits the scheduling
+    // kernels of the windows in flight could not start on an SM beside the (shared-memory
+    // staged) pack of another window.  Windows of up to 4M requests (C2: 0.735 vs 0.759 ms
+    // per window in flight); at 16M (C3) the gather-heavy K5 kernels want their L1 back.
+    at[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    at[na].val.sharedMemCarveout = (unsigned)cudaSharedmemCarveoutMaxShared;
+    ++na;
+  }
   if (cooperative) {
     at[na].id = cudaLaunchAttributeCooperative;
     at[na].val.cooperative = 1;
@@ -174,7 +198,7 @@ inline cudaError_t launch_k(const bs_ctx* ctx, void (*kernel)(KArgs...), dim3 gr
   cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
   if (e != cudaSuccess && cooperative && ctx->pdl) {
     (void)cudaGetLastError();
-    cfg.numAttrs = 1;  // cooperative only
+    cfg.numAttrs = na - 1;  // without PDL (the last attribute)
     e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
   }
   return e;

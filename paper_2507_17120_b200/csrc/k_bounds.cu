@@ -30,7 +30,7 @@ constexpr int kBT = 1024;
 // block of the fused small-L K2 (the code is block-size agnostic; 512 threads measured
 // 41 vs 35 us at C2 and gained nothing with windows in flight)
 constexpr int kSmallBT = 1024;
-constexpr int kSmallBTMin = 1;
+constexpr int kSmallBTMin = 2;  // <= 32 registers: fits on an SM beside a pack CTA of another window
 constexpr int kEcap = 8192;   // edges kept in shared memory when l_max < kEcap
 
 // p.policy[c] without a dynamically indexed kernel-parameter array (which the compiler

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
                   int32_t L, int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
                   int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in,
                   int32_t batches_cap, int32_t* __restrict__ out_tokens,
-                  uint8_t* __restrict__ out_mask, int64_t out_cap, bs_summary* sum, int32_t ptok) {
+                  uint8_t* __restrict__ out_mask, int64_t out_cap, bs_summary* sum, int32_t ptok,
+                  int32_t reverse) {
   pdl_prologue();
   const unsigned FULL = 0xffffffffu;
   int64_t b_end = b_end_arg;
@@ -133,8 +134,13 @@ __global__ void __launch_bounds__(kPackThreads, kMinBlocks)
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int4 pad4 = make_int4(pad_id, pad_id, pad_id, pad_id);
+  const int64_t n_groups = (t1 - t0 + 31) >> 5;
   unsigned fl = 0;
-  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
+  // groups in reverse (last batch first): batches are emitted shortest rows first, so
+  // the groups of the longest rows — the slowest per warp, up to 32 x 2048 tokens — start
+  // first and the kernel's tail is made of short-row groups instead of long ones
+  for (int64_t vg = w; vg < n_groups; vg += nw) {
+    const int64_t gt = t0 + (reverse ? n_groups - 1 - vg : vg) * 32;
     const int64_t t = gt + lane;
     const int32_t* src = nullptr;
     int32_t* dst = nullptr;
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
                int32_t truncate, int32_t pad_id, const bs_batch* __restrict__ batches,
                int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
-               bs_summary* sum, int32_t ptok) {
+               bs_summary* sum, int32_t ptok, int32_t reverse) {
   pdl_prologue();
   extern __shared__ __align__(128) uint8_t tma_smem[];
   __shared__ __align__(8) uint64_t bars[kTmaWarps][kTmaSlots];
@@ -380,7 +386,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
   const int4 pad4 = make_int4(pad_id, pad_id, pad_id, pad_id);
   uint32_t use[kTmaSlots] = {0, 0};
   unsigned fl = 0;
-  for (int64_t gt = t0 + w * 32; gt < t1; gt += nw * 32) {
+  const int64_t n_groups = (t1 - t0 + 31) >> 5;
+  for (int64_t vg = w; vg < n_groups; vg += nw) {  // reverse order: see k_pack_stream
+    const int64_t gt = t0 + (reverse ? n_groups - 1 - vg : vg) * 32;
     const int64_t t = gt + lane;
     PieceMeta my{nullptr, nullptr, nullptr, 0, 0, 0};
     if (t < t1) {
@@ -479,6 +487,410 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
 }
 
 // ---------------------------------------------------------------------------------
+// Bulk-staged pack (default): the packed output of a batch range is one contiguous
+// stream (batches back to back, rows back to back), cut here into chunks of kPackChunk
+// tokens.  A CTA of kW warps stays resident on its SM (persistent grid, one or two CTAs
+// per SM); each warp owns two shared-memory slots and walks its chunks u = warp, warp +
+// all_warps, ...  Per chunk:
+//   issue   the lanes read the descriptors of the chunk's rows (k_pack_rowprep below,
+//           one coalesced 16-byte record per row) into the slot and start one
+//           cp.async.bulk global -> shared per row for the row's real 16-byte token vectors
+//           inside the chunk, placed at the row's offset in the slot's image of the chunk
+//           (completion counted in bytes on the slot's mbarrier);
+//   finish  once the bytes landed: every lane takes 16-token groups of the chunk (a row
+//           starts on a group boundary: pitch % 16 == 0), finds the group's row from the
+//           per-group row-start marks (a warp max-scan), writes the row tail (<= 3 tokens,
+//           scalar loads) and the padding into the image and the group's 16 mask bytes
+//           straight to global (st.global.cs.v4); then one cp.async.bulk shared -> global
+//           stores the whole token image.
+// Bytes in flight per SM are bounded by shared memory (2 x 4 KB of reads per warp, the
+// stores asynchronous too) instead of by registers, with few threads (16 warps x 47
+// registers), so the scheduling kernels of the windows in flight keep SM room beside it.
+// Against the register stream on C2's rows (tools/pack_probe.cu, B200): 0.64-0.65 ms vs
+// 0.69 ms per 1M-request window.  Rows whose tokens are not 16-byte aligned get their
+// vectors from scalar loads in the finish step.
+constexpr uint64_t kLo40 = (1ull << 40) - 1;
+
+struct BulkSlot {
+  int32_t tok[kPackChunk];                 // token image of the chunk
+  ulonglong2 rows[kPackChunk / 16 + 1];    // descriptors of the rows overlapping the chunk
+  uint16_t mark[kPackChunk / 16];          // 1 + local index of the row starting in each group
+};
+
+struct PackRange {
+  int64_t b_begin, b_end, base_off, row_lo, rows, total;
+};
+
+// the range [b_begin, b_end) of a pack call: rows, output elements; false if empty
+__device__ __forceinline__ bool pack_range(const bs_batch* __restrict__ batches, int64_t b_begin,
+                                           int64_t b_end_arg, const bs_summary* sum_in,
+                                           int32_t batches_cap, PackRange& r) {
+  int64_t b_end = b_end_arg;
+  if (b_end < 0) {
+    b_end = sum_in->n_batches;
+    if (b_end > batches_cap) b_end = batches_cap;
+  }
+  if (b_begin >= b_end) return false;
+  const bs_batch first = batches[b_begin];
+  const bs_batch last = batches[b_end - 1];
+  r.b_begin = b_begin;
+  r.b_end = b_end;
+  r.base_off = first.out_offset;
+  r.row_lo = first.row_base;
+  r.rows = last.row_base + last.n - first.row_base;
+  r.total = last.out_offset + (int64_t)last.n * last.pitch - first.out_offset;
+  return true;
+}
+
+// K6a: one descriptor per packed row of the range, {src | x << 40, dst | pitch << 40}
+// (src = token-store offset, x = real tokens, dst = element offset in the range's output),
+// and (strided chunk order) chunk_row[u] = the row holding output element u * kPackChunk
+__global__ void __launch_bounds__(256)
+    k_pack_rowprep(const int32_t* __restrict__ len, const int32_t* __restrict__ perm,
+                   const int32_t* __restrict__ rowpos, const int64_t* __restrict__ tok_off,
+                   int32_t L, int32_t truncate, const bs_batch* __restrict__ batches,
+                   int64_t b_begin, int64_t b_end_arg, const bs_summary* sum_in,
+                   int32_t batches_cap, ulonglong2* __restrict__ desc,
+                   int32_t* __restrict__ chunk_row, int64_t chunk_cap, bs_summary* sum) {
+  pdl_prologue();
+  PackRange R;
+  if (!pack_range(batches, b_begin, b_end_arg, sum_in, batches_cap, R)) return;
+  if (chunk_row && (R.total + kPackChunk - 1) / kPackChunk > chunk_cap) chunk_row = nullptr;
+  unsigned fl = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < R.rows; i += stride) {
+    const int64_t g = R.row_lo + i;
+    int64_t lo = R.b_begin, hi = R.b_end;  // batch of row g: last b with row_base <= g
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (batches[mid].row_base <= g) lo = mid; else hi = mid;
+    }
+    const bs_batch B = batches[lo];
+    const int32_t r = perm[rowpos[g]];
+    const int32_t x = eff_len(len[r], L, truncate, fl);
+    const int64_t dst = B.out_offset - R.base_off + (g - B.row_base) * (int64_t)B.pitch;
+    desc[i] = make_ulonglong2((uint64_t)tok_off[r] | ((uint64_t)x << 40),
+                              (uint64_t)dst | ((uint64_t)B.pitch << 40));
+    if (chunk_row)  // chunk_row[u] = the row holding element u * kPackChunk
+      for (int64_t u = (dst + kPackChunk - 1) / kPackChunk; u * kPackChunk < dst + B.pitch; ++u)
+        chunk_row[u] = (int32_t)i;
+  }
+  if (fl) latch_flags(sum, fl);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// kOpt bit 1: row tails by 4-byte cp.async at issue time (else scalar loads at finish);
+// bit 2: the image goes out through registers (ld.shared + st.global.cs) instead of one
+// bulk shared -> global copy (no wait for the copy to read the slot before its refill)
+template <int kW, int kOpt>
+__global__ void __launch_bounds__(kW * 32)
+    k_pack_bulk(const ulonglong2* __restrict__ desc, const int32_t* __restrict__ chunk_row,
+                int64_t chunk_cap, const int32_t* __restrict__ tokens,
+                int32_t pad_id, const bs_batch* __restrict__ batches, int64_t b_begin,
+                int64_t b_end_arg, const bs_summary* sum_in, int32_t batches_cap,
+                int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
+                bs_summary* sum) {
+  pdl_prologue();
+  constexpr int kS = 2;
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  __shared__ __align__(8) uint64_t bars[kW][kS];
+  constexpr int T = kPackChunk;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  PackRange R;
+  if (!pack_range(batches, b_begin, b_end_arg, sum_in, batches_cap, R)) return;
+  const int64_t n_chunks = (R.total + T - 1) / T;
+  constexpr bool kContig = (kOpt & 8) != 0;
+  if (R.total > out_cap || (!kContig && n_chunks > chunk_cap)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
+    return;
+  }
+  // chunk k of this warp: strided (default) u = warp + k * all_warps, so the warps in
+  // flight write neighbouring chunks (DRAM page locality of the output stream; the first
+  // row of each chunk from chunk_row), or with kOpt & 8 a contiguous range of chunks (the
+  // rows of chunk u + 1 continue where chunk u's left off; only the range start is searched)
+  const int64_t nw = (int64_t)gridDim.x * kW;
+  const int64_t gw = (int64_t)blockIdx.x * kW + wib;
+  const int64_t cpw = (n_chunks + nw - 1) / nw;
+  const int64_t u_begin = kContig ? gw * cpw : gw;
+  const int64_t k_end = min(u_begin + cpw, n_chunks);
+  const int64_t K = kContig ? (k_end > u_begin ? k_end - u_begin : 0)
+                            : (gw < n_chunks ? (n_chunks - gw + nw - 1) / nw : 0);
+  if (K == 0) return;
+  auto chunk = [&](int64_t k) { return kContig ? u_begin + k : gw + k * nw; };
+  BulkSlot* slots = reinterpret_cast<BulkSlot*>(bulk_smem) + wib * kS;
+  uint64_t* bar = bars[wib];
+  if (lane == 0) {
+    for (int s = 0; s < kS; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t n_rows = R.rows;
+  auto load_desc = [&](int64_t g) {
+    return g >= 0 && g < n_rows ? desc[g] : make_ulonglong2(0, 0);
+  };
+
+  // issue chunk u into slot s from row g0 (d_first = the descriptors of rows g0 + lane):
+  // descriptors into the slot, one bulk copy per row for its 16-byte token vectors inside
+  // the chunk and, with kOpt & 2, the row tail (x % 4 tokens) by 4-byte cp.async.
+  // Returns the first row of chunk u + 1.
+  auto issue = [&](int s, int64_t u, int64_t g0, ulonglong2 d_first) -> int64_t {
+    BulkSlot& S = slots[s];
+    const int64_t c0 = u * T, c1 = min(c0 + T, R.total);
+    for (int i = lane; i < T / 32; i += 32) reinterpret_cast<uint32_t*>(S.mark)[i] = 0u;
+    if (kOpt & 4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    int nin = 0;  // rows of the chunk so far (rows of pitch 0 hold no output and are skipped)
+    int64_t g_next = g0;
+    for (int64_t base = g0;; base += 32) {
+      const int64_t g = base + lane;
+      const ulonglong2 d = base == g0 ? d_first : load_desc(g);
+      const int64_t dst = (int64_t)(d.y & kLo40);
+      const int32_t pitch = (int32_t)(d.y >> 40);
+      const bool reach = g < n_rows && dst < c1;
+      const bool in = reach && pitch > 0;
+      const unsigned bal = __ballot_sync(FULL, in);
+      uint32_t bytes = 0;
+      const int64_t lo = max(dst, c0);
+      const int32_t* row = tokens + (int64_t)(d.x & kLo40);
+      const int32_t* src = row + (lo - dst);
+      const bool al = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+      if (in) {
+        const int li = nin + __popc(bal & lanemask_lt());
+        S.rows[li] = d;
+        S.mark[(lo - c0) >> 4] = (uint16_t)(li + 1);
+        const int32_t x = (int32_t)(d.x >> 40);
+        const int64_t hi = min(dst + x, c1);
+        if (hi > lo && al) {
+          bytes = (uint32_t)((hi - lo) & ~3ll) * 4u;
+          if ((kOpt & 2) && hi == dst + x)  // the row ends here: its tail, asynchronously
+            for (int32_t e = x & ~3; e < x; ++e)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                               smem_addr(S.tok + (dst + e - c0))),
+                           "l"(row + e)
+                           : "memory");
+        }
+      }
+      const uint32_t tx = warp_sum(bytes);
+      if (lane == 0 && tx)
+        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                         smem_addr(&bar[s])),
+                     "r"(tx)
+                     : "memory");
+      __syncwarp();
+      if (bytes)
+        asm volatile(
+            "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(smem_addr(S.tok + (lo - c0))),
+            "l"(src), "r"(bytes), "r"(smem_addr(&bar[s]))
+            : "memory");
+      nin += __popc(bal);
+      const unsigned rb = __ballot_sync(FULL, reach);
+      if (rb) {  // the last row reaching into the chunk: the next chunk starts on it or after it
+        const int hl = 31 - __clz(rb);
+        const int64_t e = __shfl_sync(FULL, dst + pitch, hl);
+        g_next = base + hl + (e > c1 ? 0 : 1);
+      }
+      if (rb != FULL || !__shfl_sync(FULL, dst + pitch < c1, 31)) break;
+    }
+    if (kOpt & 2) asm volatile("cp.async.commit_group;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&bar[s])) : "memory");
+    return g_next;
+  };
+
+  // finish: wait for the chunk's bytes, add tails / padding / mask, store the image
+  auto finish = [&](int s, int64_t u, uint32_t parity) {
+    BulkSlot& S = slots[s];
+    const int64_t c0 = u * T, c1 = min(c0 + T, R.total);
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(&bar[s])),
+        "r"(parity)
+        : "memory");
+    // this lane's tail copies of the chunk: one cp.async group is committed per chunk in
+    // order, so the younger group (chunk u + 1) may stay pending
+    if (kOpt & 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    constexpr int kG = T / 16 / 32;  // 16-token groups per lane (contiguous)
+    uint16_t mk[kG];
+    int run = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      mk[j] = S.mark[lane * kG + j];
+      run = max(run, (int)mk[j]);
+    }
+    int incl = run;  // warp inclusive max-scan: the row holding each lane's first group
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl = max(incl, y);
+    }
+    int cur = __shfl_up_sync(FULL, incl, 1);
+    cur = lane == 0 ? 1 : max(cur, 1);
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      cur = max(cur, (int)mk[j]);
+      const int m = lane * kG + j;
+      const int64_t p = c0 + 16 * (int64_t)m;
+      if (p >= c1) continue;
+      const ulonglong2 d = S.rows[cur - 1];
+      const int32_t x = (int32_t)(d.x >> 40);
+      const int32_t o = (int32_t)(p - (int64_t)(d.y & kLo40));  // column of the group
+      if (out_mask)
+        st_stream_v4(reinterpret_cast<int4*>(out_mask + p),
+                     make_int4((int)mask_word(x - o), (int)mask_word(x - o - 4),
+                               (int)mask_word(x - o - 8), (int)mask_word(x - o - 12)));
+      const int32_t* sp = tokens + (int64_t)(d.x & kLo40);
+      const bool al = (reinterpret_cast<uintptr_t>(sp) & 15) == 0;
+      const int32_t f4 = al ? (x & ~3) : 0;  // columns below f4 arrived by the bulk copy
+      if (o + 16 > f4) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int32_t q = o + 4 * v;
+          if (q + 4 <= f4) continue;
+          int4* slot4 = reinterpret_cast<int4*>(S.tok + 16 * m + 4 * v);
+          int4 r4 = make_int4(pad_id, pad_id, pad_id, pad_id);
+          if (q < x) {
+            if ((kOpt & 2) && al) {  // the tail vector: tokens below x arrived by cp.async
+              const int4 t = *slot4;
+              r4.x = t.x;
+              if (q + 1 < x) r4.y = t.y;
+              if (q + 2 < x) r4.z = t.z;
+            } else {
+              r4.x = sp[q];
+              if (q + 1 < x) r4.y = sp[q + 1];
+              if (q + 2 < x) r4.z = sp[q + 2];
+              if (q + 3 < x) r4.w = sp[q + 3];
+            }
+          }
+          *slot4 = r4;
+        }
+      }
+    }
+    if (kOpt & 4) {  // through registers: the slot is free when the warp is done with it
+      __syncwarp();
+      const int4* img = reinterpret_cast<const int4*>(S.tok);
+      int4* o4 = reinterpret_cast<int4*>(out_tokens + c0);
+      const int nv = (int)(c1 - c0) >> 2;
+      for (int v = lane; v < nv; v += 32) st_stream_v4(o4 + v, img[v]);
+      __syncwarp();
+    } else {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out_tokens + c0),
+                     "r"(smem_addr(S.tok)), "r"((uint32_t)(c1 - c0) * 4u)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  };
+
+  auto row_of = [&](int64_t k) -> int64_t {  // strided: first row of chunk k
+    return k < K ? (int64_t)chunk_row[chunk(k)] : -1;
+  };
+  int64_t g0;
+  if (kContig) {  // first row of the range: the last row with dst <= u_begin * T (32-ary search)
+    const int64_t c = u_begin * T;
+    int64_t lo = 0, hi = n_rows;
+    while (hi - lo > 1) {
+      const int64_t step = (hi - lo + 31) >> 5;
+      const int64_t idx = lo + (lane + 1) * step;
+      const bool le = idx < hi && (int64_t)(desc[idx].y & kLo40) <= c;
+      lo += (int64_t)__popc(__ballot_sync(FULL, le)) * step;
+      hi = min(hi, lo + step);
+    }
+    g0 = lo;
+  } else {
+    g0 = row_of(0);
+  }
+  // prologue: both slots in flight.  The first row of chunk k + 2 (and, strided, of k + 3)
+  // and the descriptors of chunk k + 2 are loaded an iteration ahead of their use, so the
+  // dependent metadata loads overlap the finish of chunk k.
+  int64_t g = issue(0, chunk(0), g0, load_desc(g0 + lane));
+  if (K > 1) {
+    const int64_t g1 = kContig ? g : row_of(1);
+    g = issue(1, chunk(1), g1, load_desc(g1 + lane));
+  } else if (kOpt & 2) {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int64_t nx_g = kContig ? g : row_of(2);
+  ulonglong2 nx_d = K > 2 ? load_desc(nx_g + lane) : make_ulonglong2(0, 0);
+  int64_t nx2_g = kContig ? -1 : row_of(3);
+#pragma unroll 1
+  for (int64_t k = 0; k < K; ++k) {
+    const int s = (int)(k & 1);
+    finish(s, chunk(k), (uint32_t)((k >> 1) & 1));
+    if (k + 2 < K) {  // refill the slot (once its store has read the image)
+      if (!(kOpt & 4) && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      g = issue(s, chunk(k + 2), nx_g, nx_d);
+      if (kContig) {
+        nx_g = g;
+      } else {
+        nx_g = nx2_g;
+        nx2_g = row_of(k + 4);
+      }
+      nx_d = k + 3 < K ? load_desc(nx_g + lane) : make_ulonglong2(0, 0);
+    } else if (kOpt & 2) {
+      asm volatile("cp.async.commit_group;" ::: "memory");  // (empty) group of chunk k + 2
+    }
+  }
+  if (kOpt & 2) asm volatile("cp.async.wait_all;" ::: "memory");
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int kW>
+static size_t bulk_smem() { return sizeof(BulkSlot) * kW * 2; }
+
+// kOpt (BS_BULK_OPT): bit 1 async row tails, bit 2 register stores, bit 3 contiguous
+// chunk ranges per warp (see k_pack_bulk)
+template <int kW>
+static auto bulk_kernel(int opt) {
+  switch (opt & 14) {
+    case 0: return k_pack_bulk<kW, 0>;
+    case 2: return k_pack_bulk<kW, 2>;
+    case 4: return k_pack_bulk<kW, 4>;
+    case 6: return k_pack_bulk<kW, 6>;
+    case 8: return k_pack_bulk<kW, 8>;
+    case 10: return k_pack_bulk<kW, 10>;
+    case 12: return k_pack_bulk<kW, 12>;
+    default: return k_pack_bulk<kW, 14>;
+  }
+}
+
+template <int kW>
+static cudaError_t launch_pack_bulk(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
+                                    const int64_t* tok_off, const int32_t* tokens,
+                                    const bs_window_params& p, const bs_batch* batches,
+                                    int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
+                                    int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
+                                    bs_summary* summary, cudaStream_t st) {
+  const int64_t rows_ub = ctx->last_n > 0 ? ctx->last_n : ctx->max_n;
+  const unsigned pblocks =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_ub + 255) / 256, 8LL * ctx->num_sms));
+  launch_k(ctx, k_pack_rowprep, dim3(pblocks), dim3(256), 0, st, false, len, perm, ctx->rowpos,
+           tok_off, p.l_max, p.truncate, batches, batch_begin, batch_end, summary, batches_cap,
+           ctx->rowdesc, (ctx->pack_bulk_opt & 8) ? nullptr : ctx->chunk_row, ctx->chunk_cap,
+           summary);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  launch_k(ctx, bulk_kernel<kW>(ctx->pack_bulk_opt), dim3((unsigned)ctx->pack_bulk_blocks),
+           dim3(kW * 32), ctx->pack_excl ? (size_t)ctx->pack_smem_excl : bulk_smem<kW>(), st, false, ctx->rowdesc, ctx->chunk_row, ctx->chunk_cap,
+           tokens, p.pad_id, batches,
+           batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
+           summary);
+  ctx->launches += 2;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
 // Small windows (K0 path): K0 leaves one copy job per admitted row (source offset,
 // destination offset, length, pitch), so the pack is a single dependent load per row
 // before its vectors stream — one warp per row, no batch search / row-map walk.
@@ -524,6 +936,24 @@ cudaError_t pack_prepare(bs_ctx* ctx) {
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_tma, kTmaWarps * 32, smem);
   if (e != cudaSuccess) return e;
   ctx->pack_tma_blocks = std::max(1, per_sm) * ctx->num_sms;
+  // bulk-staged pack: 16 warps x 2 slots (~168 KB, one CTA per SM) or 8 warps (two per SM)
+  const bool w8 = ctx->pack_bulk_warps == 8;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  if (e != cudaSuccess) return e;
+  ctx->pack_smem_excl = optin - 1024;  // static mbarriers
+  const size_t bsm = ctx->pack_excl ? (size_t)ctx->pack_smem_excl : (w8 ? bulk_smem<8>() : bulk_smem<16>());
+  for (int opt = 0; opt < 16; opt += 2) {
+    e = w8 ? cudaFuncSetAttribute(bulk_kernel<8>(opt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)
+           : cudaFuncSetAttribute(bulk_kernel<16>(opt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    if (e != cudaSuccess) return e;
+  }
+  per_sm = 0;
+  e = w8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk_kernel<8>(ctx->pack_bulk_opt), 8 * 32, bsm)
+         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk_kernel<16>(ctx->pack_bulk_opt), 16 * 32, bsm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  ctx->pack_bulk_blocks = per_sm * std::max(1, ctx->num_sms - ctx->pack_free_sms);
   return cudaSuccess;
 }
 
@@ -537,7 +967,7 @@ static cudaError_t launch_pack_tma(bs_ctx* ctx, const int32_t* len, const int32_
   launch_k(ctx, k_pack_tma, dim3((unsigned)ctx->pack_tma_blocks), dim3(kTmaWarps * 32), smem, st, false, 
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary, ctx->piece_tok);
+      summary, ctx->piece_tok, (int32_t)ctx->pack_reverse);
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -557,7 +987,7 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
   launch_k(ctx, k_pack_stream<kU, kMinB, kUni>, dim3((unsigned)blocks), dim3(kPackThreads), 0, st, false, 
       len, perm, ctx->rowpos, ctx->task_base, tok_off, tokens, p.l_max, p.truncate, p.pad_id,
       batches, batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
-      summary, ctx->piece_tok);
+      summary, ctx->piece_tok, (int32_t)ctx->pack_reverse);
   ++ctx->launches;
   return cudaGetLastError();
 }
@@ -576,7 +1006,20 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   // bit-identical.  The slower forms measured in round 1 (per-row k_pack, persistent
   // grids, a cp.async shared-memory ring, 8 vectors per lane) are recorded in DESIGN.md.
   int v = ctx->pack_variant;
-  if (v != 5 && v != 21) v = p.l_max > 16384 ? 5 : 21;
+  // the bulk-staged pack (default) stores 16-byte mask words and whole 16-byte chunk images
+  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(out_tokens) | reinterpret_cast<uintptr_t>(out_mask)) & 15) == 0;
+  // default: the bulk-staged pack for contexts of up to 4M requests (C2 0.74 vs 0.79 ms per
+  // window in flight, C4 6.35 vs 6.50 ms); above (C3's 16M) the register stream (13.36 vs
+  // 13.60 ms).  BS_PACK_VARIANT: 1 = bulk-staged, 5 = TMA-staged, 21 = register stream.
+  if (v != 1 && v != 5 && v != 21)
+    v = (bulk_ok && ctx->max_n <= (4 << 20)) ? 1 : (p.l_max > 16384 ? 5 : 21);
+  if (v == 1 && !bulk_ok) v = p.l_max > 16384 ? 5 : 21;
+  if (v == 1)
+    return ctx->pack_bulk_warps == 8
+               ? launch_pack_bulk<8>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
+                                     batches_cap, out_tokens, out_mask, out_capacity, summary, st)
+               : launch_pack_bulk<16>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
+                                      batches_cap, out_tokens, out_mask, out_capacity, summary, st);
   if (v == 5)
     return launch_pack_tma(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
                            batches_cap, out_tokens, out_mask, out_capacity, summary, st);

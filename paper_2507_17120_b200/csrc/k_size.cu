@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------- K5f
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(512)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
                    const int32_t* __restrict__ misc, int64_t* __restrict__ task_base,
                    bs_summary* sum, int32_t ptok) {
@@ -975,8 +975,9 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                                            batches_cap, summary, ctx->sorted_keys, ctx->slot_seg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   ctx->piece_tok = piece_tokens_for(n);
+  ctx->last_n = n;
   ctx->pack_pieces = n * (((int64_t)p.l_max + ctx->piece_tok - 1) / ctx->piece_tok);
-  launch_k(ctx, k_size_offsets, dim3(1), dim3(1024), 0, st, false, batches, batches_cap, misc, ctx->task_base, summary,
+  launch_k(ctx, k_size_offsets, dim3(1), dim3(512), 0, st, false, batches, batches_cap, misc, ctx->task_base, summary,
                                      ctx->piece_tok);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 8, st);

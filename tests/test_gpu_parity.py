@@ -372,14 +372,23 @@ def test_sharded_window_on_one_gpu(world):
         s.close()
 
 
-PACK_VARIANTS = [5, 21]
+# K6 kernels: "0" bulk-staged (default: 16 warps per CTA, async row tails, bulk stores;
+# "0w8": 8 warps, two CTAs per SM; "0oK": BS_BULK_OPT=K), 5 = TMA-staged register
+# stores, 21 = register stream
+PACK_VARIANTS = ["0", "0w8", "0o0", "0o4", "0o6", "5", "21"]
+
+
+def _set_variant(monkeypatch, variant):
+    monkeypatch.setenv("BS_PACK_VARIANT", "1" if variant.startswith("0") else variant)
+    monkeypatch.setenv("BS_BULK_WARPS", "8" if variant == "0w8" else "16")
+    monkeypatch.setenv("BS_BULK_OPT", variant[2:] if variant.startswith("0o") else "2")
 
 
 @pytest.mark.parametrize("variant", PACK_VARIANTS)
 def test_pack_variants_bit_exact(variant, monkeypatch):
-    """Both K6 kernels (TMA staging, register stream; BS_PACK_VARIANT forces one) pack
-    the same bytes, each on the other's default window shape too."""
-    monkeypatch.setenv("BS_PACK_VARIANT", str(variant))
+    """Every K6 kernel (bulk-staged, TMA-staged, register stream; BS_PACK_VARIANT forces
+    one) packs the same bytes as the oracle, on each other's default window shape too."""
+    _set_variant(monkeypatch, variant)
     cfg, lens, cls = W.make_window("c4", n=3_000, seed=2)
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
     cfg, lens, cls = W.make_window("c2", n=50_000, seed=2)
@@ -391,7 +400,7 @@ def test_pack_variants_bit_exact(variant, monkeypatch):
 def test_pack_token_store_alignment(variant, align, monkeypatch):
     """Token rows at any int32 offset (a dense CSR store, align 1) pack the same bytes as
     the oracle: rows whose source is not 16-byte aligned take the scalar path."""
-    monkeypatch.setenv("BS_PACK_VARIANT", str(variant))
+    _set_variant(monkeypatch, variant)
     cfg, lens, cls = W.make_window("c2", n=20_000, seed=5)
     spec = _cfg_spec(cfg)
     tok_off, tokens = W.token_store(lens, align=align, seed=7)
@@ -684,7 +693,7 @@ def test_small_window_kernel_equals_multi_kernel_path(seed, monkeypatch):
         assert a == b
         return
     if n <= 2048 and L <= 8192 and C * L <= 16384:
-        assert a["launches"] <= 2, a["launches"]  # K0 (+ K6)
+        assert a["launches"] <= 3, a["launches"]  # K0 (+ K6: row prep + pack)
     for k in ("hist", "edges", "changes", "bucket", "perm", "seg_off", "req_batch", "req_row"):
         assert np.array_equal(a[k], b[k]), k
     for f in a["batches"].dtype.names:
