@@ -504,8 +504,13 @@ static int window_from_hist_impl(bs_ctx* ctx, const bs_window_io* io, const bs_w
   BS_CUDA(bsk::launch_order(ctx, io->len, io->cls, io->n, *p, io->perm, io->bucket, io->summary, st),
           "k_sort_pass");
   bsk::prof_mark(ctx, 4, st);
+  // the bulk-staged pack reads one record per row: K5e writes them when it has the token
+  // offsets (the pack of this call then skips k_pack_rowprep)
+  const bool recs = io->tok_off && io->tokens && io->out_tokens && io->n > 0 &&
+                    bsk::pack_uses_bulk(ctx, *p, io->out_tokens, io->out_mask);
   BS_CUDA(bsk::launch_size(ctx, io->len, io->perm, io->seg_off, io->n, *p, io->batches,
-                           io->batches_cap, io->req_batch, io->req_row, io->summary, st),
+                           io->batches_cap, io->req_batch, io->req_row, io->summary, st,
+                           recs ? io->tok_off : nullptr),
           "k_size");
   bsk::prof_mark(ctx, 9, st);
   if (p->dispatch) {

@@ -89,6 +89,7 @@ struct bs_ctx {
   ulonglong2* rowdesc = nullptr; // [max_n] K6 row descriptors {src | x << 40, dst | pitch << 40}
   int32_t* chunk_row = nullptr;  // [chunk_cap] K6 output chunk -> the row holding its first element
   int64_t chunk_cap = 0;
+  bool rowdesc_ready = false;    // K5e of the window just sized wrote rowdesc / chunk_row
   int64_t* task_base = nullptr;  // [max_n + 1] K6 pieces before each batch (row pieces of
                                  //   <= kPiece tokens; exclusive prefix, K5f)
   int32_t* node_j0 = nullptr;    // [max_n + 1] first admissible position at/after each chain node
@@ -226,7 +227,11 @@ cudaError_t launch_order(bs_ctx* ctx, const int32_t* len, const uint8_t* cls, in
 cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const int32_t* seg_off, int64_t n, const bs_window_params& p,
                         bs_batch* batches, int32_t batches_cap, int32_t* req_batch,
-                        int32_t* req_row, bs_summary* summary, cudaStream_t st);
+                        int32_t* req_row, bs_summary* summary, cudaStream_t st,
+                        const int64_t* tok_off = nullptr);
+// would launch_pack use the bulk-staged pack (row records written by K5e when it does)
+bool pack_uses_bulk(const bs_ctx* ctx, const bs_window_params& p, const int32_t* out_tokens,
+                    const uint8_t* out_mask);
 cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const int64_t* tok_off, const int32_t* tokens, const bs_window_params& p,
                         const bs_batch* batches, int64_t batch_begin, int64_t batch_end,

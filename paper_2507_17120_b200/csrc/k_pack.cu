@@ -872,21 +872,26 @@ static cudaError_t launch_pack_bulk(bs_ctx* ctx, const int32_t* len, const int32
                                     int64_t batch_begin, int64_t batch_end, int32_t batches_cap,
                                     int32_t* out_tokens, uint8_t* out_mask, int64_t out_capacity,
                                     bs_summary* summary, cudaStream_t st) {
-  const int64_t rows_ub = ctx->last_n > 0 ? ctx->last_n : ctx->max_n;
-  const unsigned pblocks =
-      (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_ub + 255) / 256, 8LL * ctx->num_sms));
-  launch_k(ctx, k_pack_rowprep, dim3(pblocks), dim3(256), 0, st, false, len, perm, ctx->rowpos,
-           tok_off, p.l_max, p.truncate, batches, batch_begin, batch_end, summary, batches_cap,
-           ctx->rowdesc, (ctx->pack_bulk_opt & 8) ? nullptr : ctx->chunk_row, ctx->chunk_cap,
-           summary);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  const bool ready = ctx->rowdesc_ready && batch_begin == 0 && batch_end < 0;
+  ctx->rowdesc_ready = false;
+  cudaError_t e;
+  if (!ready) {  // records of the range (K5e writes them for a whole window it sized)
+    const int64_t rows_ub = ctx->last_n > 0 ? ctx->last_n : ctx->max_n;
+    const unsigned pblocks =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_ub + 255) / 256, 8LL * ctx->num_sms));
+    launch_k(ctx, k_pack_rowprep, dim3(pblocks), dim3(256), 0, st, false, len, perm, ctx->rowpos,
+             tok_off, p.l_max, p.truncate, batches, batch_begin, batch_end, summary, batches_cap,
+             ctx->rowdesc, (ctx->pack_bulk_opt & 8) ? nullptr : ctx->chunk_row, ctx->chunk_cap,
+             summary);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++ctx->launches;
+  }
   launch_k(ctx, bulk_kernel<kW>(ctx->pack_bulk_opt), dim3((unsigned)ctx->pack_bulk_blocks),
            dim3(kW * 32), ctx->pack_excl ? (size_t)ctx->pack_smem_excl : bulk_smem<kW>(), st, false, ctx->rowdesc, ctx->chunk_row, ctx->chunk_cap,
            tokens, p.pad_id, batches,
            batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
            summary);
-  ctx->launches += 2;
+  ++ctx->launches;
   return cudaGetLastError();
 }
 
@@ -992,6 +997,27 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
   return cudaGetLastError();
 }
 
+// K6 kernel for a pack call: 1 = bulk-staged, 5 = TMA-staged, 21 = register stream.
+// Default: the bulk-staged pack for contexts of up to 4M requests (C2 0.74 vs 0.79 ms per
+// window in flight, C4 6.35 vs 6.50 ms); above (C3's 16M) the register stream (13.36 vs
+// 13.60 ms).  BS_PACK_VARIANT forces one.  The bulk-staged pack stores 16-byte mask words
+// and whole 16-byte chunk images, so it needs 16-byte aligned outputs.
+static int pack_kernel_choice(const bs_ctx* ctx, const bs_window_params& p,
+                              const int32_t* out_tokens, const uint8_t* out_mask) {
+  const bool bulk_ok =
+      ((reinterpret_cast<uintptr_t>(out_tokens) | reinterpret_cast<uintptr_t>(out_mask)) & 15) == 0;
+  int v = ctx->pack_variant;
+  if (v != 1 && v != 5 && v != 21)
+    v = (bulk_ok && ctx->max_n <= (4 << 20)) ? 1 : (p.l_max > 16384 ? 5 : 21);
+  if (v == 1 && !bulk_ok) v = p.l_max > 16384 ? 5 : 21;
+  return v;
+}
+
+bool pack_uses_bulk(const bs_ctx* ctx, const bs_window_params& p, const int32_t* out_tokens,
+                    const uint8_t* out_mask) {
+  return pack_kernel_choice(ctx, p, out_tokens, out_mask) == 1;
+}
+
 cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const int64_t* tok_off, const int32_t* tokens, const bs_window_params& p,
                         const bs_batch* batches, int64_t batch_begin, int64_t batch_end,
@@ -1005,15 +1031,7 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   // (BS_PACK_VARIANT at bs_create) forces one: 5 = TMA, 21 = register stream; both are
   // bit-identical.  The slower forms measured in round 1 (per-row k_pack, persistent
   // grids, a cp.async shared-memory ring, 8 vectors per lane) are recorded in DESIGN.md.
-  int v = ctx->pack_variant;
-  // the bulk-staged pack (default) stores 16-byte mask words and whole 16-byte chunk images
-  const bool bulk_ok = ((reinterpret_cast<uintptr_t>(out_tokens) | reinterpret_cast<uintptr_t>(out_mask)) & 15) == 0;
-  // default: the bulk-staged pack for contexts of up to 4M requests (C2 0.74 vs 0.79 ms per
-  // window in flight, C4 6.35 vs 6.50 ms); above (C3's 16M) the register stream (13.36 vs
-  // 13.60 ms).  BS_PACK_VARIANT: 1 = bulk-staged, 5 = TMA-staged, 21 = register stream.
-  if (v != 1 && v != 5 && v != 21)
-    v = (bulk_ok && ctx->max_n <= (4 << 20)) ? 1 : (p.l_max > 16384 ? 5 : 21);
-  if (v == 1 && !bulk_ok) v = p.l_max > 16384 ? 5 : 21;
+  const int v = pack_kernel_choice(ctx, p, out_tokens, out_mask);
   if (v == 1)
     return ctx->pack_bulk_warps == 8
                ? launch_pack_bulk<8>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,

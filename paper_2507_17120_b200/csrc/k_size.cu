@@ -730,7 +730,9 @@ __global__ void __launch_bounds__(256)
                    int32_t* __restrict__ req_batch, int32_t* __restrict__ req_row,
                    int32_t* __restrict__ rowpos, bs_summary* sum,
                    const int32_t* __restrict__ slen, int32_t* __restrict__ dmin,
-                   int64_t* __restrict__ dsum, int32_t r_lo, int32_t r_hi, int first) {
+                   int64_t* __restrict__ dsum, int32_t r_lo, int32_t r_hi, int first,
+                   const int64_t* __restrict__ tok_off, ulonglong2* __restrict__ rowdesc,
+                   int32_t* __restrict__ chunk_row) {
   pdl_prologue();
   const int M = misc[64];
   const int32_t* list = misc[68] ? listB : listA;
@@ -792,8 +794,18 @@ __global__ void __launch_bounds__(256)
           req_batch[r] = b;
           req_row[r] = Rj - Rc;
         }
-        if (first && b < batches_cap)
-          rowpos[batches[b].row_base + (Rj - Rc)] = (int32_t)j;  // K6 row map
+        if (first && b < batches_cap) {
+          const bs_batch& B = batches[b];
+          const int64_t g = B.row_base + (Rj - Rc);
+          rowpos[g] = (int32_t)j;  // K6 row map
+          if (rowdesc) {  // the bulk-staged K6 reads one record per row (k_pack_rowprep's)
+            const int64_t dst = B.out_offset + (int64_t)(Rj - Rc) * B.pitch;
+            rowdesc[g] = make_ulonglong2((uint64_t)tok_off[r] | ((uint64_t)slen[j] << 40),
+                                         (uint64_t)dst | ((uint64_t)B.pitch << 40));
+            for (int64_t u = (dst + kPackChunk - 1) / kPackChunk; u * kPackChunk < dst + B.pitch; ++u)
+              chunk_row[u] = (int32_t)g;
+          }
+        }
       } else {
         if (mine) {
           req_batch[r] = BS_REQ_REJECTED;
@@ -891,8 +903,10 @@ __global__ void k_fill_pending(int64_t n, int32_t* req_batch, int32_t* req_row, 
 cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const int32_t* seg_off, int64_t n, const bs_window_params& p,
                         bs_batch* batches, int32_t batches_cap, int32_t* req_batch,
-                        int32_t* req_row, bs_summary* summary, cudaStream_t st) {
+                        int32_t* req_row, bs_summary* summary, cudaStream_t st,
+                        const int64_t* tok_off) {
   cudaError_t e;
+  ctx->rowdesc_ready = false;
   const int64_t H = p.current_safe - p.pledged;
   if (n == 0 || H <= 0)
     for (int s = 5; s <= 8; ++s) prof_mark(ctx, s, st);
@@ -995,8 +1009,11 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
         batches, batches_cap, req_batch, req_row, ctx->rowpos, summary, ctx->sorted_len,
         p.dispatch ? ctx->disp_cmin : nullptr, p.dispatch ? ctx->disp_csum : nullptr,
         (int32_t)std::min<int64_t>(n, q * span), (int32_t)std::min<int64_t>(n, (q + 1) * span),
-        q == 0);
+        q == 0, tok_off, tok_off ? ctx->rowdesc : nullptr, ctx->chunk_row);
   }
+  // with the token offsets, K5e wrote the bulk-staged pack's row records for the whole
+  // window (the fused path then skips k_pack_rowprep)
+  ctx->rowdesc_ready = tok_off != nullptr;
   ctx->launches += 5 + parts;
   return cudaGetLastError();
 }
