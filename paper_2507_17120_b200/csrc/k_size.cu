@@ -206,7 +206,58 @@ __global__ void __launch_bounds__(256)
     //        admissible j0 and admits floor(T / slen[j0]) requests.
     int fast = 0;
     int32_t fast_nx = kEnd;
-    if (valid && a.padded) {
+    // whole warp inside one SJF segment, every start admissible (x <= min(S, T)): with
+    // A(k) = k - floor(T / slen[k]) (+inf for an oversize k), strictly increasing along
+    // the segment, a call from j stops at the first k with A(k) >= j (slen[k] (k - j + 1)
+    // > T  <=>  j <= A(k)).  So next(j0) by one warp-cooperative 32-ary search, and the 32
+    // starts' stops all lie in the 32 positions from there: one load + a shuffle search
+    // per lane instead of an exponential + binary search per lane
+    const int64_t seg_l0 = __shfl_sync(FULL, seg_c, 0);
+    const bool sjf_lane = valid && a.padded && seg_c == seg_l0 &&
+                          ((a.sjf_mask >> (int)(seg_c % a.C)) & 1) && (int64_t)x <= a.S &&
+                          (int64_t)x <= a.T;
+    if (__all_sync(FULL, sjf_lane)) {
+      const int64_t j0 = g << 5;
+      int64_t lo = j0 + 1, hi = e;  // first k in [lo, e) bad for j0 (hi: e or a bad k)
+      while (lo < hi) {
+        const int64_t step = (hi - lo + 31) >> 5;
+        const int64_t q = lo + lane * step;
+        bool bd = false;
+        if (q < hi) {
+          const int64_t y = slen[q];
+          bd = y > a.S || y * (q - j0 + 1) > a.T;
+        }
+        const unsigned bm = __ballot_sync(FULL, bd);
+        if (bm) {
+          const int f = __ffs(bm) - 1;
+          hi = lo + f * step;
+          lo = f ? lo + (f - 1) * step + 1 : lo;
+        } else {
+          const int64_t span_q = (hi - 1 - lo) / step;
+          const int64_t last = span_q < 31 ? span_q : 31;
+          lo = lo + last * step + 1;
+        }
+      }
+      const int64_t k0 = lo;
+      const int64_t kk = k0 + lane;
+      int64_t A = INT64_MAX;  // past the segment or oversize: every start stops there
+      if (kk < e) {
+        const int64_t y = slen[kk];
+        if (y <= a.S) A = y > 0 ? kk - a.T / y : INT64_MIN;
+      }
+      int lo2 = 0, hi2 = 32;  // first lane i with A_i >= j
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int mid = (lo2 + hi2) >> 1;
+        const int64_t am = __shfl_sync(FULL, A, mid < 31 ? mid : 31);
+        if (lo2 < hi2) {
+          if (am >= j) hi2 = mid; else lo2 = mid + 1;
+        }
+      }
+      const int64_t a_idx = __shfl_sync(FULL, A, lo2 < 31 ? lo2 : 31);
+      fast = 1;
+      fast_nx = (lo2 < 32 && a_idx != INT64_MAX) ? (int32_t)(k0 + lo2) : kEnd;
+    } else if (valid && a.padded) {
       const int c = (int)(seg_c % a.C);
       if ((a.sjf_mask >> c) & 1) {
         fast = 1;
@@ -732,7 +783,7 @@ __global__ void __launch_bounds__(256)
                    const int32_t* __restrict__ slen, int32_t* __restrict__ dmin,
                    int64_t* __restrict__ dsum, int32_t r_lo, int32_t r_hi, int first,
                    const int64_t* __restrict__ tok_off, ulonglong2* __restrict__ rowdesc,
-                   int32_t* __restrict__ chunk_row) {
+                   int32_t* __restrict__ chunk_row, int2* __restrict__ pos_out) {
   pdl_prologue();
   const int M = misc[64];
   const int32_t* list = misc[68] ? listB : listA;
@@ -784,7 +835,9 @@ __global__ void __launch_bounds__(256)
     // large windows run this kernel once per request-id range, so each pass's scattered
     // outcome writes stay inside L2 and fill whole sectors (no DRAM read-modify-write);
     // the position-ordered row map and the counters are written by the first pass
-    const bool mine = r >= r_lo && r < r_hi;
+    // with pos_out (large windows) the outcomes go out in drain order, sequentially, and
+    // k_outcome_scatter moves them to request ids in L2-sized ranges afterwards
+    const bool mine = !pos_out && r >= r_lo && r < r_hi;
     if (b >= 0) {
       if (nr) {
         const int64_t gc = c >> 5;
@@ -794,6 +847,7 @@ __global__ void __launch_bounds__(256)
           req_batch[r] = b;
           req_row[r] = Rj - Rc;
         }
+        if (pos_out) pos_out[j] = make_int2(b, Rj - Rc);
         if (first && b < batches_cap) {
           const bs_batch& B = batches[b];
           const int64_t g = B.row_base + (Rj - Rc);
@@ -811,6 +865,7 @@ __global__ void __launch_bounds__(256)
           req_batch[r] = BS_REQ_REJECTED;
           req_row[r] = -1;
         }
+        if (pos_out) pos_out[j] = make_int2(BS_REQ_REJECTED, -1);
         rej += first;
       }
     } else {  // a segment's empty tail: rejected up to the first admissible request, pending after
@@ -819,6 +874,7 @@ __global__ void __launch_bounds__(256)
         req_row[r] = -1;
         req_batch[r] = j < j0 ? BS_REQ_REJECTED : BS_REQ_PENDING;
       }
+      if (pos_out) pos_out[j] = make_int2(j < j0 ? BS_REQ_REJECTED : BS_REQ_PENDING, -1);
       if (j < j0) rej += first; else pend += first;
     }
   }
@@ -830,46 +886,67 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// K5e' (windows whose outcome arrays exceed 32 MB): drain-order outcomes -> request ids,
+// one request-id range per launch, so each pass's scattered writes fill whole sectors in
+// L2 instead of read-modify-writing DRAM; the reads (perm, outcomes) are sequential
+__global__ void __launch_bounds__(256)
+    k_outcome_scatter(int64_t n, const int32_t* __restrict__ perm, const int2* __restrict__ pos_out,
+                      int32_t r_lo, int32_t r_hi, int32_t* __restrict__ req_batch,
+                      int32_t* __restrict__ req_row) {
+  pdl_prologue();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    const int32_t r = perm[j];
+    if (r >= r_lo && r < r_hi) {
+      const int2 o = pos_out[j];
+      req_batch[r] = o.x;
+      req_row[r] = o.y;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------- K5f
+// one CTA; every thread owns a contiguous run of batches: a local pass for its sums, one
+// block scan of the three running offsets, a second pass writing them (C3's 25k batches:
+// one block scan instead of 49)
 __global__ void __launch_bounds__(512)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
                    const int32_t* __restrict__ misc, int64_t* __restrict__ task_base,
                    bs_summary* sum, int32_t ptok) {
   pdl_prologue();
-  __shared__ int64_t s_l[33];
+  __shared__ int64_t s_sc[3 * 33];
   __shared__ double s_d[32];
   __shared__ int64_t s_a[32], s_p[32], s_pk[32];
   const int nb = min(misc[66], batches_cap);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  int64_t run = 0, rrun = 0, trun = 0, adm = 0, pad = 0, peak = 0;
+  const int per = (nb + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int i0 = min(nb, tid * per), i1 = min(nb, i0 + per);
+  int64_t v[3] = {0, 0, 0};  // packed elements, rows, K6 pieces
+  int64_t adm = 0, pad = 0, peak = 0;
   double ws = 0.0;
-  for (int base = 0; base < nb; base += blockDim.x) {
-    const int i = base + tid;
-    int64_t v = 0, rows = 0, tasks = 0;
-    if (i < nb) {
-      rows = batches[i].n;
-      tasks = rows * ((batches[i].pitch + ptok - 1) / ptok);
-      const bs_batch& B = batches[i];
-      v = (int64_t)B.n * B.pitch;
-      adm += B.token_sum;
-      pad += (int64_t)B.n * B.max_input_len;
-      peak = B.footprint > peak ? B.footprint : peak;
-      ws += B.waste;
-    }
-    int64_t tot, rtot, ttot;
-    const int64_t off = block_excl_scan<int64_t>(v, s_l, &tot);
-    const int64_t roff = block_excl_scan<int64_t>(rows, s_l, &rtot);
-    const int64_t toff = block_excl_scan<int64_t>(tasks, s_l, &ttot);
-    if (i < nb) {
-      batches[i].out_offset = run + off;
-      batches[i].row_base = rrun + roff;
-      task_base[i] = trun + toff;
-    }
-    run += tot;
-    rrun += rtot;
-    trun += ttot;
+  for (int i = i0; i < i1; ++i) {
+    const bs_batch& B = batches[i];
+    v[0] += (int64_t)B.n * B.pitch;
+    v[1] += B.n;
+    v[2] += (int64_t)B.n * ((B.pitch + ptok - 1) / ptok);
+    adm += B.token_sum;
+    pad += (int64_t)B.n * B.max_input_len;
+    peak = B.footprint > peak ? B.footprint : peak;
+    ws += B.waste;
   }
-  if (tid == 0) task_base[nb] = trun;
+  int64_t tot[3];
+  block_excl_scan_k<3, int64_t>(v, tot, s_sc);
+  int64_t run = v[0], rrun = v[1], trun = v[2];
+  for (int i = i0; i < i1; ++i) {
+    bs_batch& B = batches[i];
+    B.out_offset = run;
+    B.row_base = rrun;
+    task_base[i] = trun;
+    run += (int64_t)B.n * B.pitch;
+    rrun += B.n;
+    trun += (int64_t)B.n * ((B.pitch + ptok - 1) / ptok);
+  }
+  if (tid == 0) task_base[nb] = tot[2];
   adm = warp_sum(adm);
   pad = warp_sum(pad);
   peak = warp_max(peak);
@@ -884,7 +961,7 @@ __global__ void __launch_bounds__(512)
     }
     sum->admitted_tokens = A;
     sum->padded_tokens = Pd;
-    sum->packed_elems = run;
+    sum->packed_elems = tot[0];
     sum->peak_footprint = Pk;
     sum->waste_sum = Ws;
   }
@@ -1003,13 +1080,26 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   const int parts = parts_env ? parts_env
                               : (int)std::max<int64_t>(1, (n * 8 + (32LL << 20) - 1) / (32LL << 20));
   const int64_t span = (n + parts - 1) / parts;
-  for (int q = 0; q < parts; ++q) {
-    launch_k(ctx, k_size_outcome, dim3(wblocks), dim3(256), 0, st, false, 
+  // more than one range: K5e runs once and writes the outcomes in drain order (into the
+  // doubling table's levels >= 1, free after K5c), k_outcome_scatter moves each range
+  int2* pos_out =
+      parts > 1 && ctx->r_cap >= 4 ? reinterpret_cast<int2*>(ctx->J + ((n + 1) & ~1LL)) : nullptr;
+  const int passes = pos_out ? 1 : parts;
+  for (int q = 0; q < passes; ++q) {
+    launch_k(ctx, k_size_outcome, dim3(wblocks), dim3(256), 0, st, false,
         a, perm, ctx->bmask, ctx->Rg, ctx->listA, ctx->listB, ctx->node_batch, ctx->node_j0, misc,
         batches, batches_cap, req_batch, req_row, ctx->rowpos, summary, ctx->sorted_len,
         p.dispatch ? ctx->disp_cmin : nullptr, p.dispatch ? ctx->disp_csum : nullptr,
         (int32_t)std::min<int64_t>(n, q * span), (int32_t)std::min<int64_t>(n, (q + 1) * span),
-        q == 0, tok_off, tok_off ? ctx->rowdesc : nullptr, ctx->chunk_row);
+        q == 0, tok_off, tok_off ? ctx->rowdesc : nullptr, ctx->chunk_row, pos_out);
+  }
+  if (pos_out) {
+    const unsigned sblocks = (unsigned)std::min<int64_t>((n + 255) / 256, 8LL * ctx->num_sms);
+    for (int q = 0; q < parts; ++q)
+      launch_k(ctx, k_outcome_scatter, dim3(sblocks), dim3(256), 0, st, false, n, perm,
+               (const int2*)pos_out, (int32_t)std::min<int64_t>(n, q * span),
+               (int32_t)std::min<int64_t>(n, (q + 1) * span), req_batch, req_row);
+    ctx->launches += 1;  // parts scatters + one K5e instead of parts K5e
   }
   // with the token offsets, K5e wrote the bulk-staged pack's row records for the whole
   // window (the fused path then skips k_pack_rowprep)
