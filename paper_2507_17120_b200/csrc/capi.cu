@@ -11,8 +11,6 @@
 
 #include "ctx.cuh"
 
-void* bs_chain_kernel_ptr(int wide);  // k_size.cu
-int bs_chain_threads(int wide);
 void* bs_dispatch_kernel_ptr();  // k_dispatch.cu
 
 namespace {
@@ -79,7 +77,7 @@ void free_all(bs_ctx* c) {
   void* ptrs[] = {c->P, c->PcL, c->E, c->lut, c->seg_base, c->seg_off, c->slot_lut, c->slot_seg, c->slot_len, c->bins_cnt,
                   c->tile_tot, c->tile_slen, c->tile_carry, c->bmw, c->wp, c->kinfo,
                   c->keysA, c->keysB, c->valsA, c->valsB, c->status, c->tile_ctr, c->sorted_len,
-                  c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->btot, c->J,
+                  c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->rg_tiles, c->J,
                   c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->rowdesc, c->chunk_row, c->task_base, c->segw,
                   c->disp_cseg, c->disp_cmin, c->disp_csum, c->disp_keys0, c->disp_keys1,
                   c->disp_vals0, c->disp_vals1, c->disp_hist8, c->disp_agg, c->disp_status, c->disp_tctr, c->disp_nulls, c->disp_runs, c->disp_misc,
@@ -136,12 +134,10 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* v = getenv("BS_PACK_VARIANT")) ctx->pack_variant = atoi(v);
   if (const char* v = getenv("BS_HIST_AGG")) ctx->hist_agg = atoi(v);
-  if (const char* v = getenv("BS_CHAIN_WIDE")) ctx->chain_wide = atoi(v);
   ctx->hist_maxb = 2 * ctx->num_sms;
   if (const char* v = getenv("BS_HIST_EPT")) ctx->hist_ept = std::max(1, atoi(v));
   if (const char* v = getenv("BS_HIST_MAXB")) ctx->hist_maxb = std::max(1, atoi(v));
   if (const char* v = getenv("BS_SORT_ITEMS")) ctx->sort_items = atoi(v);
-  if (const char* v = getenv("BS_CHAIN_CTAS")) ctx->chain_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("BS_CHAIN_WALK")) ctx->chain_walk = std::max(1, atoi(v));
   if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
   if (const char* v = getenv("BS_PACK_REVERSE")) ctx->pack_reverse = atoi(v) != 0;
@@ -215,22 +211,9 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
     delete ctx;
     return rc;
   }
-  // co-resident blocks for the cooperative chain kernel
+  // K5c: per-tile admissible counts and their prefix (Rg tiles of 8192 groups)
+  A(rg_tiles, 2 * (groups / 8192 + 2));
   int per_sm = 0;
-  for (int wide = 0; wide < 2 && e == cudaSuccess; ++wide) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_chain_kernel_ptr(wide),
-                                                      bs_chain_threads(wide), 0);
-    if (e == cudaSuccess && per_sm < 1) break;
-  }
-  if (e != cudaSuccess || per_sm < 1) {
-    int rc = e != cudaSuccess ? cuda_fail(ctx, e, "occupancy(k_chain)")
-                              : fail(ctx, BS_ERR_NOT_BUILT, "k_chain cannot be resident");
-    free_all(ctx);
-    delete ctx;
-    return rc;
-  }
-  ctx->chain_blocks = ctx->num_sms;  // one CTA per SM (per_sm >= 1 checked above)
-  A(btot, ctx->chain_blocks);
   // the cooperative K7 dispatch kernel: one 1024-thread CTA per SM, ~211 KB of shared memory
   e = cudaFuncSetAttribute(bs_dispatch_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            bsk::dispatch_smem_bytes());

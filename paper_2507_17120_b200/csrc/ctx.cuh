@@ -15,20 +15,17 @@ struct bs_ctx {
   int32_t c_max = 0;
   int r_cap = 0;            // doubling levels stored for the K5 chain
   int64_t max_tiles = 0;    // K4 tiles per pass
-  int chain_blocks = 0;     // co-resident blocks of the cooperative chain kernel
   int64_t scratch_bytes = 0;
   int64_t launches = 0;     // kernels launched through this ctx
   int pack_variant = 0;     // K6 tuning variant (env BS_PACK_VARIANT)
   int hist_agg = 0;         // K1: 1 = warp-aggregated shared atomics (env BS_HIST_AGG)
   int32_t piece_tok = 2048;  // K6 piece size of the last sized window (piece_tokens_for)
   int64_t pack_pieces = 0;   // upper bound on its K6 pieces: n * ceil(l_max / piece_tok)
-  int chain_wide = -1;      // K5c: -1 = by window size, 0/1 = 512/1024 threads (env BS_CHAIN_WIDE)
   // tuning hooks, read from the environment once per context by bs_create (per-device
   // state such as shared-memory opt-ins and occupancy lives here too, not in statics)
   int hist_ept = 4;         // K1 elements per thread (BS_HIST_EPT)
   int hist_maxb = 0;        // K1 CTA cap (BS_HIST_MAXB; default 2 per SM)
   int sort_items = 0;       // K4 keys per thread: 0 = by window size, 8 | 16 (BS_SORT_ITEMS)
-  int chain_ctas = 0;       // K5c CTA cap, 0 = one per SM (BS_CHAIN_CTAS)
   int chain_walk = 0;       // K5c serial-walk limit, 0 = default (BS_CHAIN_WALK)
   int pack_tma_blocks = 0;  // K6 TMA grid: co-resident CTAs per SM x SMs
   int pack_reverse = 1;     // K6 takes its 32-piece groups last batch first (BS_PACK_REVERSE=0: in order)
@@ -84,7 +81,7 @@ struct bs_ctx {
   int32_t* bmin = nullptr;       //   non-rejected length min
   uint32_t* bmask = nullptr;     //   bit l: position 32g+l is admissible (len <= S)
   int32_t* Rg = nullptr;         // [max_n/32+1] exclusive prefix of bcnt
-  int32_t* btot = nullptr;       // [chain_blocks] per-block partials of the Rg scan
+  int32_t* rg_tiles = nullptr;   // [2][groups/8192+2] K5c Rg tile sums, then their prefix
   int32_t* rowpos = nullptr;     // [max_n] admitted window row -> drain position (K6)
   ulonglong2* rowdesc = nullptr; // [max_n] K6 row descriptors {src | x << 40, dst | pitch << 40}
   int32_t* chunk_row = nullptr;  // [chunk_cap] K6 output chunk -> the row holding its first element

@@ -20,13 +20,11 @@
 //                  32 group summaries per step (shuffle scans + per-lane binary
 //                  search), then <= 32 element steps per lane.  Work per start is
 //                  O(1 + span/1024) warp steps instead of O(span/32) serial loads.
-//   K5c  chain     one cooperative kernel (one 1024-thread CTA per SM): group-count
-//                  prefix scan; every segment's chain next(next(...)) followed serially
-//                  by one thread for up to kWalk calls (dependent L2 hits, C2's longest
-//                  chain is 75 calls); only when some chain is longer: pointer doubling
-//                  J[r] = next^(2^r) (grid.sync per level) and binary lifting for those
-//                  segments; then every chain node (= batch start) is materialised in
-//                  emission order in parallel.
+//   K5c  chain     the chain next(next(...)) of every segment = its form_batch calls:
+//                  one thread per segment walks up to kWalk calls (C2's longest chain is
+//                  75), one CTA per longer segment doubles pointers over its positions
+//                  only, then node / batch bases and every chain node in emission order
+//                  (four plain kernels, no grid barrier, no cooperative launch)
 //   K5d  describe  one warp per batch: n / sum / max / min from group summaries
 //   K5f  offsets   one CTA: packed-buffer offsets (scan of n*pitch), row bases, totals
 //   K5e  outcome   one warp per 32 positions: batch id / row / rejected / pending,
@@ -50,7 +48,8 @@ struct SizeArgs {
   int32_t C;         // classes (segment s holds class s % C)
   int32_t sjf_mask;  // bit c: class c drains SJF (lengths ascending in its segments)
   int32_t ljf_mask;  // bit c: class c drains LJF (lengths descending)
-  int32_t walk;      // K5c: chain calls followed serially before pointer doubling is used
+  int32_t walk;      // K5c: chain calls followed serially before doubling is considered
+  int32_t walk_forced;  // (tuning / test hook) hand every longer chain to doubling
 };
 
 struct Stat {
@@ -440,185 +439,158 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------- K5c
-// one CTA per SM (fewer CTAs per grid barrier).  Windows up to kChainWide requests use
-// 512 threads capped at 40 registers: the CTA needs only a third of an SM, so it starts
-// as soon as a few pack CTAs of the previous window in flight retire (two windows in
-// flight: 0.858 vs 0.905 ms per C2 window).  Larger windows (C3: 16M) use 1024 threads,
-// whose extra loads in flight the pointer-doubling levels need (C3 chain 0.93 vs 1.65 ms).
-constexpr int kChainWide = 4 << 20;
-constexpr int kWalk = 128;           // chain calls followed serially before doubling is used
-
-struct ChainShared {
-  int32_t si[33];
-  int32_t flag;
-};
+// The chain of every segment, next(next(...)) from its start, is the sequence of its
+// form_batch calls.  Four plain (non-cooperative) kernels, so no launch waits for a whole
+// GPU to be free beside the pack of another window in flight:
+//   walk   one thread per segment follows its chain for up to `walk` calls (dependent L2
+//          hits; C2's longest chain is 75 calls) into listB; longer segments are listed;
+//          extra CTAs sum the admissible counts of 8192-group tiles (for Rg)
+//   long   one 1024-thread CTA per listed segment: pointer doubling J[r+1] = J[r][J[r]]
+//          over the segment's positions only (__syncthreads per level, no grid barrier)
+//          until the start's 2^r-th successor is past the segment, then binary lifting
+//          for the chain length and last node
+//   bases  one CTA: node / batch bases per segment, the window's totals, the tile prefix
+//   nodes  every chain node (= batch start) in emission order; extra CTAs finish Rg
+// K5c walk policy.  A segment's chain is followed serially (one dependent L2 hit per call,
+// ~0.25 us) for kWalk calls; if it goes on, the walk estimates the remaining calls from the
+// positions consumed so far and keeps walking (up to kWalkMax calls) only while that is
+// cheaper than one CTA doubling pointers over the whole segment (~0.19 ns per position and
+// level): C3's first bucket (576 calls of ~3k requests over 1.4M positions) is walked in
+// ~0.1 ms where doubling would take ~2.4 ms, C4's long-context tail (1,591 calls of ~8
+// requests over 12.7k positions) is doubled in ~30 us instead of walked in ~0.35 ms.
+constexpr int kWalk = 64;
+constexpr int kWalkMax = 16384;
+constexpr int kRgTile = 8192;        // 32-position groups per Rg tile (256 threads x 32)
 
 __device__ __forceinline__ int32_t ld_rel_i32(const int32_t* p) {
   return (int32_t)ld_relaxed(reinterpret_cast<const uint32_t*>(p));
 }
 
-template <int kThreads, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-    k_chain(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
-            int32_t* J, int r_cap, const uint8_t* __restrict__ is_start, int32_t* alive,
-            int32_t* listA, int32_t* listB, int32_t* node_batch, int32_t* node_j0, int32_t* misc,
-            const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
-            const int32_t* __restrict__ bcnt, int32_t* __restrict__ Rg, int32_t* btot,
-            int32_t* segw, int32_t batches_cap, bs_summary* sum, int32_t* dseg, int32_t* dmin,
-            int64_t* dsum) {
+struct SegArrays {
+  int32_t *len, *empty, *tailj0, *nbase, *ebase, *lvl, *long_list;
+};
+__device__ __forceinline__ SegArrays seg_arrays(int32_t* segw, int32_t n_segs) {
+  const int64_t w = n_segs + 1;
+  return SegArrays{segw, segw + w, segw + 2 * w, segw + 3 * w, segw + 4 * w, segw + 5 * w,
+                   segw + 6 * w};
+}
+
+__global__ void __launch_bounds__(256)
+    k_chain_walk(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
+                 const int32_t* __restrict__ J0, int32_t* __restrict__ listB,
+                 const int32_t* __restrict__ slen, const uint32_t* __restrict__ bmask,
+                 const int32_t* __restrict__ bcnt, int32_t* __restrict__ segw,
+                 int32_t* __restrict__ misc, int32_t* __restrict__ tile_sum, int32_t n_tiles) {
   pdl_prologue();
-  cg::grid_group grid = cg::this_grid();
-  __shared__ ChainShared sh;
-  const int64_t n = a.n;
-  const int32_t n_segs = kinfo[2];
-  const int tid = threadIdx.x, bt = blockDim.x;
-  int32_t* seg_len = segw;
-  int32_t* seg_empty = segw + (n_segs + 1);
-  int32_t* seg_tailj0 = segw + 2 * (n_segs + 1);
-  int32_t* seg_nbase = segw + 3 * (n_segs + 1);
-  int32_t* seg_ebase = segw + 4 * (n_segs + 1);
-  int32_t* seg_long = segw + 5 * (n_segs + 1);
-  int32_t* long_list = segw + 6 * (n_segs + 1);
-  // ---- phase 0: Rg = exclusive prefix of admissible counts per 32-position group ----
-  const int64_t G = (n + 31) >> 5;
-  const int64_t per = (G + gridDim.x - 1) / gridDim.x;
-  const int64_t g0 = (int64_t)blockIdx.x * per;
-  const int64_t g1 = g0 + per < G ? g0 + per : G;
-  {
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x < n_tiles) {  // admissible count of one Rg tile
+    const int64_t G = (a.n + 31) >> 5;
+    const int64_t g0 = (int64_t)blockIdx.x * kRgTile;
+    const int64_t g1 = g0 + kRgTile < G ? g0 + kRgTile : G;
     int32_t loc = 0;
-    for (int64_t g = g0 + tid; g < g1; g += bt) loc += bcnt[g];
-    int32_t tot;
-    block_excl_scan<int32_t>(loc, sh.si, &tot);
-    if (tid == 0) btot[blockIdx.x] = tot;
-  }
-  // ---- phase W: follow every segment's chain next(next(...)) for up to kWalk calls,
-  // one thread per segment (dependent L2 hits: ~kWalk x 130 ns); nodes land in listB
-  // at seg_off[s] + k.  Only segments with longer chains need pointer doubling.
-  {
-    bool any_long = false;
-    for (int64_t sg = (int64_t)blockIdx.x * bt + tid; sg < n_segs; sg += (int64_t)gridDim.x * bt) {
-      const int64_t st = seg_off[sg], en = seg_off[sg + 1];
-      int32_t len = 0, empty = 0, tj0 = 0, lng = 0;
-      if (st < en) {
-        int64_t pos = st;
-        int32_t k = 0;
-        listB[st] = (int32_t)st;
-        for (;;) {
-          const int32_t y = J[pos];
-          if (y == kEnd) break;
-          if (++k >= a.walk) { lng = 1; break; }
-          listB[st + k] = y;
-          pos = y;
-        }
-        if (!lng) {
-          len = k + 1;
-          const int64_t j0 = first_nonrej(pos, en, bmask);
-          empty = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
-          tj0 = (int32_t)j0;
-        }
-      }
-      seg_len[sg] = len;
-      seg_empty[sg] = empty;
-      seg_tailj0[sg] = tj0;
-      seg_long[sg] = lng;
-      if (lng) {  // compact list of the long segments: doubling only touches their positions
-        const int32_t idx = atomicAdd(misc + 70, 1);
-        if (idx <= n_segs) long_list[idx] = (int32_t)sg;
-      }
-      any_long |= lng != 0;
+    for (int64_t g = g0 + tid; g < g1; g += blockDim.x) loc += bcnt[g];
+    loc = warp_sum(loc);
+    __shared__ int32_t s_w[8];
+    if ((tid & 31) == 0) s_w[tid >> 5] = loc;
+    __syncthreads();
+    if (tid == 0) {
+      int32_t t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+      tile_sum[blockIdx.x] = t;
     }
-    if (any_long) misc[69] = 1;
+    return;
   }
-  grid.sync();
-  {
-    int32_t pre = 0;
-    for (int b = tid; b < (int)blockIdx.x; b += bt) pre += ld_rel_i32(btot + b);
-    int32_t off;
-    block_excl_scan<int32_t>(pre, sh.si, &off);
-    int32_t run = off;
-    for (int64_t base = g0; base < g1; base += bt) {
-      const int64_t g = base + tid;
-      const int32_t v = g < g1 ? bcnt[g] : 0;
-      int32_t t;
-      const int32_t o = block_excl_scan<int32_t>(v, sh.si, &t);
-      if (g < g1) Rg[g] = run + o;
-      run += t;
+  const int32_t n_segs = kinfo[2];
+  const SegArrays S = seg_arrays(segw, n_segs);
+  const int64_t sg = (int64_t)(blockIdx.x - n_tiles) * blockDim.x + tid;
+  if (sg >= n_segs) return;
+  const int64_t st = seg_off[sg], en = seg_off[sg + 1];
+  int32_t len = 0, empty = 0, tj0 = 0, lng = 0;
+  if (st < en) {
+    int64_t pos = st;
+    int32_t k = 0;
+    listB[st] = (int32_t)st;
+    int32_t limit = a.walk;
+    for (;;) {
+      const int32_t y = J0[pos];
+      if (y == kEnd) break;
+      if (++k >= limit) {
+        if (a.walk_forced || k >= kWalkMax) { lng = 1; break; }
+        // remaining calls at the average call size so far vs levels x positions
+        const double avg = (double)(pos - st + 1) / (double)k;
+        const double rest = (double)(en - pos) / avg;
+        const double walk_us = rest * 0.25;
+        const double dbl_us = 10.0 + (double)(en - st) * (log2(rest + k) + 1.0) * 1.9e-4;
+        if (walk_us > dbl_us) { lng = 1; break; }
+        limit = kWalkMax;
+      }
+      listB[st + k] = y;
+      pos = y;
+    }
+    if (!lng) {
+      len = k + 1;
+      const int64_t j0 = first_nonrej(pos, en, bmask);
+      empty = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
+      tj0 = (int32_t)j0;
     }
   }
-  int r = 0;
-  const bool need_doubling = ld_rel_i32(misc + 69) != 0;
-  if (need_doubling) {
-    // ---- phase 1: pointer doubling over the positions of the long segments ---------------
-    // (chain successors stay inside their segment, so the other segments' entries of
-    // J[r >= 1] are never read); every CTA maps a virtual index onto the long segments
-    // through a shared-memory prefix of their sizes (all positions beyond kMaxLong)
-    constexpr int kMaxLong = 256;
-    __shared__ int32_t s_lseg[kMaxLong];
-    __shared__ int64_t s_lpre[kMaxLong + 1];
-    const int32_t n_long = ld_rel_i32(misc + 70);
-    const bool listed = n_long <= kMaxLong;
-    int64_t span = n;
-    if (listed) {
-      int64_t sz = 0;
-      if (tid < n_long) {
-        const int32_t sg = ld_rel_i32(long_list + tid);
-        s_lseg[tid] = sg;
-        sz = (int64_t)seg_off[sg + 1] - seg_off[sg];
-      }
-      __shared__ int64_t s_sc[33];
-      int64_t tot;
-      const int64_t o = block_excl_scan<int64_t>(tid < kMaxLong ? sz : 0, s_sc, &tot);
-      if (tid < kMaxLong) s_lpre[tid] = o;
-      if (tid == 0) s_lpre[kMaxLong] = tot;
-      __syncthreads();
-      span = tot;
-    }
-    auto position = [&](int64_t v) -> int64_t {
-      if (!listed) return v;
-      int lo = 0, hi = n_long;  // last i with s_lpre[i] <= v
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_lpre[mid] <= v) lo = mid; else hi = mid;
-      }
-      return (int64_t)seg_off[s_lseg[lo]] + (v - s_lpre[lo]);
-    };
-    while (r + 1 < r_cap && ld_rel_i32(alive + r)) {
+  S.len[sg] = len;
+  S.empty[sg] = empty;
+  S.tailj0[sg] = tj0;
+  S.lvl[sg] = 0;
+  if (lng) {
+    const int32_t idx = atomicAdd(misc + 70, 1);
+    if (idx <= n_segs) S.long_list[idx] = (int32_t)sg;
+  }
+}
+
+__global__ void __launch_bounds__(1024, 2)
+    k_chain_long(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
+                 int32_t* J, int r_cap, const int32_t* __restrict__ slen,
+                 const uint32_t* __restrict__ bmask, int32_t* __restrict__ segw,
+                 const int32_t* __restrict__ misc, bs_summary* sum) {
+  pdl_prologue();
+  const int32_t n_segs = kinfo[2];
+  const SegArrays S = seg_arrays(segw, n_segs);
+  const int32_t n_long = misc[70];
+  const int64_t n = a.n;
+  __shared__ int s_more;
+  for (int32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
+    const int32_t sg = S.long_list[li];
+    const int64_t st = seg_off[sg], en = seg_off[sg + 1];
+    int r = 0;
+    if (threadIdx.x == 0) s_more = 1;
+    __syncthreads();
+    for (;;) {  // level r + 1 over the segment's positions (successors stay inside it)
+      if (r + 1 >= r_cap) break;
       const int32_t* Jr = J + (int64_t)r * n;
       int32_t* Jn = J + (int64_t)(r + 1) * n;
-      bool any = false;
-      // kIlp independent positions per thread in flight (the second load is a gather)
       constexpr int kIlp = 4;
-      const int64_t S = (int64_t)gridDim.x * blockDim.x;
-      for (int64_t x0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < span;
-           x0 += kIlp * S) {
+      const int64_t span = en - st;
+      for (int64_t x0 = threadIdx.x; x0 < span; x0 += kIlp * (int64_t)blockDim.x) {
         int32_t v[kIlp];
-        int64_t xs[kIlp];
 #pragma unroll
         for (int k = 0; k < kIlp; ++k) {
-          const int64_t q = x0 + k * S;
-          xs[k] = q < span ? position(q) : -1;
-          v[k] = xs[k] >= 0 ? Jr[xs[k]] : kEnd;
+          const int64_t q = x0 + k * (int64_t)blockDim.x;
+          v[k] = q < span ? Jr[st + q] : kEnd;
         }
 #pragma unroll
         for (int k = 0; k < kIlp; ++k) v[k] = v[k] == kEnd ? kEnd : Jr[v[k]];
 #pragma unroll
         for (int k = 0; k < kIlp; ++k) {
-          if (xs[k] >= 0) {
-            Jn[xs[k]] = v[k];
-            if (v[k] != kEnd && is_start[xs[k]]) any = true;
-          }
+          const int64_t q = x0 + k * (int64_t)blockDim.x;
+          if (q < span) Jn[st + q] = v[k];
         }
       }
-      if (any) alive[r + 1] = 1;
-      grid.sync();
+      __syncthreads();
       ++r;
+      if (threadIdx.x == 0) s_more = Jn[st] != kEnd;  // the chain has >= 2^r more calls
+      __syncthreads();
+      if (!s_more) break;
     }
-    // ---- phase 2: long segments: chain length and last node by binary lifting ------------
-    // len = number of chain nodes (form_batch calls); the last one may be an empty tail
-    // (everything left is oversize, or the drain blocks on a request that does not fit)
-    for (int64_t sg = (int64_t)blockIdx.x * bt + tid; sg < n_segs; sg += (int64_t)gridDim.x * bt) {
-      if (!seg_long[sg]) continue;
-      const int64_t st = seg_off[sg], en = seg_off[sg + 1];
+    if (threadIdx.x == 0) {
+      if (s_more && r + 1 >= r_cap) latch_flags(sum, BS_FLAG_BATCH_CAP);  // table exhausted
+      // chain length and last node by binary lifting over the levels just built
       int64_t pos = st;
       int32_t cnt = 0;
       for (int lv = r - 1; lv >= 0; --lv) {
@@ -626,61 +598,115 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         if (y != kEnd) { pos = y; cnt += 1 << lv; }
       }
       const int64_t j0 = first_nonrej(pos, en, bmask);
-      seg_len[sg] = cnt + 1;
-      seg_empty[sg] = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
-      seg_tailj0[sg] = (int32_t)j0;
+      S.len[sg] = cnt + 1;
+      S.empty[sg] = !((j0 < en) && ((int64_t)slen[j0] <= a.T));
+      S.tailj0[sg] = (int32_t)j0;
+      S.lvl[sg] = r;
     }
-    grid.sync();
+    __syncthreads();
   }
-  // ---- phase 3 (block 0): node / batch bases per segment ---------------------------------
-  if (blockIdx.x == 0) {
-    if (tid == 0) sh.flag = (need_doubling && r + 1 >= r_cap && ld_rel_i32(alive + r)) ? 1 : 0;
-    int32_t run_n = 0, run_e = 0;
-    for (int base = 0; base < n_segs; base += bt) {
-      const int sg = base + tid;
-      const int32_t ln = sg < n_segs ? ld_rel_i32(seg_len + sg) : 0;
-      const int32_t em = sg < n_segs ? ld_rel_i32(seg_empty + sg) : 0;
-      int32_t tn, te;
-      const int32_t on = block_excl_scan<int32_t>(ln, sh.si, &tn);
-      const int32_t oe = block_excl_scan<int32_t>(em, sh.si, &te);
-      if (sg < n_segs) { seg_nbase[sg] = run_n + on; seg_ebase[sg] = run_e + oe; }
-      run_n += tn;
-      run_e += te;
-    }
-    if (tid == 0) {
-      seg_nbase[n_segs] = run_n;
-      seg_ebase[n_segs] = run_e;
-      const int32_t nb = run_n - run_e;
-      misc[64] = run_n;
-      misc[65] = r;
-      misc[66] = nb;
-      misc[68] = 0;
-      sum->n_batches = nb;
-      if (nb > batches_cap) latch_flags(sum, BS_FLAG_BATCH_CAP);
-      if (sh.flag) latch_flags(sum, BS_FLAG_BATCH_CAP);  // doubling table exhausted
-    }
+}
+
+__global__ void __launch_bounds__(1024)
+    k_chain_bases(const int32_t* __restrict__ kinfo, int32_t* __restrict__ segw,
+                  int32_t* __restrict__ misc, const int32_t* __restrict__ tile_sum,
+                  int32_t* __restrict__ tile_pre, int32_t n_tiles, int32_t batches_cap,
+                  bs_summary* sum) {
+  pdl_prologue();
+  __shared__ int32_t s_sc[3 * 33];
+  const int32_t n_segs = kinfo[2];
+  const SegArrays S = seg_arrays(segw, n_segs);
+  const int tid = threadIdx.x;
+  // contiguous runs per thread: one block scan for the node / empty-tail bases of the
+  // segments and the Rg tile prefix
+  const int per = (n_segs + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int i0 = min(n_segs, tid * per), i1 = min(n_segs, i0 + per);
+  const int tper = (n_tiles + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int t0 = min(n_tiles, tid * tper), t1 = min(n_tiles, t0 + tper);
+  int32_t v[3] = {0, 0, 0};
+  for (int i = i0; i < i1; ++i) { v[0] += S.len[i]; v[1] += S.empty[i]; }
+  for (int t = t0; t < t1; ++t) v[2] += tile_sum[t];
+  int32_t tot[3];
+  block_excl_scan_k<3, int32_t>(v, tot, s_sc);
+  int32_t rn = v[0], re = v[1], rt = v[2];
+  for (int i = i0; i < i1; ++i) {
+    S.nbase[i] = rn;
+    S.ebase[i] = re;
+    rn += S.len[i];
+    re += S.empty[i];
   }
-  grid.sync();
-  // ---- phase 4: materialise every chain node in emission order (fully parallel) -------
-  const int32_t M = ld_rel_i32(seg_nbase + n_segs);
-  for (int64_t i = (int64_t)blockIdx.x * bt + tid; i < M; i += (int64_t)gridDim.x * bt) {
-    int32_t lo = 0, hi = n_segs;  // last segment with seg_nbase <= i (non-empty ones win ties)
+  for (int t = t0; t < t1; ++t) {
+    tile_pre[t] = rt;
+    rt += tile_sum[t];
+  }
+  if (tid == 0) {
+    S.nbase[n_segs] = tot[0];
+    S.ebase[n_segs] = tot[1];
+    const int32_t nb = tot[0] - tot[1];
+    misc[64] = tot[0];
+    misc[66] = nb;
+    misc[68] = 0;
+    sum->n_batches = nb;
+    if (nb > batches_cap) latch_flags(sum, BS_FLAG_BATCH_CAP);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_chain_nodes(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
+                  const int32_t* __restrict__ J, const int32_t* __restrict__ listB,
+                  int32_t* __restrict__ listA, int32_t* __restrict__ node_batch,
+                  int32_t* __restrict__ node_j0, const int32_t* __restrict__ segw_c,
+                  const int32_t* __restrict__ misc, const int32_t* __restrict__ bcnt,
+                  const int32_t* __restrict__ tile_pre, int32_t* __restrict__ Rg, int32_t n_tiles,
+                  int32_t* dseg, int32_t* dmin, int64_t* dsum) {
+  pdl_prologue();
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x < n_tiles) {  // Rg: exclusive prefix of the admissible counts
+    __shared__ int32_t s_sc[33];
+    const int64_t G = (a.n + 31) >> 5;
+    const int64_t g0 = (int64_t)blockIdx.x * kRgTile;
+    constexpr int kPer = kRgTile / 256;
+    const int64_t gb = g0 + (int64_t)tid * kPer;
+    int32_t c[kPer];
+    int32_t loc = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      c[k] = gb + k < G ? bcnt[gb + k] : 0;
+      loc += c[k];
+    }
+    int32_t tot;
+    int32_t run = tile_pre[blockIdx.x] + block_excl_scan<int32_t>(loc, s_sc, &tot);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      if (gb + k < G) Rg[gb + k] = run;
+      run += c[k];
+    }
+    return;
+  }
+  const int32_t n_segs = kinfo[2];
+  int32_t* segw = const_cast<int32_t*>(segw_c);
+  const SegArrays S = seg_arrays(segw, n_segs);
+  const int32_t M = misc[64];
+  const int64_t stride = (int64_t)(gridDim.x - n_tiles) * blockDim.x;
+  for (int64_t i = (int64_t)(blockIdx.x - n_tiles) * blockDim.x + tid; i < M; i += stride) {
+    int32_t lo = 0, hi = n_segs;  // last segment with nbase <= i (non-empty ones win ties)
     while (hi - lo > 1) {
       const int32_t mid = (lo + hi) >> 1;
-      if (ld_rel_i32(seg_nbase + mid) <= i) lo = mid; else hi = mid;
+      if (S.nbase[mid] <= i) lo = mid; else hi = mid;
     }
-    const int32_t k = (int32_t)(i - ld_rel_i32(seg_nbase + lo));
+    const int32_t k = (int32_t)(i - S.nbase[lo]);
     int64_t pos = seg_off[lo];
-    if (ld_rel_i32(seg_long + lo)) {
-      for (int lv = 0; lv < r; ++lv)
-        if ((k >> lv) & 1) pos = J[(int64_t)lv * n + pos];
+    const int32_t lv = S.lvl[lo];
+    if (lv) {  // long segment: binary lifting over its doubling levels
+      for (int l = 0; l < lv; ++l)
+        if ((k >> l) & 1) pos = J[(int64_t)l * a.n + pos];
     } else {
-      pos = ld_rel_i32(listB + pos + k);  // walked in phase W
+      pos = listB[pos + k];  // walked
     }
     listA[i] = (int32_t)pos;
-    const bool tail_empty = (k == ld_rel_i32(seg_len + lo) - 1) && ld_rel_i32(seg_empty + lo);
-    node_batch[i] = tail_empty ? -1 : (int32_t)(i - ld_rel_i32(seg_ebase + lo));
-    node_j0[i] = tail_empty ? ld_rel_i32(seg_tailj0 + lo) : (int32_t)pos;
+    const bool tail_empty = (k == S.len[lo] - 1) && S.empty[lo];
+    node_batch[i] = tail_empty ? -1 : (int32_t)(i - S.ebase[lo]);
+    node_j0[i] = tail_empty ? S.tailj0[lo] : (int32_t)pos;
     if (dseg) {  // K7 per-call accumulators (filled by K5e)
       dseg[i] = lo;
       dmin[i] = INT32_MAX;
@@ -1004,6 +1030,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   a.C = p.n_classes;
   a.sjf_mask = a.ljf_mask = 0;
   a.walk = ctx->chain_walk > 0 ? ctx->chain_walk : kWalk;
+  a.walk_forced = ctx->chain_walk > 0;
   for (int c = 0; c < p.n_classes; ++c) {
     if (p.policy[c] == BS_POLICY_SJF) a.sjf_mask |= 1 << c;
     if (p.policy[c] == BS_POLICY_LJF) a.ljf_mask |= 1 << c;
@@ -1026,38 +1053,30 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   prof_mark(ctx, 6, st);
   {
-    int r_cap = ctx->r_cap;
-    const int32_t* ki = ctx->kinfo;
-    const int32_t* so = seg_off;
-    int32_t* J = ctx->J;
-    const uint8_t* is_start = ctx->is_start;
-    int32_t* alive = misc;
-    int32_t *la = ctx->listA, *lb = ctx->listB, *nbp = ctx->node_batch, *nj0 = ctx->node_j0;
-    const int32_t* sl = ctx->sorted_len;
-    const uint32_t* bm = ctx->bmask;
-    const int32_t* bc = ctx->bcnt;
-    int32_t* rg = ctx->Rg;
-    int32_t* bt = ctx->btot;
-    int32_t* sw = ctx->segw;
-    int32_t bcap = batches_cap;
-    bs_summary* sm = summary;
+    const int64_t G = (n + 31) >> 5;
+    const int32_t n_tiles = (int32_t)((G + kRgTile - 1) / kRgTile);
+    const int64_t segs_ub = (int64_t)p.l_max * p.n_classes;  // K2 makes at most L*C segments
     int32_t* dseg = p.dispatch ? ctx->disp_cseg : nullptr;
     int32_t* dmin = p.dispatch ? ctx->disp_cmin : nullptr;
     int64_t* dsum = p.dispatch ? ctx->disp_csum : nullptr;
-    const bool wide = ctx->chain_wide >= 0 ? ctx->chain_wide != 0 : n > kChainWide;
-    // small windows: fewer CTAs (a grid barrier over 148 CTAs costs more than the work)
-    const int cap = ctx->chain_ctas > 0 ? ctx->chain_ctas : ctx->chain_blocks;  // tuning hook
-    const unsigned cblocks = (unsigned)std::min<int64_t>(
-        std::min(ctx->chain_blocks, cap), std::max<int64_t>(1, (n + 4095) / 4096));
-    if (wide)
-      e = launch_k(ctx, k_chain<1024, 1>, dim3(cblocks), dim3(1024), 0, st, true, a, ki, so, J,
-                   r_cap, is_start, alive, la, lb, nbp, nj0, misc, sl, bm, bc, rg, bt, sw, bcap,
-                   sm, dseg, dmin, dsum);
-    else
-      e = launch_k(ctx, k_chain<512, 3>, dim3(cblocks), dim3(512), 0, st, true, a, ki, so, J,
-                   r_cap, is_start, alive, la, lb, nbp, nj0, misc, sl, bm, bc, rg, bt, sw, bcap,
-                   sm, dseg, dmin, dsum);
-    if (e != cudaSuccess) return e;
+    launch_k(ctx, k_chain_walk, dim3((unsigned)(n_tiles + (segs_ub + 255) / 256)), dim3(256), 0, st,
+             false, a, ctx->kinfo, seg_off, ctx->J, ctx->listB, ctx->sorted_len, ctx->bmask,
+             ctx->bcnt, ctx->segw, misc, ctx->rg_tiles, n_tiles);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    launch_k(ctx, k_chain_long, dim3((unsigned)ctx->num_sms), dim3(1024), 0, st, false, a,
+             ctx->kinfo, seg_off, ctx->J, ctx->r_cap, ctx->sorted_len, ctx->bmask, ctx->segw,
+             misc, summary);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    launch_k(ctx, k_chain_bases, dim3(1), dim3(1024), 0, st, false, ctx->kinfo, ctx->segw, misc,
+             ctx->rg_tiles, ctx->rg_tiles + n_tiles, n_tiles, batches_cap, summary);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int64_t nodes_blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4LL * ctx->num_sms));
+    launch_k(ctx, k_chain_nodes, dim3((unsigned)(n_tiles + nodes_blocks)), dim3(256), 0, st, false,
+             a, ctx->kinfo, seg_off, ctx->J, ctx->listB, ctx->listA, ctx->node_batch,
+             ctx->node_j0, ctx->segw, misc, ctx->bcnt, ctx->rg_tiles + n_tiles, ctx->Rg, n_tiles,
+             dseg, dmin, dsum);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ctx->launches += 3;  // four chain kernels where the count below has one
   }
   prof_mark(ctx, 7, st);
   launch_k(ctx, k_size_describe, dim3(wblocks), dim3(256), 0, st, false, a, ctx->kinfo, seg_off, ctx->sorted_len, ctx->bmax,
@@ -1110,8 +1129,3 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
 
 }  // namespace bsk
 
-void* bs_chain_kernel_ptr(int wide) {
-  return wide ? reinterpret_cast<void*>(&bsk::k_chain<1024, 1>)
-              : reinterpret_cast<void*>(&bsk::k_chain<512, 3>);
-}
-int bs_chain_threads(int wide) { return wide ? 1024 : 512; }

@@ -508,6 +508,23 @@ def test_outcome_in_request_id_ranges(parts, monkeypatch):
         test_gpu_matches_reference_fixture(name)
 
 
+@pytest.mark.parametrize("walk", ["1", "2", "5"])
+def test_chain_doubling_forced(walk, monkeypatch):
+    """K5c's long-segment path (one CTA per segment doubling pointers over its positions,
+    then binary lifting) gives the same batches as the serial walk: forced on every
+    segment whose chain is longer than BS_CHAIN_WALK calls (C2/C3-shaped windows with
+    rejections, pending requests, four classes, EXACT accounting)."""
+    monkeypatch.setenv("BS_CHAIN_WALK", walk)
+    monkeypatch.setenv("BS_SMALL", "0")  # small fixtures through the multi-kernel path too
+    for cfg_name, n in (("c2", 200_000), ("c3", 60_000)):
+        cfg, lens, cls = W.make_window(cfg_name, n=n, seed=11)
+        _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
+    for name in ("reject_heavy_acc0", "pledged_acc1", "zero_headroom", "four_class_exact",
+                 "equal_lengths", "c2_n30000", "c3_n20000", "c2_exact_ljf", "c2_fcfs_theta1",
+                 "tiny_L7_sjf_padded", "truncate"):
+        test_gpu_matches_reference_fixture(name)
+
+
 def _adversarial_moments(rng, budget, L, count):
     """(N, sum_len) pairs whose mean puts token_budget / mean on or next to an integer,
     where float rounding of the mean decides CPython's floor division."""
