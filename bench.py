@@ -51,7 +51,7 @@ def _pack_kernel(l_max, max_n):
     """the K6 kernel(s) the library launches by default (k_pack.cu: launch_pack)."""
     v = int(os.environ.get("BS_PACK_VARIANT", "0") or 0)
     if v not in (1, 5, 21):
-        v = 1 if max_n <= (4 << 20) else (5 if l_max > 16384 else 21)
+        v = 1
     return {1: "k_pack_bulk", 5: "k_pack_tma", 21: "k_pack_stream"}[v]
 
 

@@ -998,17 +998,17 @@ static cudaError_t launch_pack_stream(bs_ctx* ctx, const int32_t* len, const int
 }
 
 // K6 kernel for a pack call: 1 = bulk-staged, 5 = TMA-staged, 21 = register stream.
-// Default: the bulk-staged pack for contexts of up to 4M requests (C2 0.74 vs 0.79 ms per
-// window in flight, C4 6.35 vs 6.50 ms); above (C3's 16M) the register stream (13.36 vs
-// 13.60 ms).  BS_PACK_VARIANT forces one.  The bulk-staged pack stores 16-byte mask words
-// and whole 16-byte chunk images, so it needs 16-byte aligned outputs.
+// Default: the bulk-staged pack (windows in flight: C2 0.724 vs 0.79 ms, C3 12.18 vs
+// 12.70 ms, C4 6.33 vs 6.50 ms per window; it leaves SM room for the scheduling kernels
+// of the other windows).  BS_PACK_VARIANT forces one.  The bulk-staged pack stores 16-byte
+// mask words and whole 16-byte chunk images, so it needs 16-byte aligned outputs.
 static int pack_kernel_choice(const bs_ctx* ctx, const bs_window_params& p,
                               const int32_t* out_tokens, const uint8_t* out_mask) {
   const bool bulk_ok =
       ((reinterpret_cast<uintptr_t>(out_tokens) | reinterpret_cast<uintptr_t>(out_mask)) & 15) == 0;
   int v = ctx->pack_variant;
   if (v != 1 && v != 5 && v != 21)
-    v = (bulk_ok && ctx->max_n <= (4 << 20)) ? 1 : (p.l_max > 16384 ? 5 : 21);
+    v = bulk_ok ? 1 : (p.l_max > 16384 ? 5 : 21);
   if (v == 1 && !bulk_ok) v = p.l_max > 16384 ? 5 : 21;
   return v;
 }

@@ -932,9 +932,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------- K5f
-// one CTA; every thread owns a contiguous run of batches: a local pass for its sums, one
-// block scan of the three running offsets, a second pass writing them (C3's 25k batches:
-// one block scan instead of 49)
+// one 512-thread CTA (fits on an SM beside a pack CTA); every warp owns a contiguous run of
+// batches and reads it 32 batches (2 KB, coalesced) per step: warp sums, one block scan of
+// the warp totals, then a second coalesced pass writing the running offsets (warp scans)
 __global__ void __launch_bounds__(512)
     k_size_offsets(bs_batch* __restrict__ batches, int32_t batches_cap,
                    const int32_t* __restrict__ misc, int64_t* __restrict__ task_base,
@@ -944,13 +944,14 @@ __global__ void __launch_bounds__(512)
   __shared__ double s_d[32];
   __shared__ int64_t s_a[32], s_p[32], s_pk[32];
   const int nb = min(misc[66], batches_cap);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (nb + (int)blockDim.x - 1) / (int)blockDim.x;
-  const int i0 = min(nb, tid * per), i1 = min(nb, i0 + per);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+  const int per = ((nb + nw - 1) / nw + 31) & ~31;
+  const int i0 = min(nb, wid * per), i1 = min(nb, i0 + per);
   int64_t v[3] = {0, 0, 0};  // packed elements, rows, K6 pieces
   int64_t adm = 0, pad = 0, peak = 0;
   double ws = 0.0;
-  for (int i = i0; i < i1; ++i) {
+#pragma unroll 4
+  for (int i = i0 + lane; i < i1; i += 32) {
     const bs_batch& B = batches[i];
     v[0] += (int64_t)B.n * B.pitch;
     v[1] += B.n;
@@ -960,17 +961,33 @@ __global__ void __launch_bounds__(512)
     peak = B.footprint > peak ? B.footprint : peak;
     ws += B.waste;
   }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = warp_sum(v[k]);
+  if (lane != 0) v[0] = v[1] = v[2] = 0;  // one contribution per warp to the block scan
   int64_t tot[3];
   block_excl_scan_k<3, int64_t>(v, tot, s_sc);
-  int64_t run = v[0], rrun = v[1], trun = v[2];
-  for (int i = i0; i < i1; ++i) {
-    bs_batch& B = batches[i];
-    B.out_offset = run;
-    B.row_base = rrun;
-    task_base[i] = trun;
-    run += (int64_t)B.n * B.pitch;
-    rrun += B.n;
-    trun += (int64_t)B.n * ((B.pitch + ptok - 1) / ptok);
+  int64_t run[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) run[k] = __shfl_sync(0xffffffffu, v[k], 0);
+  for (int base = i0; base < i1; base += 32) {
+    const int i = base + lane;
+    int64_t x[3] = {0, 0, 0};
+    if (i < i1) {
+      const bs_batch& B = batches[i];
+      x[0] = (int64_t)B.n * B.pitch;
+      x[1] = B.n;
+      x[2] = (int64_t)B.n * ((B.pitch + ptok - 1) / ptok);
+    }
+    int64_t inc[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) inc[k] = warp_incl_scan(x[k]);
+    if (i < i1) {
+      batches[i].out_offset = run[0] + inc[0] - x[0];
+      batches[i].row_base = run[1] + inc[1] - x[1];
+      task_base[i] = run[2] + inc[2] - x[2];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) run[k] += __shfl_sync(0xffffffffu, inc[k], 31);
   }
   if (tid == 0) task_base[nb] = tot[2];
   adm = warp_sum(adm);
@@ -982,7 +999,7 @@ __global__ void __launch_bounds__(512)
   if (tid == 0) {
     int64_t A = 0, Pd = 0, Pk = 0;
     double Ws = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    for (int w = 0; w < nw; ++w) {
       A += s_a[w]; Pd += s_p[w]; Pk = s_pk[w] > Pk ? s_pk[w] : Pk; Ws += s_d[w];
     }
     sum->admitted_tokens = A;
