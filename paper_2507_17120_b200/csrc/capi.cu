@@ -80,7 +80,7 @@ void free_all(bs_ctx* c) {
                   c->bmax, c->bcnt, c->bsum, c->bmin, c->bmask, c->Rg, c->rg_tiles, c->J,
                   c->is_start, c->listA, c->listB, c->node_batch, c->node_j0, c->rowpos, c->rowdesc, c->chunk_row, c->task_base, c->segw,
                   c->disp_cseg, c->disp_cmin, c->disp_csum, c->disp_keys0, c->disp_keys1,
-                  c->disp_vals0, c->disp_vals1, c->disp_hist8, c->disp_agg, c->disp_status, c->disp_tctr, c->disp_nulls, c->disp_runs, c->disp_misc,
+                  c->disp_vals0, c->disp_vals1, c->disp_hist8, c->disp_agg, c->disp_status, c->disp_tctr, c->disp_nulls, c->disp_bkeys, c->disp_runs, c->disp_misc,
                   c->misc, c->small_rows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -204,7 +204,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   A(disp_keys0, N + 1); A(disp_keys1, N + 1); A(disp_vals0, N + 1); A(disp_vals1, N + 1);
   A(disp_hist8, 8 * 256);
   A(disp_status, 8 * ((N + 7167) / 7168 * 256 + 256)); A(disp_tctr, 8);
-  A(disp_nulls, L * C + 1); A(disp_runs, 4 * (2 * L * C + 32)); A(disp_misc, 32);
+  A(disp_nulls, L * C + 1); A(disp_bkeys, L * C + 1); A(disp_runs, 4 * (2 * L * C + 32)); A(disp_misc, 32);
   if ((e = cudaMemset(ctx->disp_hist8, 0, sizeof(uint32_t) * 8 * 256)) != cudaSuccess) {
     int rc = cuda_fail(ctx, e, "cudaMemset disp_hist8");
     free_all(ctx);

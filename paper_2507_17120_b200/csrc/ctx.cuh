@@ -108,6 +108,7 @@ struct bs_ctx {
   uint32_t* disp_status = nullptr;   // [8][max_n/7168+2][256] look-back words
   uint32_t* disp_tctr = nullptr;     // [8] tile counters
   int32_t* disp_nulls = nullptr;     // [l_cap*c_max+1] sorted positions of null calls
+  uint64_t* disp_bkeys = nullptr;    // [l_cap*c_max+1] per null call: its blocked bucket's key
   int32_t* disp_runs = nullptr;      // [2*l_cap*c_max+32][4] runs of consecutive plans
   int64_t* disp_misc = nullptr;      // [32]
   // C1 over peer memory (bs_peer_*)

@@ -114,6 +114,7 @@ struct DispArgs {
   int64_t stat_words;
   uint32_t* tctr;             // [8] tile counters
   int32_t* nulls;             // sorted positions of null calls
+  uint64_t* bkeys;            // per null call: key of its blocked bucket's remaining requests
   void* runs;
   int64_t* dmisc;
   SegVal* agg;                // [gridDim.x] chunk aggregates of the key scan
@@ -367,6 +368,30 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
     s_cb[tid] = lo;
   }
   const int nn_ = compact_nulls(a, V, M);
+  // the key a blocked bucket re-enters select_bucket with (min rank / length sum of the
+  // requests left after its null call, i.e. from the blocking request to the segment
+  // end): one warp per null call reduces its range (a blocked bucket may hold millions of
+  // requests), so the single-thread walk below only reads the result
+  {
+    const int lane = tid & 31, wid = tid >> 5, nwarps = (int)(blockDim.x >> 5);
+    unsigned kfl = 0;
+    for (int i = wid; i < nn_; i += nwarps) {
+      const uint32_t call = V[a.nulls[i]];
+      const int32_t sg = a.cseg[call];
+      const int64_t j0 = a.node_j0[call], en = a.seg_off[sg + 1];
+      if (j0 >= en) continue;  // not blocked: everything left was oversize
+      int32_t mn = INT32_MAX;
+      int64_t sm = 0;
+      for (int64_t j = j0 + lane; j < en; j += 32) {
+        mn = min(mn, a.perm[j]);
+        sm += a.slen[j];
+      }
+      mn = -warp_max(-mn);
+      sm = warp_sum(sm);
+      if (lane == 0) a.bkeys[i] = call_key(sg, SegVal{1, mn, sm}, C, kfl);
+    }
+    if (kfl) latch_flags(a.sum, kfl);
+  }
   if (tid == 0) s_nn = nn_;
   __syncthreads();
   if (tid != 0) return;
@@ -394,16 +419,6 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
     q[c] = lo;
   }
   unsigned fl = 0;
-  auto blocked_key = [&](uint32_t call) -> uint64_t {
-    const int32_t sg = a.cseg[call];
-    const int64_t j0 = a.node_j0[call], en = a.seg_off[sg + 1];
-    SegVal x{1, INT32_MAX, 0};
-    for (int64_t j = j0; j < en; ++j) {
-      x.mn = min(x.mn, a.perm[j]);
-      x.sm += a.slen[j];
-    }
-    return call_key(sg, x, C, fl);
-  };
   int64_t t = 0;
   int nr = 0;
   for (;;) {
@@ -447,7 +462,7 @@ __device__ void walk(const DispArgs& a, const uint64_t* K, const uint32_t* V, in
       }
       const uint32_t call = V[p[c]];
       if (a.node_j0[call] < a.seg_off[a.cseg[call] + 1]) {  // blocked drain
-        const uint64_t k2 = blocked_key(call);
+        const uint64_t k2 = a.bkeys[q[c]];  // q[c]: this null call's index in `nulls`
         thr[c] = k2 < thr[c] ? k2 : thr[c];
       }
       ++p[c];  // the call itself is spent (its oversize requests are rejected)
@@ -744,6 +759,7 @@ cudaError_t launch_dispatch(bs_ctx* ctx, const int32_t* perm, const int32_t* seg
   a.stat_words = (ctx->max_n + kSmall - 1) / kSmall * 256 + 256;
   a.tctr = ctx->disp_tctr;
   a.nulls = ctx->disp_nulls;
+  a.bkeys = ctx->disp_bkeys;
   a.runs = ctx->disp_runs;
   a.dmisc = ctx->disp_misc;
   a.agg = reinterpret_cast<SegVal*>(ctx->disp_agg);

@@ -177,3 +177,24 @@ def test_gpu_dispatch_blocked_bucket_reenters(seed):
     select_bucket with a smaller key and the class may go on with other buckets —
     3-4 classes, pledged memory blocking several buckets."""
     test_gpu_dispatch_random_vs_oracle(seed)
+
+
+def test_gpu_dispatch_large_blocked_buckets():
+    """Pledged memory blocks two buckets of 20k requests each (length 3000 > headroom
+    of 2500 tokens, admissible against current_safe): the key each re-enters
+    select_bucket with is reduced over its 20k remaining requests by one warp per null
+    call (it was a single-thread loop on the walk's critical path) — the
+    dispatch order equals the oracle's."""
+    rng = np.random.default_rng(77)
+    n = 400_000
+    lens = rng.choice(np.array([100, 200, 3000], np.int32), size=n, p=[0.45, 0.45, 0.10])
+    cls = rng.integers(0, 2, size=n).astype(np.uint8)
+    kvpt = 2
+    spec = dict(l_max=4096, n_classes=2, policies=(0, 1), theta=0.5, adjust=True,
+                max_passes=0, init_edges=None, kvpt=kvpt, current_safe=kvpt * 4000,
+                pledged=kvpt * 1500, accounting=0, truncate=True)
+    sched = _sched(spec, n)
+    h = sched.schedule(lens, cls).to_host()
+    assert (h["req_batch"] == -1).sum() > 30_000  # the blocked buckets stay pending
+    _check_vs_oracle(spec, lens, cls, h)
+    sched.close()
