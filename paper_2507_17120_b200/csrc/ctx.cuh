@@ -31,12 +31,8 @@ struct bs_ctx {
   int pack_reverse = 1;     // K6 takes its 32-piece groups last batch first (BS_PACK_REVERSE=0: in order)
   int pack_bulk_blocks = 0; // K6 bulk-staged grid: co-resident CTAs per SM x SMs (pack_prepare)
   int pack_bulk_warps = 16; // warps per CTA of the bulk-staged pack (BS_BULK_WARPS: 8 | 16)
-  int pack_free_sms = 0;    // SMs the bulk-staged pack leaves to other kernels (BS_PACK_FREE_SMS)
-  int pack_excl = 0;        // bulk-staged pack CTAs claim a whole SM's shared memory (BS_PACK_EXCL)
-  int pack_smem_excl = 0;   //   that request (bytes)
   int carveout_uniform = 0; // every kernel at the maximum shared-memory carveout (launch_k;
                             // bs_create: max_n <= 4M, BS_CARVEOUT overrides)
-  int pack_bulk_opt = 2;    // its options (BS_BULK_OPT): bit 1 async row tails, bit 2 register stores, bit 3 contiguous chunk ranges
   int64_t last_n = 0;       // requests of the last sized window (grid bound of the K6 row prep)
   int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
   int small_path = 1;       // K0 single-CTA path for small windows (BS_SMALL=0 disables)

@@ -582,10 +582,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// kOpt bit 1: row tails by 4-byte cp.async at issue time (else scalar loads at finish);
-// bit 2: the image goes out through registers (ld.shared + st.global.cs) instead of one
-// bulk shared -> global copy (no wait for the copy to read the slot before its refill)
-template <int kW, int kOpt>
+template <int kW>
 __global__ void __launch_bounds__(kW * 32)
     k_pack_bulk(const ulonglong2* __restrict__ desc, const int32_t* __restrict__ chunk_row,
                 int64_t chunk_cap, const int32_t* __restrict__ tokens,
@@ -594,7 +591,7 @@ __global__ void __launch_bounds__(kW * 32)
                 int32_t* __restrict__ out_tokens, uint8_t* __restrict__ out_mask, int64_t out_cap,
                 bs_summary* sum) {
   pdl_prologue();
-  constexpr int kS = 2;
+  constexpr int kS = 2;  // slots per warp: one chunk in flight while the other finishes
   extern __shared__ __align__(128) uint8_t bulk_smem[];
   __shared__ __align__(8) uint64_t bars[kW][kS];
   constexpr int T = kPackChunk;
@@ -603,24 +600,19 @@ __global__ void __launch_bounds__(kW * 32)
   PackRange R;
   if (!pack_range(batches, b_begin, b_end_arg, sum_in, batches_cap, R)) return;
   const int64_t n_chunks = (R.total + T - 1) / T;
-  constexpr bool kContig = (kOpt & 8) != 0;
-  if (R.total > out_cap || (!kContig && n_chunks > chunk_cap)) {
+  if (R.total > out_cap || n_chunks > chunk_cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) latch_flags(sum, BS_FLAG_PACK_CAPACITY);
     return;
   }
-  // chunk k of this warp: strided (default) u = warp + k * all_warps, so the warps in
-  // flight write neighbouring chunks (DRAM page locality of the output stream; the first
-  // row of each chunk from chunk_row), or with kOpt & 8 a contiguous range of chunks (the
-  // rows of chunk u + 1 continue where chunk u's left off; only the range start is searched)
+  // chunk k of this warp is u = warp + k * all_warps, so the warps in flight write
+  // neighbouring chunks (DRAM page locality of the output stream); the first row of each
+  // chunk comes from chunk_row.  (Contiguous chunk ranges per warp measured 0.83 vs 0.69 ms
+  // at C2: 2,368 far-apart write streams.)
   const int64_t nw = (int64_t)gridDim.x * kW;
   const int64_t gw = (int64_t)blockIdx.x * kW + wib;
-  const int64_t cpw = (n_chunks + nw - 1) / nw;
-  const int64_t u_begin = kContig ? gw * cpw : gw;
-  const int64_t k_end = min(u_begin + cpw, n_chunks);
-  const int64_t K = kContig ? (k_end > u_begin ? k_end - u_begin : 0)
-                            : (gw < n_chunks ? (n_chunks - gw + nw - 1) / nw : 0);
+  const int64_t K = gw < n_chunks ? (n_chunks - gw + nw - 1) / nw : 0;
   if (K == 0) return;
-  auto chunk = [&](int64_t k) { return kContig ? u_begin + k : gw + k * nw; };
+  auto chunk = [&](int64_t k) { return gw + k * nw; };
   BulkSlot* slots = reinterpret_cast<BulkSlot*>(bulk_smem) + wib * kS;
   uint64_t* bar = bars[wib];
   if (lane == 0) {
@@ -634,18 +626,16 @@ __global__ void __launch_bounds__(kW * 32)
     return g >= 0 && g < n_rows ? desc[g] : make_ulonglong2(0, 0);
   };
 
-  // issue chunk u into slot s from row g0 (d_first = the descriptors of rows g0 + lane):
-  // descriptors into the slot, one bulk copy per row for its 16-byte token vectors inside
-  // the chunk and, with kOpt & 2, the row tail (x % 4 tokens) by 4-byte cp.async.
-  // Returns the first row of chunk u + 1.
-  auto issue = [&](int s, int64_t u, int64_t g0, ulonglong2 d_first) -> int64_t {
+  // issue chunk u into slot s from row g0 (d_first = the records of rows g0 + lane): the
+  // records into the slot, one bulk copy per row for its 16-byte token vectors inside the
+  // chunk, and the row tail (x % 4 tokens, where the row ends inside the chunk) by 4-byte
+  // cp.async into the image
+  auto issue = [&](int s, int64_t u, int64_t g0, ulonglong2 d_first) {
     BulkSlot& S = slots[s];
     const int64_t c0 = u * T, c1 = min(c0 + T, R.total);
     for (int i = lane; i < T / 32; i += 32) reinterpret_cast<uint32_t*>(S.mark)[i] = 0u;
-    if (kOpt & 4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     int nin = 0;  // rows of the chunk so far (rows of pitch 0 hold no output and are skipped)
-    int64_t g_next = g0;
     for (int64_t base = g0;; base += 32) {
       const int64_t g = base + lane;
       const ulonglong2 d = base == g0 ? d_first : load_desc(g);
@@ -667,7 +657,7 @@ __global__ void __launch_bounds__(kW * 32)
         const int64_t hi = min(dst + x, c1);
         if (hi > lo && al) {
           bytes = (uint32_t)((hi - lo) & ~3ll) * 4u;
-          if ((kOpt & 2) && hi == dst + x)  // the row ends here: its tail, asynchronously
+          if (hi == dst + x)  // the row ends here: its tail, asynchronously
             for (int32_t e = x & ~3; e < x; ++e)
               asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
                                smem_addr(S.tok + (dst + e - c0))),
@@ -689,18 +679,11 @@ __global__ void __launch_bounds__(kW * 32)
             "l"(src), "r"(bytes), "r"(smem_addr(&bar[s]))
             : "memory");
       nin += __popc(bal);
-      const unsigned rb = __ballot_sync(FULL, reach);
-      if (rb) {  // the last row reaching into the chunk: the next chunk starts on it or after it
-        const int hl = 31 - __clz(rb);
-        const int64_t e = __shfl_sync(FULL, dst + pitch, hl);
-        g_next = base + hl + (e > c1 ? 0 : 1);
-      }
-      if (rb != FULL || !__shfl_sync(FULL, dst + pitch < c1, 31)) break;
+      if (!__shfl_sync(FULL, reach && dst + pitch < c1, 31)) break;
     }
-    if (kOpt & 2) asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&bar[s])) : "memory");
-    return g_next;
   };
 
   // finish: wait for the chunk's bytes, add tails / padding / mask, store the image
@@ -715,7 +698,7 @@ __global__ void __launch_bounds__(kW * 32)
         : "memory");
     // this lane's tail copies of the chunk: one cp.async group is committed per chunk in
     // order, so the younger group (chunk u + 1) may stay pending
-    if (kOpt & 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
     constexpr int kG = T / 16 / 32;  // 16-token groups per lane (contiguous)
     uint16_t mk[kG];
@@ -757,12 +740,12 @@ __global__ void __launch_bounds__(kW * 32)
           int4* slot4 = reinterpret_cast<int4*>(S.tok + 16 * m + 4 * v);
           int4 r4 = make_int4(pad_id, pad_id, pad_id, pad_id);
           if (q < x) {
-            if ((kOpt & 2) && al) {  // the tail vector: tokens below x arrived by cp.async
+            if (al) {  // the tail vector: tokens below x arrived by cp.async
               const int4 t = *slot4;
               r4.x = t.x;
               if (q + 1 < x) r4.y = t.y;
               if (q + 2 < x) r4.z = t.z;
-            } else {
+            } else {   // a row whose tokens are not 16-byte aligned: scalar loads
               r4.x = sp[q];
               if (q + 1 < x) r4.y = sp[q + 1];
               if (q + 2 < x) r4.z = sp[q + 2];
@@ -773,97 +756,54 @@ __global__ void __launch_bounds__(kW * 32)
         }
       }
     }
-    if (kOpt & 4) {  // through registers: the slot is free when the warp is done with it
-      __syncwarp();
-      const int4* img = reinterpret_cast<const int4*>(S.tok);
-      int4* o4 = reinterpret_cast<int4*>(out_tokens + c0);
-      const int nv = (int)(c1 - c0) >> 2;
-      for (int v = lane; v < nv; v += 32) st_stream_v4(o4 + v, img[v]);
-      __syncwarp();
-    } else {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out_tokens + c0),
-                     "r"(smem_addr(S.tok)), "r"((uint32_t)(c1 - c0) * 4u)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out_tokens + c0),
+                   "r"(smem_addr(S.tok)), "r"((uint32_t)(c1 - c0) * 4u)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   };
 
-  auto row_of = [&](int64_t k) -> int64_t {  // strided: first row of chunk k
+  auto row_of = [&](int64_t k) -> int64_t {  // first row of chunk k
     return k < K ? (int64_t)chunk_row[chunk(k)] : -1;
   };
-  int64_t g0;
-  if (kContig) {  // first row of the range: the last row with dst <= u_begin * T (32-ary search)
-    const int64_t c = u_begin * T;
-    int64_t lo = 0, hi = n_rows;
-    while (hi - lo > 1) {
-      const int64_t step = (hi - lo + 31) >> 5;
-      const int64_t idx = lo + (lane + 1) * step;
-      const bool le = idx < hi && (int64_t)(desc[idx].y & kLo40) <= c;
-      lo += (int64_t)__popc(__ballot_sync(FULL, le)) * step;
-      hi = min(hi, lo + step);
-    }
-    g0 = lo;
-  } else {
-    g0 = row_of(0);
-  }
-  // prologue: both slots in flight.  The first row of chunk k + 2 (and, strided, of k + 3)
-  // and the descriptors of chunk k + 2 are loaded an iteration ahead of their use, so the
-  // dependent metadata loads overlap the finish of chunk k.
-  int64_t g = issue(0, chunk(0), g0, load_desc(g0 + lane));
+  // prologue: both slots in flight.  The first rows of chunks k + 2, k + 3 and the records
+  // of chunk k + 2 are loaded an iteration ahead of their use, so the dependent metadata
+  // loads (chunk_row -> rowdesc) overlap the finish of chunk k.
+  const int64_t g0 = row_of(0);
+  issue(0, chunk(0), g0, load_desc(g0 + lane));
   if (K > 1) {
-    const int64_t g1 = kContig ? g : row_of(1);
-    g = issue(1, chunk(1), g1, load_desc(g1 + lane));
-  } else if (kOpt & 2) {
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    const int64_t g1 = row_of(1);
+    issue(1, chunk(1), g1, load_desc(g1 + lane));
+  } else {
+    asm volatile("cp.async.commit_group;" ::: "memory");  // keeps one group per chunk
   }
-  int64_t nx_g = kContig ? g : row_of(2);
+  int64_t nx_g = row_of(2);
   ulonglong2 nx_d = K > 2 ? load_desc(nx_g + lane) : make_ulonglong2(0, 0);
-  int64_t nx2_g = kContig ? -1 : row_of(3);
+  int64_t nx2_g = row_of(3);
 #pragma unroll 1
   for (int64_t k = 0; k < K; ++k) {
     const int s = (int)(k & 1);
     finish(s, chunk(k), (uint32_t)((k >> 1) & 1));
-    if (k + 2 < K) {  // refill the slot (once its store has read the image)
-      if (!(kOpt & 4) && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (k + 2 < K) {  // refill the slot once its store has read the image
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
-      g = issue(s, chunk(k + 2), nx_g, nx_d);
-      if (kContig) {
-        nx_g = g;
-      } else {
-        nx_g = nx2_g;
-        nx2_g = row_of(k + 4);
-      }
+      issue(s, chunk(k + 2), nx_g, nx_d);
+      nx_g = nx2_g;
+      nx2_g = row_of(k + 4);
       nx_d = k + 3 < K ? load_desc(nx_g + lane) : make_ulonglong2(0, 0);
-    } else if (kOpt & 2) {
+    } else {
       asm volatile("cp.async.commit_group;" ::: "memory");  // (empty) group of chunk k + 2
     }
   }
-  if (kOpt & 2) asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int kW>
 static size_t bulk_smem() { return sizeof(BulkSlot) * kW * 2; }
-
-// kOpt (BS_BULK_OPT): bit 1 async row tails, bit 2 register stores, bit 3 contiguous
-// chunk ranges per warp (see k_pack_bulk)
-template <int kW>
-static auto bulk_kernel(int opt) {
-  switch (opt & 14) {
-    case 0: return k_pack_bulk<kW, 0>;
-    case 2: return k_pack_bulk<kW, 2>;
-    case 4: return k_pack_bulk<kW, 4>;
-    case 6: return k_pack_bulk<kW, 6>;
-    case 8: return k_pack_bulk<kW, 8>;
-    case 10: return k_pack_bulk<kW, 10>;
-    case 12: return k_pack_bulk<kW, 12>;
-    default: return k_pack_bulk<kW, 14>;
-  }
-}
 
 template <int kW>
 static cudaError_t launch_pack_bulk(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
@@ -881,13 +821,12 @@ static cudaError_t launch_pack_bulk(bs_ctx* ctx, const int32_t* len, const int32
         (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows_ub + 255) / 256, 8LL * ctx->num_sms));
     launch_k(ctx, k_pack_rowprep, dim3(pblocks), dim3(256), 0, st, false, len, perm, ctx->rowpos,
              tok_off, p.l_max, p.truncate, batches, batch_begin, batch_end, summary, batches_cap,
-             ctx->rowdesc, (ctx->pack_bulk_opt & 8) ? nullptr : ctx->chunk_row, ctx->chunk_cap,
-             summary);
+             ctx->rowdesc, ctx->chunk_row, ctx->chunk_cap, summary);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++ctx->launches;
   }
-  launch_k(ctx, bulk_kernel<kW>(ctx->pack_bulk_opt), dim3((unsigned)ctx->pack_bulk_blocks),
-           dim3(kW * 32), ctx->pack_excl ? (size_t)ctx->pack_smem_excl : bulk_smem<kW>(), st, false, ctx->rowdesc, ctx->chunk_row, ctx->chunk_cap,
+  launch_k(ctx, k_pack_bulk<kW>, dim3((unsigned)ctx->pack_bulk_blocks), dim3(kW * 32),
+           bulk_smem<kW>(), st, false, ctx->rowdesc, ctx->chunk_row, ctx->chunk_cap,
            tokens, p.pad_id, batches,
            batch_begin, batch_end, summary, batches_cap, out_tokens, out_mask, out_capacity,
            summary);
@@ -943,22 +882,16 @@ cudaError_t pack_prepare(bs_ctx* ctx) {
   ctx->pack_tma_blocks = std::max(1, per_sm) * ctx->num_sms;
   // bulk-staged pack: 16 warps x 2 slots (~168 KB, one CTA per SM) or 8 warps (two per SM)
   const bool w8 = ctx->pack_bulk_warps == 8;
-  int optin = 0;
-  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  const size_t bsm = w8 ? bulk_smem<8>() : bulk_smem<16>();
+  e = w8 ? cudaFuncSetAttribute(k_pack_bulk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)
+         : cudaFuncSetAttribute(k_pack_bulk<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
   if (e != cudaSuccess) return e;
-  ctx->pack_smem_excl = optin - 1024;  // static mbarriers
-  const size_t bsm = ctx->pack_excl ? (size_t)ctx->pack_smem_excl : (w8 ? bulk_smem<8>() : bulk_smem<16>());
-  for (int opt = 0; opt < 16; opt += 2) {
-    e = w8 ? cudaFuncSetAttribute(bulk_kernel<8>(opt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm)
-           : cudaFuncSetAttribute(bulk_kernel<16>(opt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
-    if (e != cudaSuccess) return e;
-  }
   per_sm = 0;
-  e = w8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk_kernel<8>(ctx->pack_bulk_opt), 8 * 32, bsm)
-         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk_kernel<16>(ctx->pack_bulk_opt), 16 * 32, bsm);
+  e = w8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_bulk<8>, 8 * 32, bsm)
+         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_bulk<16>, 16 * 32, bsm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  ctx->pack_bulk_blocks = per_sm * std::max(1, ctx->num_sms - ctx->pack_free_sms);
+  ctx->pack_bulk_blocks = per_sm * ctx->num_sms;
   return cudaSuccess;
 }
 

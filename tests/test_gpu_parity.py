@@ -372,16 +372,14 @@ def test_sharded_window_on_one_gpu(world):
         s.close()
 
 
-# K6 kernels: "0" bulk-staged (default: 16 warps per CTA, async row tails, bulk stores;
-# "0w8": 8 warps, two CTAs per SM; "0oK": BS_BULK_OPT=K), 5 = TMA-staged register
-# stores, 21 = register stream
-PACK_VARIANTS = ["0", "0w8", "0o0", "0o4", "0o6", "5", "21"]
+# K6 kernels: "0" bulk-staged (default: 16 warps per CTA; "0w8": 8 warps, two CTAs per
+# SM), 5 = TMA-staged register stores, 21 = register stream
+PACK_VARIANTS = ["0", "0w8", "5", "21"]
 
 
 def _set_variant(monkeypatch, variant):
     monkeypatch.setenv("BS_PACK_VARIANT", "1" if variant.startswith("0") else variant)
     monkeypatch.setenv("BS_BULK_WARPS", "8" if variant == "0w8" else "16")
-    monkeypatch.setenv("BS_BULK_OPT", variant[2:] if variant.startswith("0o") else "2")
 
 
 @pytest.mark.parametrize("variant", PACK_VARIANTS)
