@@ -78,8 +78,9 @@ enum bs_change_kind { BS_CHANGE_SPLIT = 1, BS_CHANGE_MERGE = 2, BS_CHANGE_SKIP =
 #define BS_REQ_REJECTED (-2)   /* OversizeRejection, batch_controller.py:44-67,165-169 */
 
 #define BS_MAX_CLASSES 8
-#define BS_PACK_ALIGN  32      /* packed row pitch = round_up(max_input_len, 32) tokens: every
-                                  row starts on a 128-byte line (tokens) / 32-byte sector (mask) */
+#define BS_PACK_ALIGN  16      /* packed row pitch = round_up(max_input_len, 16) tokens: every
+                                  row starts on a 64-byte boundary (tokens) / 16 bytes (mask), so
+                                  16-token mask words never straddle rows */
 
 /* ---- parameter block (host memory) ------------------------------------------ */
 typedef struct bs_window_params {

@@ -61,7 +61,7 @@ enum { SPLIT = 1, MERGE = 2, SKIP = 3 };
 #define F_BATCH_CAP 0x40
 #define REQ_PENDING (-1)
 #define REQ_REJECTED (-2)
-#define PACK_ALIGN 32 /* BS_PACK_ALIGN */
+#define PACK_ALIGN 16 /* BS_PACK_ALIGN */
 
 int bso_num_threads(void) {
 #ifdef _OPENMP

@@ -42,7 +42,7 @@ ACCOUNTING_PADDED, ACCOUNTING_EXACT = 0, 1
 CHANGE_SPLIT, CHANGE_MERGE, CHANGE_SKIP = 1, 2, 3
 REQ_PENDING, REQ_REJECTED = -1, -2
 MAX_CLASSES = 8
-PACK_ALIGN = 32
+PACK_ALIGN = 16
 
 EXPORTS = ("bs_abi_version", "bs_last_error", "bs_scratch_bytes", "bs_create", "bs_destroy",
            "bs_histogram", "bs_boundaries", "bs_assign", "bs_order", "bs_size", "bs_pack",

@@ -3,7 +3,7 @@
 // No reference counterpart (bucketsim never holds token ids); the layout is the
 // one the memory model charges: a batch is padded to its max_input_len
 // (batch_controller.py:136-139, the PADDED footprint), stored with row pitch
-// round_up(max_input_len, 32) so every row starts on a 128-byte line; padding carries
+// round_up(max_input_len, 16) (BS_PACK_ALIGN) so every row starts 64-byte aligned; padding carries
 // pad_id and mask 0, so the padding fraction of [n, max_input_len] equals the
 // batch's waste_ratio (memory_model.py:92-100).
 //
