@@ -142,8 +142,8 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
   if (const char* v = getenv("BS_PACK_REVERSE")) ctx->pack_reverse = atoi(v) != 0;
   if (const char* v = getenv("BS_BULK_WARPS")) ctx->pack_bulk_warps = atoi(v) == 8 ? 8 : 16;
-  ctx->carveout_uniform = max_n <= (4 << 20);
-  if (const char* v = getenv("BS_CARVEOUT")) ctx->carveout_uniform = atoi(v) != 0;
+  ctx->carveout_uniform = max_n <= (4 << 20) ? 100 : 0;
+  if (const char* v = getenv("BS_CARVEOUT")) ctx->carveout_uniform = std::max(0, std::min(100, atoi(v)));
   if (const char* v = getenv("BS_SMALL")) ctx->small_path = atoi(v) != 0;
   if (const char* v = getenv("BS_SMALL_TIMING")) ctx->small_timing = atoi(v) != 0;
   int r = 1;

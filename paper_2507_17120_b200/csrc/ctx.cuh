@@ -31,8 +31,8 @@ struct bs_ctx {
   int pack_reverse = 1;     // K6 takes its 32-piece groups last batch first (BS_PACK_REVERSE=0: in order)
   int pack_bulk_blocks = 0; // K6 bulk-staged grid: co-resident CTAs per SM x SMs (pack_prepare)
   int pack_bulk_warps = 16; // warps per CTA of the bulk-staged pack (BS_BULK_WARPS: 8 | 16)
-  int carveout_uniform = 0; // every kernel at the maximum shared-memory carveout (launch_k;
-                            // bs_create: max_n <= 4M, BS_CARVEOUT overrides)
+  int carveout_uniform = 0; // > 0: every kernel at this shared-memory carveout, percent of the
+                            // maximum (launch_k; bs_create: 100 for max_n <= 4M, BS_CARVEOUT)
   int64_t last_n = 0;       // requests of the last sized window (grid bound of the K6 row prep)
   int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
   int small_path = 1;       // K0 single-CTA path for small windows (BS_SMALL=0 disables)
@@ -168,14 +168,14 @@ inline cudaError_t launch_k(const bs_ctx* ctx, void (*kernel)(KArgs...), dim3 gr
   cfg.stream = st;
   cudaLaunchAttribute at[3];
   unsigned na = 0;
-  if (ctx->carveout_uniform) {
+  if (ctx->carveout_uniform > 0) {
     // every kernel of the window at the maximum shared-memory carveout: an SM only runs
     // CTAs of one L1 / shared-memory split at a time, so with mixed splits the scheduling
     // kernels of the windows in flight could not start on an SM beside the (shared-memory
     // staged) pack of another window.  Windows of up to 4M requests (C2: 0.735 vs 0.759 ms
     // per window in flight); at 16M (C3) the gather-heavy K5 kernels want their L1 back.
     at[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
-    at[na].val.sharedMemCarveout = (unsigned)cudaSharedmemCarveoutMaxShared;
+    at[na].val.sharedMemCarveout = (unsigned)ctx->carveout_uniform;  // percent of the maximum
     ++na;
   }
   if (cooperative) {

@@ -123,13 +123,19 @@ cudaError_t launch_window_init(bs_ctx* ctx, bs_summary* s, int64_t n, uint32_t* 
   return cudaGetLastError();
 }
 
-// per-context setup on the context's device (bs_create): 64 KB of privatised counters
+// privatised head of K1: <= 48 KB of shared counters per CTA, so a K1 CTA fits on an SM
+// beside a bulk-staged pack CTA (168 KB) of another window in flight (with 64 KB, C3's
+// four-class K1 waited for the pack to end); lengths beyond the head go to L2 atomics
+constexpr int kHistSmem = 48 * 1024;
+
+// per-context setup on the context's device (bs_create)
 cudaError_t hist_prepare(bs_ctx* ctx) {
+  (void)ctx;
   cudaError_t e = cudaFuncSetAttribute(k_histogram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       64 * 1024);
+                                       kHistSmem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_histogram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             64 * 1024);
+                             kHistSmem);
   return e;
 }
 
@@ -140,8 +146,7 @@ cudaError_t launch_histogram(bs_ctx* ctx, const int32_t* len, const uint8_t* cls
   cudaError_t e = cudaSuccess;
   if (!ctx->window_zeroed) e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)L * C, st);
   if (e != cudaSuccess || n == 0) return e;
-  // privatised head: <= 64 KB of shared counters per CTA (3 CTAs / SM)
-  const int32_t H = (int32_t)std::min<int64_t>(L, (64 * 1024 / 4) / C);
+  const int32_t H = (int32_t)std::min<int64_t>(L, (kHistSmem / 4) / C);
   const size_t smem = sizeof(uint32_t) * (size_t)C * H;
   const int threads = 512;
   // >= ept elements per thread and at most 2 CTAs per SM: the per-CTA zero/flush of the
