@@ -16,8 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
-@pytest.mark.parametrize("tool,args", [("memcheck", []), ("racecheck", ["--small"]),
-                                       ("synccheck", ["--small"])])
+@pytest.mark.parametrize("tool,args", [("memcheck", []), ("memcheck", ["--paths"]),
+                                       ("racecheck", ["--small"]), ("synccheck", ["--small"])])
 def test_sanitizer_clean(tool, args):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")

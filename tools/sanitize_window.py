@@ -3,6 +3,7 @@ unaligned token stores, long-context TMA pack, four classes), for compute-saniti
 
     compute-sanitizer --tool memcheck  --error-exitcode 9 python tools/sanitize_window.py
     compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_window.py --small
+    compute-sanitizer --tool memcheck  --error-exitcode 9 python tools/sanitize_window.py --paths
 """
 import os
 import sys
@@ -16,6 +17,12 @@ from paper_2507_17120_b200 import workloads as W  # noqa: E402
 from paper_2507_17120_b200.window import WindowScheduler  # noqa: E402
 
 cases = [("c2", 30000, 32), ("c2", 20000, 1), ("c4", 2000, 32), ("c3", 40000, 4)]
+if "--paths" in sys.argv:
+    # the rarer K5 paths: every chain longer than 2 calls through K5c's doubling CTAs, and
+    # K5e's drain-order outcomes scattered in three request-id ranges
+    os.environ["BS_CHAIN_WALK"] = "2"
+    os.environ["BS_OUTCOME_PARTS"] = "3"
+    cases = [("c2", 30000, 32), ("c3", 40000, 4)]
 if "--small" in sys.argv:
     cases = [("c2", 3000, 32), ("c3", 3000, 1), ("c4", 300, 32)]
 for name, n, align in cases:
