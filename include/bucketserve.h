@@ -215,7 +215,11 @@ int bs_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int32_t*
  * beyond, and out_mask (1 for real tokens, 0 for padding; may be NULL).  Offsets are
  * relative to the first packed batch of the call (chunked packing into a reusable
  * buffer); out_capacity is in elements.  Uses the row map of the last bs_size call on
- * ctx.  Rows are moved with 128-bit accesses when tok_off[i] % 4 == 0. */
+ * ctx.  out_tokens must be 16-byte aligned, out_mask 4-byte aligned.  With both 16-byte
+ * aligned (the usual case) the bulk-staged kernel runs: the output is cut into
+ * 1024-token chunks filled in shared memory by bulk copies (rows whose tokens start
+ * 16-byte aligned, i.e. tok_off[i] % 4 == 0 for an aligned store; other rows by scalar
+ * loads) and stored by bulk copies; otherwise a 128-bit register stream. */
 int bs_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm, const int64_t* tok_off,
             const int32_t* tokens, const bs_window_params* p, const bs_batch* batches,
             int64_t batch_begin, int64_t batch_end, int32_t* out_tokens, uint8_t* out_mask,

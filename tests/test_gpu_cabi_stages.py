@@ -92,6 +92,15 @@ def _run_stages(spec, lens, cls, tok_off, tokens, chunk=None):
                             0, -1, _p(tok_all), _p(msk_all), cap_el, _p(summ), st), ctx.ptr)
     torch.cuda.synchronize()
     out["tokens"], out["mask"] = tok_all[:total].cpu().numpy(), msk_all[:total].cpu().numpy()
+    if nb:  # a mask buffer that is only 4-byte aligned: the register-stream fallback
+        tok_u = torch.full((cap_el + 8,), -7, **i32)
+        msk_u = torch.zeros(cap_el + 16, dtype=torch.uint8, device=DEV)
+        N.check(lib.bs_pack(ctx.ptr, _p(d_len), _p(perm), _p(d_off), _p(d_tok), C.byref(prm),
+                            _p(batches), 0, -1, C.c_void_p(tok_u.data_ptr() + 16),
+                            C.c_void_p(msk_u.data_ptr() + 4), cap_el, _p(summ), st), ctx.ptr)
+        torch.cuda.synchronize()
+        out["tokens_u"] = tok_u[4:4 + total].cpu().numpy()
+        out["mask_u"] = msk_u[4:4 + total].cpu().numpy()
     if chunk and nb:
         pieces_t, pieces_m = [], []
         buf_t = torch.empty(cap_el, **i32)
@@ -142,6 +151,8 @@ def test_stages_match_oracle(name):
     if "chunked_tokens" in g:
         assert np.array_equal(g["chunked_tokens"], g["tokens"])
         assert np.array_equal(g["chunked_mask"], g["mask"])
+    if "tokens_u" in g:
+        assert np.array_equal(g["tokens_u"], g["tokens"]) and np.array_equal(g["mask_u"], g["mask"])
     assert int(g["summary"]["n_max"]) == int(ref["n_max"])
 
 
