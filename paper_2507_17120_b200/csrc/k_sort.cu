@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 
   const int64_t tbase = (int64_t)tile * kTile;
   const int64_t wbase = tbase + (int64_t)w * (32 * kItems);
 
-  uint32_t key[kItems], val[kItems], rank[kItems];
+  // values: the first pass sorts the indices themselves (val = e, recomputed where needed,
+  // so the 16-item tiles fit 64 registers without spilling)
+  uint32_t key[kItems], val[kFirst ? 1 : kItems], rank[kItems];
   unsigned fl = 0;
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
@@ -96,7 +98,6 @@ __global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 
         const int32_t x = eff_len(len[e], L, truncate, fl);
         const int32_t c = eff_cls(cls[e], C, fl);
         key[k] = slot_lut[(int64_t)c * L + x];
-        val[k] = (uint32_t)e;
         if (bucket_out) bucket_out[e] = lut[x];
       } else {
         key[k] = keys_in[e];
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 
       }
     } else {
       key[k] = 0xffffffffu;
-      val[k] = 0;
+      if (!kFirst) val[k] = 0;
     }
   }
   // ---- warp-level stable ranking (items in index order: k-major, lane-minor) ----
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kSortThreads, kItems >= 16 ? kSortMinBlocks16 
       const uint32_t d = (key[k] >> shift) & dmask;
       const uint32_t lp = s_dstart[d] + s_cnt[w][d] + rank[k];
       s_keys[lp] = key[k];
-      s_vals[lp] = val[k];
+      s_vals[lp] = kFirst ? (uint32_t)e : val[kFirst ? 0 : k];
     }
   }
   __syncthreads();
