@@ -489,26 +489,27 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
 // ---------------------------------------------------------------------------------
 // Bulk-staged pack (default): the packed output of a batch range is one contiguous
 // stream (batches back to back, rows back to back), cut here into chunks of kPackChunk
-// tokens.  A CTA of kW warps stays resident on its SM (persistent grid, one or two CTAs
-// per SM); each warp owns two shared-memory slots and walks its chunks u = warp, warp +
-// all_warps, ...  Per chunk:
-//   issue   the lanes read the descriptors of the chunk's rows (k_pack_rowprep below,
-//           one coalesced 16-byte record per row) into the slot and start one
-//           cp.async.bulk global -> shared per row for the row's real 16-byte token vectors
-//           inside the chunk, placed at the row's offset in the slot's image of the chunk
-//           (completion counted in bytes on the slot's mbarrier);
+// tokens.  A CTA of kW warps stays resident on its SM (persistent grid, one CTA per SM
+// with 16 warps); each warp owns two shared-memory slots and walks its chunks u = warp,
+// warp + all_warps, ...  Per chunk:
+//   issue   the lanes read the records of the chunk's rows (one coalesced 16-byte record
+//           per row, written by K5e for a fused window or by k_pack_rowprep below) into
+//           the slot and start one cp.async.bulk global -> shared per row for the row's
+//           real 16-byte token vectors inside the chunk, placed at the row's offset in the
+//           slot's image of the chunk (completion counted in bytes on the slot's
+//           mbarrier), and the row tail (<= 3 tokens) by 4-byte cp.async;
 //   finish  once the bytes landed: every lane takes 16-token groups of the chunk (a row
 //           starts on a group boundary: pitch % 16 == 0), finds the group's row from the
-//           per-group row-start marks (a warp max-scan), writes the row tail (<= 3 tokens,
-//           scalar loads) and the padding into the image and the group's 16 mask bytes
-//           straight to global (st.global.cs.v4); then one cp.async.bulk shared -> global
-//           stores the whole token image.
-// Bytes in flight per SM are bounded by shared memory (2 x 4 KB of reads per warp, the
-// stores asynchronous too) instead of by registers, with few threads (16 warps x 47
-// registers), so the scheduling kernels of the windows in flight keep SM room beside it.
-// Against the register stream on C2's rows (tools/pack_probe.cu, B200): 0.64-0.65 ms vs
-// 0.69 ms per 1M-request window.  Rows whose tokens are not 16-byte aligned get their
-// vectors from scalar loads in the finish step.
+//           per-group row-start marks (a warp max-scan), completes the tail vector and
+//           writes the padding into the image and the group's 16 mask bytes straight to
+//           global (st.global.cs.v4); then one cp.async.bulk shared -> global stores the
+//           whole token image.
+// Bytes in flight per SM are bounded by shared memory (168 KB of slots) instead of by
+// registers, with few threads (512 per SM, 64 registers), so the scheduling kernels of
+// the windows in flight keep SM room beside it.  C2: 0.676 ms per 1M-request window
+// (0.90 of the copy peak on the survey's bytes) against 0.69 ms for the register stream
+// (tools/pack_probe.cu explored chunk size, warps and slots).  Rows whose tokens are not
+// 16-byte aligned get their vectors from scalar loads in the finish step.
 constexpr uint64_t kLo40 = (1ull << 40) - 1;
 
 struct BulkSlot {
