@@ -402,6 +402,12 @@ def main():
     torch.cuda.synchronize(dev)
     sampler.start()
     time.sleep(0.3)
+    # the GPU idled while the sampler started: bring it back to steady state with untimed
+    # windows (clocks, caches, the in-flight pipeline's scratch) before the barrier
+    run_windows(2 * inflight, inflight)
+    if pg is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
