@@ -1,7 +1,8 @@
 """Run the UNMODIFIED reference (bucketsim) on a window — golden-vector generator.
 
 TEST INFRASTRUCTURE ONLY; needs /root/reference (present in the build container,
-absent on the GPU box).  It composes the reference's own public classes exactly
+absent on the GPU box) or its unmodified pip install under baseline/_ref (made by
+__graft_entry__.build(), git-ignored, shipped to the GPU box).  It composes the reference's own public classes exactly
 as SURVEY §3.4 describes the window:
 
   1. BucketSet(L_max, split_threshold[, buckets])           bucket_manager.py:79-97
@@ -27,7 +28,12 @@ from collections import deque
 
 import numpy as np
 
-REF_SRC = os.environ.get("BUCKETSIM_REF_SRC", "/root/reference/pkg/src")
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the reference sources in the build container, else the unmodified package installed
+# by `pip install --target baseline/_ref` (git-ignored; it travels to the GPU box)
+REF_SRC = os.environ.get("BUCKETSIM_REF_SRC") or next(
+    (p for p in ("/root/reference/pkg/src", os.path.join(_ROOT, "baseline", "_ref"))
+     if os.path.isdir(os.path.join(p, "bucketsim"))), "/root/reference/pkg/src")
 
 
 def available() -> bool:

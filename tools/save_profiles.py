@@ -15,7 +15,7 @@ for src, dst in (("bench.json", "bench_c2"), ("bench_c3.json", "bench_c3"), ("be
     if os.path.exists(os.path.join(S, src)):
         shutil.copy(os.path.join(S, src), os.path.join(P, f"{pre}_{dst}.json"))
 shutil.copy(os.path.join(S, "full_summary.json"), os.path.join(P, f"{pre}_ncu_c2_kernels.json"))
-for extra in ("timeline_c2.txt", "pytest_gpu.log", "smoke.log"):
+for extra in ("timeline_c2.txt", "pytest_gpu.log", "smoke.log", "reference_python_host.jsonl"):
     if os.path.exists(os.path.join(S, extra)):
         shutil.copy(os.path.join(S, extra), os.path.join(P, f"{pre}_{extra}"))
 for k in ("k_pack_bulk", "k_pack_stream", "k_histogram", "k_sort_pass", "k_dispatch", "k_size_next", "k_chain_walk"):
