@@ -145,7 +145,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   ctx->carveout_uniform = max_n <= (4 << 20) ? 100 : 0;
   if (const char* v = getenv("BS_CARVEOUT")) ctx->carveout_uniform = std::max(0, std::min(100, atoi(v)));
   if (const char* v = getenv("BS_SMALL")) ctx->small_path = atoi(v) != 0;
-  if (const char* v = getenv("BS_SMALL_TIMING")) ctx->small_timing = atoi(v) != 0;
+  if (const char* v = getenv("BS_SMALL_TIMING")) ctx->small_timing = atoi(v);
   int r = 1;
   while (((int64_t)1 << r) < max_n + 1) ++r;
   ctx->r_cap = r + 2;

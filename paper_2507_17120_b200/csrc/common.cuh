@@ -121,6 +121,15 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
   return v;
 }
 template <typename T>
+__device__ __forceinline__ T warp_incl_max(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(0xffffffffu, v, o);
+    if ((int)lane_id() >= o && t > v) v = t;
+  }
+  return v;
+}
+template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

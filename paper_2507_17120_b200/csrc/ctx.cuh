@@ -37,7 +37,7 @@ struct bs_ctx {
   int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
   int small_path = 1;       // K0 single-CTA path for small windows (BS_SMALL=0 disables)
   int small_smem_max = 0;   // its dynamic shared-memory opt-in (bytes)
-  int small_timing = 0;     // K0 phase timestamps into summary.reserved (BS_SMALL_TIMING)
+  int small_timing = 0;     // K0 phase timestamps into summary.reserved (BS_SMALL_TIMING=1 ns, 2 cycles)
   bool window_zeroed = false;  // inside a fused window call whose k_window_init zeroed the
                                // accumulators (the launchers then skip their memsets)
   std::string err;

@@ -31,9 +31,11 @@ namespace bsk {
 
 constexpr int kSmallT = 512;
 constexpr int kSmallN = 2048;
-// phase timestamps (globaltimer ns) into summary.reserved[0..7] when timing != 0
+// phase timestamps into summary.reserved[0..7]: timing 1 = globaltimer ns (its update
+// granularity is ~1 us outside a profiler), 2 = the SM cycle counter (one CTA, one SM)
 #define BS_SMALL_MARK(k) \
-  if (timing && threadIdx.x == 0) sum->reserved[k] = (int64_t)globaltimer_ns()
+  if (timing && threadIdx.x == 0) \
+    sum->reserved[k] = timing == 2 ? (int64_t)clock64() : (int64_t)globaltimer_ns()
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
@@ -44,10 +46,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 struct SmallSh {
   int64_t s64[33];
   int32_t s32[33];
-  uint32_t s32m[8 * 33];  // multi-value scans
+  uint32_t s32m[9 * 33];  // multi-value scans
   int32_t i32m[3 * 33];
   uint32_t total;
-  int64_t n_max;
+  int64_t n_max, sum_len;
   int32_t k, nruns, nb, bad;
   int64_t nch;
   int32_t passes;
@@ -92,6 +94,16 @@ struct SmallLayout {
 
 __host__ __device__ inline int64_t r16(int64_t b) { return (b + 15) & ~15LL; }
 
+// histogram rows keep one pad word per 32 entries: a thread scanning its chunk of
+// consecutive lengths (x = tid * chunk + k, chunk a power of two <= 16) then hits 32
+// distinct banks across the warp instead of 32 / chunk
+__host__ __device__ __forceinline__ int32_t hx(int32_t x) { return x + (x >> 5); }
+__host__ __device__ __forceinline__ int32_t hrow(int32_t L) { return hx(L) + 1; }
+
+// K4 ranking counters: [64 digits][17] (16 warps + 1 pad word)
+constexpr int kRankDig = 64, kRankPitch = 17;
+static_assert(kSmallN <= (kSmallT / 32) * 4 * 32, "K4 ranks at most 4 steps per warp");
+
 __host__ __device__ inline SmallLayout small_layout(int32_t n, int32_t L, int32_t C) {
   SmallLayout s;
   const int64_t n4 = 4 * (int64_t)(n + 4);
@@ -103,16 +115,64 @@ __host__ __device__ inline SmallLayout small_layout(int32_t n, int32_t L, int32_
   s.aex = r16(s.runid + n4);
   s.cs = r16(s.aex + n4);
   s.region = r16(s.cs + n + 4);
-  // K1..K4: per-class histogram -> prefix [C][L+1], total prefix P[L+1], edges e / ne
+  // K1..K4: per-class histogram -> prefix [C][L+1], total prefix P[L+1] (padded rows,
+  // hx), edges e / ne; K4's ranking counters reuse the start of the region
   s.hc = 0;
-  s.P = r16(s.hc + 4 * (int64_t)C * (L + 1));
-  s.e = r16(s.P + 4 * (int64_t)(L + 1));
+  s.P = r16(s.hc + 4 * (int64_t)C * hrow(L));
+  s.e = r16(s.P + 4 * (int64_t)hrow(L));
   s.ne = r16(s.e + 4 * (int64_t)(L + 1));
-  const int64_t phase1 = r16(s.ne + 4 * (int64_t)(L + 1));
+  int64_t phase1 = r16(s.ne + 4 * (int64_t)(L + 1));
+  if (phase1 < 4 * kRankDig * kRankPitch) phase1 = 4 * kRankDig * kRankPitch;
   // K5: 10 int32 tables of n + 2 entries and one byte table of n + 2
   const int64_t phase2 = 4 * 10 * (int64_t)(n + 2) + (n + 2) + 16;
   s.total = s.region + (phase1 > phase2 ? phase1 : phase2);
   return s;
+}
+
+// K1 epilogue: every class row of Hc becomes its exclusive prefix (Hc[c][L] = the class
+// total), P[x] = #{len < x} over all classes; one multi-value block scan for the CM
+// class sums and sum(len) (<= n * (L - 1) < 2^24: fits 32 bits)
+template <int CM>
+__device__ __forceinline__ void small_prefix(uint32_t* Hc, uint32_t* P, int32_t L, int32_t C,
+                                             uint32_t* scratch, uint32_t& tot, uint32_t& sltot) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int32_t LP = hrow(L);
+  const int chunk = (L + nt - 1) / nt;  // <= 16 (host: L <= 8192)
+  const int x0 = min(L, tid * chunk), x1 = min(L, x0 + chunk);
+  uint32_t v[CM + 1], ct[CM + 1];
+#pragma unroll
+  for (int c = 0; c <= CM; ++c) v[c] = 0;
+  for (int x = x0; x < x1; ++x) {
+    const int32_t px = hx(x);
+    uint32_t h = 0;
+#pragma unroll
+    for (int c = 0; c < CM; ++c)
+      if (c < C) { const uint32_t q = Hc[c * LP + px]; v[c] += q; h += q; }
+    v[CM] += h * (uint32_t)x;
+  }
+  block_excl_scan_k<CM + 1, uint32_t>(v, ct, scratch);
+  for (int x = x0; x < x1; ++x) {
+    const int32_t px = hx(x);
+    uint32_t sx = 0;
+#pragma unroll
+    for (int c = 0; c < CM; ++c)
+      if (c < C) {
+        const uint32_t h = Hc[c * LP + px];
+        Hc[c * LP + px] = v[c];
+        sx += v[c];
+        v[c] += h;
+      }
+    P[px] = sx;
+  }
+  tot = 0;
+#pragma unroll
+  for (int c = 0; c < CM; ++c) tot += ct[c];
+  sltot = ct[CM];
+  if (tid == 0) {
+#pragma unroll
+    for (int c = 0; c < CM; ++c)
+      if (c < C) Hc[c * LP + hx(L)] = ct[c];
+  }
 }
 
 __global__ void __launch_bounds__(kSmallT, 1)
@@ -134,7 +194,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int nwarps = nt >> 5;
   const unsigned FULL = 0xffffffffu;
-  const int32_t L = p.l_max, C = p.n_classes, L1 = L + 1;
+  const int32_t L = p.l_max, C = p.n_classes, LP = hrow(L);
   const SmallLayout lay = small_layout(n, L, C);
   int32_t* xs = reinterpret_cast<int32_t*>(smem + lay.xs);       // [n] lengths (arrival order)
   int32_t* seg = reinterpret_cast<int32_t*>(smem + lay.seg);     // [n] segment of request i
@@ -144,8 +204,8 @@ __global__ void __launch_bounds__(kSmallT, 1)
   int32_t* aex = reinterpret_cast<int32_t*>(smem + lay.aex);     // [n+1] admitted prefix
   uint8_t* cs = smem + lay.cs;                                   // [n] classes
   unsigned char* region = smem + lay.region;
-  uint32_t* Hc = reinterpret_cast<uint32_t*>(region + lay.hc);   // [C][L+1]
-  uint32_t* P = reinterpret_cast<uint32_t*>(region + lay.P);     // [L+1]
+  uint32_t* Hc = reinterpret_cast<uint32_t*>(region + lay.hc);   // [C][hrow(L)], index hx(x)
+  uint32_t* P = reinterpret_cast<uint32_t*>(region + lay.P);     // [hrow(L)], index hx(x)
   int32_t* e = reinterpret_cast<int32_t*>(region + lay.e);       // [L+1]
   int32_t* ne = reinterpret_cast<int32_t*>(region + lay.ne);     // [L+1]
   if (tid == 0) {
@@ -153,7 +213,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
     sh.wsum = 0.0;
   }
   // ---- K1 -------------------------------------------------------------------------------
-  for (int i = tid; i < C * L1; i += nt) Hc[i] = 0;
+  for (int i = tid; i < C * LP; i += nt) Hc[i] = 0;
   __syncthreads();
   {
     unsigned fl = 0;
@@ -162,55 +222,22 @@ __global__ void __launch_bounds__(kSmallT, 1)
       const int32_t c = eff_cls(cls[i], C, fl);
       xs[i] = x;
       cs[i] = (uint8_t)c;
-      atomicAdd(&Hc[c * L1 + x], 1u);
+      atomicAdd(&Hc[c * LP + hx(x)], 1u);
     }
     if (fl) atomicOr(&sh.flags, fl);
   }
   __syncthreads();
   BS_SMALL_MARK(1);
-  for (int i = tid; i < C * L; i += nt) hist[i] = Hc[(i / L) * L1 + (i % L)];
-  // every class row of Hc becomes its exclusive prefix (Hc[c][L] = the class total) and
-  // P[x] = #{len < x} over all classes = the sum of the class prefixes; sum(len) for n_max
-  uint32_t tot = 0;
+  for (int c = 0; c < C; ++c)
+    for (int x = tid; x < L; x += nt) hist[c * L + x] = Hc[c * LP + hx(x)];
   {
-    const int chunk = (L + nt - 1) / nt;  // <= 16 (host: L <= 8192)
-    const int x0 = min(L, tid * chunk), x1 = min(L, x0 + chunk);
-    uint32_t v[8], ct[8];
-    uint64_t sl = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = 0;
-    for (int x = x0; x < x1; ++x) {
-      uint32_t h = 0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < C) { const uint32_t q = Hc[c * L1 + x]; v[c] += q; h += q; }
-      sl += (uint64_t)h * (uint64_t)x;
-    }
-    block_excl_scan_k<8, uint32_t>(v, ct, sh.s32m);
-    int64_t sltot;
-    block_excl_scan<int64_t>((int64_t)sl, sh.s64, &sltot);
-    for (int x = x0; x < x1; ++x) {
-      uint32_t px = 0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < C) {
-          const uint32_t h = Hc[c * L1 + x];
-          Hc[c * L1 + x] = v[c];
-          px += v[c];
-          v[c] += h;
-        }
-      P[x] = px;
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) tot += ct[c];
-    if (tid == 0)
-      for (int c = 0; c < C; ++c) Hc[c * L1 + L] = ct[c];
-    if (tid == 0) sh.s64[32] = sltot;
-  }
-  {
+    uint32_t tot, sl;
+    if (C <= 2) small_prefix<2>(Hc, P, L, C, sh.s32m, tot, sl);
+    else if (C <= 4) small_prefix<4>(Hc, P, L, C, sh.s32m, tot, sl);
+    else small_prefix<8>(Hc, P, L, C, sh.s32m, tot, sl);
     if (tid == 0) {
-      const int64_t sltot = sh.s64[32];
-      P[L] = tot;
+      const int64_t sltot = sl;
+      P[hx(L)] = tot;
       sh.total = tot;
       int64_t nm;
       if (p.n_max > 0) {
@@ -228,6 +255,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
         }
       }
       sh.n_max = nm;
+      sh.sum_len = sltot;
       sum->total_global = tot;
       sum->sum_len_global = sltot;
       sum->n_max = nm;
@@ -288,7 +316,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
       int32_t ecnt = 0, ccnt = 0;
       for (int b = b0; b < b1; ++b) {
         const int32_t lo = e[b], up = e[b + 1], mid = (lo + up) >> 1;
-        const uint32_t c = P[up] - P[lo], s = P[mid] - P[lo];
+        const uint32_t c = P[hx(up)] - P[hx(lo)], s = P[hx(mid)] - P[hx(lo)];
         uint8_t kd = 0;
         if ((int64_t)c > n_max && (double)s > __dmul_rn(p.split_threshold, (double)c))
           kd = mid <= lo ? 2 : 1;  // 2: width-1 skip (:175-178)
@@ -350,24 +378,17 @@ __global__ void __launch_bounds__(kSmallT, 1)
     if (bucket_out) bucket_out[i] = lo;
     const int32_t blo = e[lo], bup = e[lo + 1];
     const int c = cs[i];
-    int32_t base = (int32_t)P[blo];  // requests of earlier buckets, then earlier classes
-    for (int c2 = 0; c2 < c; ++c2) base += (int32_t)(Hc[c2 * L1 + bup] - Hc[c2 * L1 + blo]);
-    const uint32_t* row = Hc + c * L1;
+    const int32_t hlo = hx(blo), hup = hx(bup);
+    int32_t base = (int32_t)P[hlo];  // requests of earlier buckets, then earlier classes
+    for (int c2 = 0; c2 < c; ++c2) base += (int32_t)(Hc[c2 * LP + hup] - Hc[c2 * LP + hlo]);
+    const uint32_t* row = Hc + c * LP;
     const int pol = small_policy(p, c);
-    int32_t g, off;
-    if (pol == BS_POLICY_SJF) {
-      g = c * L + x;
-      off = base + (int32_t)(row[x] - row[blo]);
-    } else if (pol == BS_POLICY_LJF) {
-      g = c * L + x;
-      off = base + (int32_t)(row[bup] - row[x + 1]);
-    } else {
-      g = c * L + blo;
-      off = base;
-    }
+    int32_t off;
+    if (pol == BS_POLICY_SJF) off = base + (int32_t)(row[hx(x)] - row[hlo]);
+    else if (pol == BS_POLICY_LJF) off = base + (int32_t)(row[hup] - row[hx(x + 1)]);
+    else off = base;
     seg[i] = lo * C + c;
-    goff[i] = off;
-    runid[i] = g;
+    goff[i] = off;  // the sorted offset of i's group: (class, length) or (class, bucket)
   }
   const int32_t nseg = K * C;
   for (int s2 = tid; s2 <= nseg; s2 += nt) {  // segment offsets of the drain order
@@ -375,32 +396,72 @@ __global__ void __launch_bounds__(kSmallT, 1)
     if (s2 < nseg) {
       const int b = s2 / C, c = s2 - b * C;
       const int32_t blo = e[b], bup = e[b + 1];
-      v = (int32_t)P[blo];
-      for (int c2 = 0; c2 < c; ++c2) v += (int32_t)(Hc[c2 * L1 + bup] - Hc[c2 * L1 + blo]);
+      v = (int32_t)P[hx(blo)];
+      for (int c2 = 0; c2 < c; ++c2) v += (int32_t)(Hc[c2 * LP + hx(bup)] - Hc[c2 * LP + hx(blo)]);
     }
     seg_off_out[s2] = v;
   }
   __syncthreads();
-  uint32_t* gcnt = Hc;  // per-group counters (the prefix rows are dead now)
-  for (int i = tid; i < C * L; i += nt) gcnt[i] = 0;
-  __syncthreads();
-  if (wid == 0) {  // ranks inside the groups in arrival order: one warp walks the window
-    for (int i0 = 0; i0 < n; i0 += 32) {
-      const int i = i0 + lane;
-      const bool valid = i < n;
-      const int32_t g = valid ? runid[i] : -1 - lane;
-      const unsigned peers = __match_any_sync(FULL, g);
-      const int leader = __ffs(peers) - 1;
-      uint32_t base = 0;
-      if (valid && lane == leader) {
-        base = gcnt[g];
-        gcnt[g] = base + __popc(peers);
+  {  // the drain order = the requests stably sorted by their group's offset goff[i] (< n):
+     // two LSD passes of 6-bit digits; warp w ranks its contiguous chunk (match_any per
+     // 32 requests, per-warp digit counters), one block scan of the counters digit-major
+     // gives every (digit, warp) its output base
+    int32_t* tk = runid;  // pass-0 output keys / values (dead until K5)
+    int32_t* tv = aex;
+    uint32_t* wc = reinterpret_cast<uint32_t*>(region);  // [kRankDig][kRankPitch]
+    const int CH = ((n + nwarps - 1) / nwarps + 31) & ~31;
+    const int i_lo = wid * CH, i_hi = min(n, i_lo + CH);
+    for (int pass = 0; pass < 2; ++pass) {
+      const int32_t* ik = pass ? tk : goff;
+      const int shift = pass ? 6 : 0;
+      for (int q = tid; q < kRankDig * kRankPitch; q += nt) wc[q] = 0;
+      __syncthreads();
+      int32_t loc[4], dg[4];
+#pragma unroll
+      for (int st2 = 0; st2 < 4; ++st2) {
+        dg[st2] = -1;
+        loc[st2] = 0;
+        if (i_lo + st2 * 32 < i_hi) {  // warp-uniform
+          const int i = i_lo + st2 * 32 + lane;
+          const bool valid = i < i_hi;
+          const int32_t d = valid ? (ik[i] >> shift) & (kRankDig - 1) : -1 - lane;
+          const unsigned peers = __match_any_sync(FULL, d);
+          const int leader = __ffs(peers) - 1;
+          uint32_t b0 = 0;
+          if (valid && lane == leader) {
+            b0 = wc[d * kRankPitch + wid];
+            wc[d * kRankPitch + wid] = b0 + __popc(peers);
+          }
+          __syncwarp();  // the next step's leaders read these counters
+          b0 = __shfl_sync(FULL, b0, leader);
+          dg[st2] = valid ? d : -1;
+          loc[st2] = (int32_t)b0 + __popc(peers & lanemask_lt());
+        }
       }
-      base = __shfl_sync(FULL, base, leader);
-      if (valid) perm_s[goff[i] + (int32_t)base + __popc(peers & lanemask_lt())] = i;
+      __syncthreads();
+      {  // exclusive scan over (digit, warp); kRankDig * nwarps == 2 * nt
+        const int e0 = 2 * tid, e1 = e0 + 1;
+        const int a0i = (e0 / nwarps) * kRankPitch + e0 % nwarps;
+        const int a1i = (e1 / nwarps) * kRankPitch + e1 % nwarps;
+        const int32_t a0 = (int32_t)wc[a0i], a1 = (int32_t)wc[a1i];
+        int32_t tt;
+        const int32_t ex = block_excl_scan<int32_t>(a0 + a1, sh.s32, &tt);
+        wc[a0i] = (uint32_t)ex;
+        wc[a1i] = (uint32_t)(ex + a0);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int st2 = 0; st2 < 4; ++st2) {
+        if (dg[st2] >= 0) {
+          const int i = i_lo + st2 * 32 + lane;
+          const int32_t pos = (int32_t)wc[dg[st2] * kRankPitch + wid] + loc[st2];
+          if (pass == 0) { tk[pos] = goff[i]; tv[pos] = i; }
+          else perm_s[pos] = tv[i];
+        }
+      }
+      __syncthreads();
     }
   }
-  __syncthreads();
   BS_SMALL_MARK(3);
   for (int j = tid; j < n; j += nt) perm_out[j] = perm_s[j];
   // ---- K5 -------------------------------------------------------------------------------
@@ -443,50 +504,119 @@ __global__ void __launch_bounds__(kSmallT, 1)
   __syncthreads();
   BS_SMALL_MARK(4);
   const int nruns = sh.nruns;
+  int32_t* bid = seg;  // [n] batch of each position (seg is dead once the runs are known)
   const int64_t Hd = p.current_safe - p.pledged;
   const bool padded = p.accounting == BS_ACCOUNTING_PADDED;
   const int64_t T = Hd > 0 ? Hd / p.kv_bytes_per_token : 0;
-  // A: the form_batch calls of every segment run (one warp per run, 32 positions per
-  //    step): where each call that admits something starts, and where the drain stops
-  for (int r = wid; r < nruns; r += nwarps) {
-    const int32_t a = run_start[r], b = run_start[r + 1];
-    int32_t cnt = 0, m = 0, sm = 0, call = a, pos = a, pend = b;
-    while (Hd > 0 && pos < b) {
-      const int32_t j = pos + lane;
-      const bool valid = j < b;
-      const int32_t x = valid ? xs[perm_s[j]] : 0;
-      const bool adm = valid && (int64_t)x <= S;
-      int32_t pc = adm, pm = adm ? x : 0, ps = adm ? x : 0;  // lane prefix over admissible
+  // A: the form_batch calls of every segment run: where each call that admits something
+  //    starts, and where the drain stops.  Every position first learns, by its own scan
+  //    of at most kNextCap positions, where a call starting there would end; one warp per
+  //    run then hops from call to call, and only a call longer than the cap is re-scanned
+  //    by the warp, 32 positions per step
+  int32_t* xd = bn;    // [n] lengths in drain order (bn / bmx are free until the batch tables)
+  int32_t* nxt = bmx;  // [n] end of the call starting at j: k, or -1 - k when it admits
+                       // nothing (the drain stops at k), or kNxtUnknown past the cap
+  constexpr int kNextCap = 32;
+  // the scan's products stay below 8192 * 33 < 2^19: clamped budgets compare the same
+  const int32_t S32 = S < (1 << 30) ? (int32_t)S : (1 << 30);
+  const int32_t T32 = T < (1 << 30) ? (int32_t)T : (1 << 30);
+  constexpr int32_t kNxtUnknown = INT32_MIN;
+  for (int j = tid; j < n; j += nt) xd[j] = xs[perm_s[j]];
+  __syncthreads();
+  BS_SMALL_MARK(8);
+  // the per-position scan pays only where the average call (budget / mean length) is
+  // shorter than the cap; otherwise every call is found by the warp
+  const bool prescan = Hd > 0 && (int64_t)T * sh.total < (int64_t)kNextCap * sh.sum_len;
+  if (prescan) {
+    for (int j = tid; j < n; j += nt) {
+      const int32_t b = run_start[runid[j] + 1];
+      const int32_t kend = min(b, j + kNextCap);
+      int32_t cnt = 0, m = 0, sm = 0, res = kNxtUnknown;
+      for (int32_t k0 = j; k0 < kend; k0 += 8) {
+        int32_t xv[8];  // eight lengths loaded ahead (lengths are >= 0; -1 = past the end)
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t tc = __shfl_up_sync(FULL, pc, o);
-        const int32_t tm = __shfl_up_sync(FULL, pm, o);
-        const int32_t ts = __shfl_up_sync(FULL, ps, o);
-        if (lane >= o) { pc += tc; pm = tm > pm ? tm : pm; ps += ts; }
-      }
-      const int32_t cm = pm > m ? pm : m;
-      const bool viol = adm && (padded ? (int64_t)cm * (cnt + pc) : (int64_t)(sm + ps)) > T;
-      const unsigned vb = __ballot_sync(FULL, viol);
-      const int f = vb ? __ffs(vb) - 1 : min(32, b - pos);  // lanes < f are consumed
-      if (f > 0) {
-        cnt += __shfl_sync(FULL, pc, f - 1);
-        m = max(m, __shfl_sync(FULL, pm, f - 1));
-        sm += __shfl_sync(FULL, ps, f - 1);
-      }
-      pos += f;
-      if (vb) {
-        if (cnt == 0) {  // this call admits nothing: the drain of the segment stops here
-          pend = pos;
+        for (int u = 0; u < 8; ++u) xv[u] = k0 + u < kend ? xd[k0 + u] : -1;
+        int hit = 8, c_hit = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // 32-bit: x < 8192, cnt <= kNextCap, S32 / T32 clamped
+          const int32_t x = xv[u];
+          const bool adm = x >= 0 && x <= S32;  // rejected ones are skipped
+          const int32_t cm = x > m ? x : m;
+          const bool viol = adm && (padded ? cm * (cnt + 1) : sm + x) > T32;
+          if (viol && hit == 8) { hit = u; c_hit = cnt; }
+          if (adm && hit == 8) { ++cnt; m = cm; sm += x; }
+        }
+        if (hit < 8) {
+          res = c_hit ? k0 + hit : -1 - (k0 + hit);
           break;
         }
-        if (lane == 0) bflag[call] = 1;  // the call closes its batch; the next starts at pos
-        call = pos;
-        cnt = m = sm = 0;
       }
+      if (res == kNxtUnknown && kend == b) res = cnt ? b : -1 - b;
+      nxt[j] = res;
     }
-    if (Hd > 0 && pend == b && cnt > 0 && lane == 0) bflag[call] = 1;
+  }
+  __syncthreads();
+  BS_SMALL_MARK(9);
+  for (int r = wid; r < nruns; r += nwarps) {
+    const int32_t a = run_start[r], b = run_start[r + 1];
+    // run order: SJF ascending lengths, LJF descending, FCFS arrival (K4)
+    const int pol = small_policy(p, run_seg[r] % C);
+    int32_t pos = a, pend = b;
     if (Hd <= 0) pend = a;  // form_batch returns None before touching the queue (:150-152)
+    while (Hd > 0 && pos < b) {
+      int32_t nx = prescan ? nxt[pos] : kNxtUnknown;
+      if (nx == kNxtUnknown) {  // a call longer than the cap
+        int32_t cnt = 0, m = 0, sm = 0, q = pos;
+        for (;;) {
+          if (q >= b) { nx = cnt ? b : -1 - b; break; }
+          const int32_t j = q + lane;
+          const bool valid = j < b;
+          const int32_t x = valid ? xd[j] : 0;
+          const bool adm = valid && (int64_t)x <= S;
+          int32_t pc = adm, pm = adm ? x : 0, ps = adm ? x : 0;  // lane prefix over admissible
+          if (__all_sync(FULL, adm || !valid)) {
+            // every valid lane admissible (the valid lanes are a prefix): the count is the
+            // lane, the padded accounting needs only the running max — the own length in
+            // an ascending run, the step's first in a descending one — the exact one only
+            // the sum
+            pc = lane + 1;
+            if (padded) {
+              if (pol == BS_POLICY_LJF) pm = __shfl_sync(FULL, x, 0);
+              else if (pol != BS_POLICY_SJF) pm = warp_incl_max(pm);
+            } else {
+              ps = warp_incl_scan(ps);
+            }
+          } else {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int32_t tc = __shfl_up_sync(FULL, pc, o);
+              const int32_t tm = __shfl_up_sync(FULL, pm, o);
+              const int32_t ts = __shfl_up_sync(FULL, ps, o);
+              if (lane >= o) { pc += tc; pm = tm > pm ? tm : pm; ps += ts; }
+            }
+          }
+          const int32_t cm = pm > m ? pm : m;
+          const bool viol = adm && (padded ? (int64_t)cm * (cnt + pc) : (int64_t)(sm + ps)) > T;
+          const unsigned vb = __ballot_sync(FULL, viol);
+          const int f = vb ? __ffs(vb) - 1 : min(32, b - q);  // lanes < f are consumed
+          if (f > 0) {
+            cnt += __shfl_sync(FULL, pc, f - 1);
+            m = max(m, __shfl_sync(FULL, pm, f - 1));
+            sm += __shfl_sync(FULL, ps, f - 1);
+          }
+          q += f;
+          if (vb) { nx = cnt ? q : -1 - q; break; }
+        }
+      }
+      if (nx < 0) {  // this call admits nothing: the drain of the segment stops here
+        pend = -1 - nx;
+        break;
+      }
+      bflag[pos] = 1;  // the call closes its batch; the next starts at nx (every lane: no branch)
+      pos = nx;
+    }
     if (lane == 0) run_pend[r] = pend;
+
   }
   __syncthreads();
   BS_SMALL_MARK(5);
@@ -506,6 +636,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
     int32_t q = sv[0], qa = sv[1];
     for (int j = j0; j < j1; ++j) {
       if (bflag[j]) bpos[q++] = j;
+      bid[j] = q - 1;  // the last call start <= j: the batch of j when j is admitted
       aex[j] = qa;
       qa += j < run_pend[runid[j]] && (int64_t)xs[perm_s[j]] <= S;
     }
@@ -524,11 +655,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
   for (int j = tid; j < n; j += nt) {
     const int32_t x = xs[perm_s[j]];
     if (!(j < run_pend[runid[j]] && (int64_t)x <= S)) continue;
-    int lo = 0, hi = nb - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (bpos[mid] <= j) lo = mid; else hi = mid - 1;
-    }
+    const int lo = bid[j];
     atomicAdd(&bn[lo], 1);
     atomicMax(&bmx[lo], x);
     atomicAdd(&bsm[lo], x);
@@ -576,11 +703,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
       req_row[idx] = -1;
       ++rej;
     } else {
-      int lo = 0, hi = nb - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (bpos[mid] <= j) lo = mid; else hi = mid - 1;
-      }
+      const int lo = bid[j];
       const int32_t row = aex[j] - aex[bpos[lo]];
       req_batch[idx] = lo;
       req_row[idx] = row;

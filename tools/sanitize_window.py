@@ -24,14 +24,15 @@ if "--paths" in sys.argv:
     os.environ["BS_OUTCOME_PARTS"] = "3"
     cases = [("c2", 30000, 32), ("c3", 40000, 4)]
 if "--small" in sys.argv:
-    cases = [("c2", 3000, 32), ("c3", 3000, 1), ("c4", 300, 32)]
+    # + windows of <= 2048 requests, which take K0 (k_window_small)
+    cases = [("c2", 3000, 32), ("c3", 3000, 1), ("c4", 300, 32), ("c1", 1000, 32), ("c2", 2000, 4)]
 for name, n, align in cases:
     cfg, lens, cls = W.make_window(name, n=n, seed=11)
     tok_off, tokens = W.token_store(lens, align=align)
     s = WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
                         policies=cfg.policies, kv_bytes_per_token=cfg.kvpt,
                         current_safe=cfg.current_safe, device=torch.device("cuda", 0),
-                        dispatch=True)
+                        dispatch=not (n <= 2048 and cfg.l_max <= 8192))  # K0 has no K7
     h = s.schedule(*(torch.as_tensor(a).cuda() for a in (lens, cls, tok_off, tokens))).to_host()
     assert int(h["summary"]["flags"]) == 0
     print(name, n, align, int(h["summary"]["n_batches"]))
