@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
     seg_off_out[s2] = v;
   }
   __syncthreads();
+  BS_SMALL_MARK(10);
   {  // the drain order = the requests stably sorted by their group's offset goff[i] (< n):
      // two LSD passes of 6-bit digits; warp w ranks its contiguous chunk (match_any per
      // 32 requests, per-warp digit counters), one block scan of the counters digit-major
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
         }
       }
       __syncthreads();
+      if (pass == 0) BS_SMALL_MARK(11);
     }
   }
   BS_SMALL_MARK(3);

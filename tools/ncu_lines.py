@@ -20,7 +20,7 @@ for r in csv.reader(io.StringIO(out)):
     if hdr and len(r) == len(hdr) and r[0].isdigit():
         lines.append((f, r))
 ie = hdr.index("Instructions Executed")
-wf = hdr.index("L1 Wavefronts Shared")
+wf = hdr.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in hdr else hdr.index("Instructions Executed")
 st = hdr.index("Warp Stall Sampling (All Samples)")
 g = lambda r, i: float(r[i] or 0)  # noqa: E731
 tot = sum(g(r, ie) for _, r in lines) or 1
