@@ -4,8 +4,9 @@ both implementations of the drop-in surface.
 Every test restates one test of pkg/tests/test_bucket_manager.py or
 pkg/tests/test_batch_controller.py (file:line in each docstring) against a namespace
 `M` that is either
-  * "reference" — the live bucketsim package (build container only: it reads
-    /root/reference, so it is CPU-marked and skipped where that tree is absent), or
+  * "reference" — the live bucketsim package (/root/reference in the build container,
+    or its unmodified pip install in baseline/_ref; CPU-marked, skipped where neither
+    exists), or
   * "b200"      — paper_2507_17120_b200 (compat.BucketSet / BatchController with
     adjust_buckets on K2 and form_batch on K4+K5; GPU-marked).
 Passing on "reference" shows the restatement says what the reference's test says;
@@ -22,7 +23,8 @@ from types import SimpleNamespace
 import numpy as np
 import pytest
 
-REF_SRC = os.environ.get("BUCKETSIM_REF_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle.ref_compose import REF_SRC  # noqa: E402  (/root/reference, else baseline/_ref)
 
 
 def _reference_ns():
