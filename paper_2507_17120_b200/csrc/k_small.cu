@@ -13,15 +13,20 @@
 //   K3  bucket id per request                     bucket_manager.py:110-131
 //   K4  drain order as a stable counting sort: every request's group — (class, length)
 //       for SJF / LJF classes, (class, bucket) for FCFS — has its sorted offset in the
-//       per-class length prefix sums; the rank inside the group comes from one warp
-//       walking the requests in arrival order (match_any + per-group counters)
+//       per-class length prefix sums; the drain order is the requests stably sorted by
+//       that offset: two LSD radix passes (6-bit digits) on all 16 warps, match_any
+//       ranks per warp chunk, one block scan of the (digit, warp) counters
 //                                                 batch_controller.py:33-41,154-156
-//   K5  form_batch drained per segment: one warp per segment run finds where each call
-//       starts and where the drain stops, 32 positions per step (lane prefix of
-//       count / max / sum, first violating lane by ballot); then every position learns
-//       its batch and row from prefix sums, the batch statistics come from shared
-//       atomics, the offsets from block scans; oversize rejections, the
-//       pledged-headroom stop, waste_ratio in float64
+//   K5  form_batch drained per segment: where each call starts and where the drain
+//       stops.  When the average call is short (budget / mean length < 32 requests)
+//       every position first scans ahead for the end of a call starting there, and one
+//       warp per segment run hops call to call; calls past the scan's reach (and every
+//       call otherwise) are found by the warp 32 positions per step (lane prefix of
+//       count / max / sum — none needed for an ascending / descending run under the
+//       padded accounting — first violating lane by ballot).  Then every position
+//       learns its batch from the call-start flag scan and its row from prefix sums,
+//       the batch statistics come from shared atomics, the offsets from block scans;
+//       oversize rejections, the pledged-headroom stop, waste_ratio in float64
 //                                                 batch_controller.py:136-191; memory_model.py:92-100
 // and leaves the row map / piece prefix K6 reads, so the pack launches right after.
 // Dispatch order (K7) and sharded windows take the multi-kernel path.
