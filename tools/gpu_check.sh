@@ -19,6 +19,7 @@ timeout 600 python bench.py --config c3 --steps 20 --no-cpu-baseline > $OUT/benc
 timeout 600 python bench.py --config c4 --steps 20 --no-cpu-baseline > $OUT/bench_c4.json 2> $OUT/bench_c4.err
 timeout 600 python bench.py --config c1 --steps 200 > $OUT/bench_c1.json 2> $OUT/bench_c1.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+timeout 300 python tools/small_timing.py 2 > $OUT/k0_phases.txt 2>&1
 timeout 600 python tools/ref_python_bench.py --out $OUT/reference_python_host.jsonl > /dev/null 2> $OUT/reference_python_host.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
