@@ -24,7 +24,7 @@ for name, n in (("c1", 1000), ("c2", 2000), ("c2", 500)):
         r = s.schedule(lens, cls)
     raw = s.summary.cpu().numpy().view(np.int64)
     t = raw[18:30]
-    print(name, n, "phase us:", [round((t[i + 1] - t[i]) / scale, 2) for i in range(7)],
+    print(name, n, "phase us:", [float(round((t[i + 1] - t[i]) / scale, 2)) for i in range(7)],
           "total", round((t[7] - t[0]) / scale, 2), r.summary()["n_batches"],
           "| K5-A: prep", round((t[8] - t[4]) / scale, 2), "scan", round((t[9] - t[8]) / scale, 2),
           "walk", round((t[5] - t[9]) / scale, 2), "| K3", round((t[10] - t[2]) / scale, 2),
