@@ -542,7 +542,8 @@ def main():
                     landed.append(ev)
             for ev in landed:
                 comp.wait_event(ev)
-            sched.schedule(d_l, d_c, d_o, d_t, sync=False, check=False)
+            # one captured graph per input set (the scheduler keeps both)
+            sched.schedule(d_l, d_c, d_o, d_t, sync=False, check=False, graph=use_graph)
             freed[i & 1].record(comp)
             h_rb.copy_(sched.req_batch[:n], non_blocking=True)
             h_bt.copy_(sched.batches_raw[:64 * nb], non_blocking=True)

@@ -17,6 +17,7 @@ windows) all-reduces the length histogram over NCCL.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 from dataclasses import dataclass
 
@@ -291,8 +292,9 @@ class WindowScheduler:
             self.init_edges = torch.as_tensor(e).to(dev)
             self.k_init = len(e) - 1
         self.with_mask = with_mask
-        self._graph = None
-        self._graph_key = None
+        # captured window graphs by input buffers (a double-buffered serving loop
+        # alternates two input sets), least recently used first
+        self._graphs = collections.OrderedDict()
         self.out_tokens = None
         self.out_mask = None
         self.pack_capacity = 0
@@ -336,8 +338,7 @@ class WindowScheduler:
                     self.k_init = len(e) - 1
                     changed = True
         if changed:
-            self._graph = None
-            self._graph_key = None
+            self._graphs.clear()
         return self
 
     # ------------------------------------------------------------------------
@@ -388,12 +389,26 @@ class WindowScheduler:
         self.collective = "nccl"
         if self.hist_global is None:
             self.hist_global = torch.zeros_like(self.hist)
-        self._graph = None
+        self._graphs.clear()
+
+    _GRAPHS = 4  # captured graphs kept per scheduler
+
+    def _graph_for(self, key):
+        g = self._graphs.get(key)
+        if g is not None:
+            self._graphs.move_to_end(key)
+        return g
+
+    def _keep_graph(self, key, g):
+        self._graphs[key] = g
+        while len(self._graphs) > self._GRAPHS:
+            self._graphs.popitem(last=False)
 
     def _ensure_pack(self, cap: int):
         if cap <= self.pack_capacity:
             return
         cap = (cap + 63) // 64 * 64
+        self._graphs.clear()  # captured graphs write the outputs being replaced
         self.out_tokens = torch.empty(cap, dtype=torch.int32, device=self.device)
         self.out_mask = torch.empty(cap, dtype=torch.uint8, device=self.device) if self.with_mask else None
         self.pack_capacity = cap
@@ -483,8 +498,8 @@ class WindowScheduler:
             key = (lens.data_ptr(), cls.data_ptr(), n,
                    tok_off.data_ptr() if pack else 0, tokens.data_ptr() if pack else 0,
                    self.pack_capacity)
-            if self._graph is None or self._graph_key != key:
-                self._graph = None
+            g = self._graph_for(key)
+            if g is None:
                 torch.cuda.synchronize(dev)
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, capture_error_mode="thread_local"):
@@ -493,8 +508,8 @@ class WindowScheduler:
                         io_g.hist_global = _ptr(self.hist_global)
                     N.check(lib.bs_window_schedule(self.ctx.ptr, C.byref(io_g), C.byref(p),
                                                    _stream_handle(dev)), self.ctx.ptr)
-                self._graph, self._graph_key = g, key
-            self._graph.replay()
+                self._keep_graph(key, g)
+            g.replay()
             res = WindowResult(self, n, pack)
             if sync:
                 torch.cuda.current_stream(dev).synchronize()
@@ -517,8 +532,8 @@ class WindowScheduler:
             key = ("from_hist", lens.data_ptr(), cls.data_ptr(), n,
                    tok_off.data_ptr() if pack else 0, tokens.data_ptr() if pack else 0,
                    self.pack_capacity)
-            if self._graph is None or self._graph_key != key:
-                self._graph = None
+            g = self._graph_for(key)
+            if g is None:
                 torch.cuda.synchronize(dev)
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, capture_error_mode="thread_local"):
@@ -526,8 +541,8 @@ class WindowScheduler:
                     io_g.hist_global = _ptr(self.hist_global)
                     N.check(lib.bs_window_from_hist(self.ctx.ptr, C.byref(io_g), C.byref(p),
                                                     _stream_handle(dev)), self.ctx.ptr)
-                self._graph, self._graph_key = g, key
-            self._graph.replay()
+                self._keep_graph(key, g)
+            g.replay()
             res = WindowResult(self, n, pack)
             if sync:
                 torch.cuda.current_stream(dev).synchronize()
@@ -691,6 +706,6 @@ class WindowScheduler:
     def close(self):
         """Release the context scratch, the captured graph and the output buffers."""
         self.ctx.close()
-        self._graph = None
+        self._graphs.clear()
         self.out_tokens = self.out_mask = None
         self.pack_capacity = 0
