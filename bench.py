@@ -195,41 +195,30 @@ def run_reference(args, rank, world):
 def reference_python_leg(args, lens, cls, cfg):
     """The UNMODIFIED reference itself (bucketsim's classes composed as SURVEY §3.4,
     oracle/ref_compose.py) timed on this host, one thread pinned to one core, on the
-    leading --ref-python-sample requests of the arm's window.  Needs
-    its pip install in baseline/_ref (made by __graft_entry__.build()); reported beside
-    the port, not as the line's value.  Runs in a child process so the pin does not
-    touch the arm's threads."""
-    import subprocess
+    arm's window (or a --ref-python-sample-request window of the config), checked
+    against the oracle port: tools/ref_python_bench.py in a child process (the pin stays
+    out of this process).  Needs the reference package: /root/reference, or its pip
+    install in baseline/_ref (made by __graft_entry__.build()).  Reported beside the
+    port, not as the line's value."""
     n = min(len(lens), args.ref_python_sample)
-    code = (
-        "import json,os,sys,time,platform\n"
-        f"sys.path.insert(0,{ROOT!r})\n"
-        "from oracle import ref_compose as R\n"
-        "from paper_2507_17120_b200 import workloads as W\n"
-        "if not R.available(): print(json.dumps({'unavailable':'reference package not installed "
-        "(baseline/_ref)'})); raise SystemExit\n"
-        "core=sorted(os.sched_getaffinity(0))[0]; os.sched_setaffinity(0,{core})\n"
-        f"cfg,lens,cls=W.make_window({args.config!r},n={len(lens)},seed=1234)\n"
-        f"lens,cls=lens[:{n}],cls[:{n}]\n"
-        "t0=time.perf_counter()\n"
-        "r=R.reference_window(lens,cls,l_max=cfg.l_max,n_classes=cfg.n_classes,"
-        "policies=cfg.policies,theta=cfg.theta,adjust=cfg.adjust,init_edges=cfg.init_edges,"
-        "kvpt=cfg.kvpt,current_safe=cfg.current_safe,accounting=cfg.accounting)\n"
-        "dt=time.perf_counter()-t0\n"
-        f"print(json.dumps({{'value':{n}/dt,'unit':{UNIT!r},'cores':1,'seconds':dt,"
-        f"'requests':{n},'batches':int(len(r['batch_meta'])),'nproc':os.cpu_count(),"
-        "'kind':'reference (bucketsim, unmodified, pure Python)'}))\n")
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "ref_python_bench.py"),
+           "--window", f"{args.config}:{n}"]
     try:
-        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                           timeout=600, env=dict(os.environ, OMP_NUM_THREADS="1"))
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                           env=dict(os.environ, OMP_NUM_THREADS="1"))
         ln = [x for x in r.stdout.splitlines() if x.startswith("{")]
-        out = json.loads(ln[-1]) if ln else {"unavailable": (r.stderr or "no output")[-300:]}
+        if not ln:
+            return {"unavailable": (r.stderr or "no output").strip().splitlines()[-1][-300:]}
+        d = json.loads(ln[-1])
     except subprocess.TimeoutExpired:
-        out = {"unavailable": "timed out after 600 s"}
-    if "value" in out:
-        out["sample"] = (f"{args.config} window, first {n} of its {len(lens)} requests, "
-                         "one run (assign, adjust_buckets fixpoint, form_batch drain)")
-    return out
+        return {"unavailable": "timed out after 900 s"}
+    return {"value": d["requests_per_s"], "unit": UNIT, "cores": 1, "seconds": d["seconds"],
+            "requests": d["requests"], "batches": d["batches"], "nproc": d["nproc"],
+            "oracle_parity": d["oracle_parity"],
+            "kind": "reference (bucketsim, unmodified, pure Python)",
+            "sample": f"{args.config} window of {n} requests (seed 1234: the arm's own window "
+                      f"when {n} = {len(lens)}), one run (assign, adjust_buckets fixpoint, "
+                      "form_batch drain), checked against the oracle port"}
 
 
 def _free_port() -> int:

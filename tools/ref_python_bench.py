@@ -56,12 +56,18 @@ def main():
     ap.add_argument("--repeats", type=int, default=5, help="runs per window below 100k requests")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--out", default=None, help="also append the lines to this file")
+    ap.add_argument("--window", default=None, metavar="CONFIG:N",
+                    help="time only this window (e.g. c2:1000000), one run")
     a = ap.parse_args()
     assert ref_compose.available(), ("needs the reference: /root/reference or baseline/_ref "
                                      "(run __graft_entry__.build() in the build container)")
     core = sorted(os.sched_getaffinity(0))[0]
     os.sched_setaffinity(0, {core})                 # one core, as BASELINE.md §4.1 states
     runs = [("c1", 1_000)] + [("c2", n) for n in a.sizes]
+    if a.window:
+        name, n = a.window.split(":")
+        runs = [(name, int(n))]
+        a.repeats = 1
     out = open(a.out, "a") if a.out else None
     for name, n in runs:
         cfg, lens, cls = W.make_window(name, n=n, seed=1234)
