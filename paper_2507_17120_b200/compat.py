@@ -203,6 +203,51 @@ class Bucket:
         self._dq = deque(r for r in self._dq if id(r) not in dead)
         self._dead = set()
 
+    @classmethod
+    def _split_of(cls, b: "Bucket", mid: int) -> tuple["Bucket", "Bucket"]:
+        """The stable partition of `b` at `mid` (bucket_manager.py:171-188) with both
+        children's aggregates (short counts, OFFLINE mass, ONLINE heap) gathered in the
+        same single pass over the parent's requests."""
+        kind: dict = {}  # task-class object -> 1 online, 2 offline, 0 other
+        parts = []
+        for lo, up in ((b.low, mid), (mid, b.up)):
+            c = cls.__new__(cls)
+            c.low, c.up, c._counts = lo, up, b._counts
+            c._dq, c._dead, c._version, c._drains, c._gone = deque(), set(), 0, {}, {}
+            c.mid = (lo + up) // 2
+            parts.append(c)
+        left, right = parts
+        lq, rq = left._dq.append, right._dq.append
+        lmid, rmid = left.mid, right.mid
+        l_short = r_short = l_off = r_off = 0
+        l_on, r_on = [], []
+        for r in b.requests:
+            x = r.input_len
+            tc = r.task_class
+            k = kind.get(tc)
+            if k is None:
+                k = kind[tc] = 1 if is_online(tc) else (2 if is_offline(tc) else 0)
+            if x < mid:
+                lq(r)
+                if x < lmid:
+                    l_short += 1
+                if k == 2:
+                    l_off += x
+                elif k == 1:
+                    l_on.append((r.arrival_time, r.id))
+            else:
+                rq(r)
+                if x < rmid:
+                    r_short += 1
+                if k == 2:
+                    r_off += x
+                elif k == 1:
+                    r_on.append((r.arrival_time, r.id))
+        for c, sc, off, on in ((left, l_short, l_off, l_on), (right, r_short, r_off, r_on)):
+            heapq.heapify(on)
+            c.short_count, c._offline_mass, c._online, c._n = sc, off, on, len(c._dq)
+        return left, right
+
     def _reset_aggregates(self) -> None:
         live = [r for r in self._dq if id(r) not in self._dead] if self._dead else self._dq
         self._n = len(live)
@@ -380,10 +425,8 @@ class BucketSet:
             if mid is None:
                 new_buckets.append(b)
                 continue
-            reqs = b.requests
-            left = Bucket(b.low, mid, deque(r for r in reqs if r.input_len < mid), b._counts)
-            right = Bucket(mid, b.up, deque(r for r in reqs if r.input_len >= mid), b._counts)
-            self.requests_moved += len(reqs)
+            left, right = Bucket._split_of(b, mid)
+            self.requests_moved += len(left) + len(right)
             new_buckets.extend((left, right))
         self.buckets = new_buckets
         assert self.edges() == new_edges

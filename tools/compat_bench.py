@@ -1,7 +1,8 @@
 """Per-call latency of the stateful drop-in at queue sizes the
 simulator reaches: adjust_buckets (one Alg. 1 pass, K1 + K2 on the GPU) and form_batch
 (K4 + K5 on the GPU) on a BucketSet holding Q queued requests, against the reference's
-own classes when they are importable (build container only; the GPU box has no copy).
+own classes (from /root/reference, or its unmodified install in baseline/_ref, which
+ships to the GPU box), so both run on the same host.
 
     python tools/compat_bench.py [--q 10000 100000] [--reps 20]
 Prints one JSON line per queue size."""
@@ -23,7 +24,8 @@ ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
 a = ap.parse_args()
 
 if a.impl == "reference":
-    sys.path.insert(0, "/root/reference/pkg/src")
+    from oracle.ref_compose import REF_SRC
+    sys.path.insert(0, REF_SRC)
     sys.dont_write_bytecode = True
     from bucketsim.batch_controller import BatchController, DispatchPolicy, MemoryAccounting
     from bucketsim.bucket_manager import BucketSet
@@ -50,7 +52,7 @@ def build(q, seed=3):
 
 
 for q in a.q:
-    t_adj, t_form, t_steady, nb = [], [], [], 0
+    t_adj, t_form, t_steady, t_drain, nb, calls = [], [], [], [], 0, 0
     for rep in range(a.reps):
         bs, ctl = build(q, seed=3 + rep)
         n_max = ctl.current_n_max(bs)
@@ -71,8 +73,18 @@ for q in a.q:
         plan = ctl.form_batch(bs.buckets[big], DispatchPolicy.SJF, task_class=TaskClass.OFFLINE)
         t_form.append(time.perf_counter() - t0)
         nb = len(plan) if plan is not None else 0
+        # the rest of that bucket's offline drain, call by call (the simulator's pattern)
+        calls = 1
+        t0 = time.perf_counter()
+        while plan is not None:
+            plan = ctl.form_batch(bs.buckets[big], DispatchPolicy.SJF, task_class=TaskClass.OFFLINE)
+            calls += 1
+        t_drain.append(time.perf_counter() - t0)
     print(json.dumps({"impl": a.impl, "queue": q, "buckets": len(bs.buckets),
                       "adjust_first_pass_ms_median": 1e3 * float(np.median(t_adj)),
                       "adjust_steady_ms_median": 1e3 * float(np.median(t_steady)),
                       "form_batch_ms_median": 1e3 * float(np.median(t_form)),
-                      "batch_size": nb, "reps": a.reps}))
+                      "batch_size": nb, "drain_calls": calls,
+                      "drain_rest_ms_median": 1e3 * float(np.median(t_drain)),
+                      "reps": a.reps, "host": os.uname().nodename, "nproc": os.cpu_count()}),
+          flush=True)
