@@ -18,6 +18,7 @@ ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--no-pack", action="store_true")
 ap.add_argument("--dispatch", action="store_true")
 ap.add_argument("--no-mask", action="store_true")
+ap.add_argument("--policies", default=None, help="override, e.g. fcfs,sjf,sjf,sjf")
 a = ap.parse_args()
 cfg, lens_np, cls_np = W.make_window(a.config, n=a.n, seed=1234)
 dev = torch.device("cuda", 0)
@@ -26,8 +27,12 @@ cls = torch.as_tensor(cls_np).to(dev)
 tok_off = tokens = None
 if not a.no_pack:
     tok_off, tokens = W.token_store_device(lens)
+pol = cfg.policies
+if a.policies:
+    names = {"fcfs": 0, "sjf": 1, "ljf": 2}
+    pol = tuple(names[x] for x in a.policies.split(","))
 s = WindowScheduler(max_requests=len(lens_np), max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
-                    policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
+                    policies=pol, split_threshold=cfg.theta, adjust=cfg.adjust,
                     buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
                     current_safe=cfg.current_safe, accounting=cfg.accounting, device=dev,
                     dispatch=a.dispatch, with_mask=not a.no_mask)
