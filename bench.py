@@ -344,15 +344,36 @@ def main():
     tok_off, tokens = W.token_store_device(lens, seed=rank)
     torch.cuda.synchronize(dev)
     free0 = torch.cuda.mem_get_info(dev)[0]
-    sched = WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
-                            policies=cfg.policies, split_threshold=cfg.theta, adjust=cfg.adjust,
-                            buckets=cfg.init_edges, kv_bytes_per_token=cfg.kvpt,
-                            current_safe=cfg.current_safe, accounting=cfg.accounting,
-                            device=dev, process_group=pg, dispatch=args.dispatch,
-                            collective=args.collective)
-    # first window sizes the reusable packed-output buffer
-    l_a = sched.ctx.launches
-    res = sched.schedule(lens, cls, tok_off, tokens)
+
+    def make_sched():
+        return WindowScheduler(max_requests=n, max_seq_len=cfg.l_max, n_classes=cfg.n_classes,
+                               policies=cfg.policies, split_threshold=cfg.theta,
+                               adjust=cfg.adjust, buckets=cfg.init_edges,
+                               kv_bytes_per_token=cfg.kvpt, current_safe=cfg.current_safe,
+                               accounting=cfg.accounting, device=dev, process_group=pg,
+                               dispatch=args.dispatch, collective=args.collective)
+
+    # first window sizes the reusable packed-output buffer.  If the library's own NCCL
+    # communicator cannot be set up on some rank (e.g. libnccl not resolvable), every rank
+    # falls back to torch.distributed's all-reduce between K1 and K2, and the line says so
+    fallback = None
+    try:
+        sched = make_sched()
+        res = sched.schedule(lens, cls, tok_off, tokens)
+        failed = 0
+    except Exception as err:  # noqa: BLE001 - reported in the line, then retried
+        failed, fallback = 1, f"collective {args.collective} failed ({type(err).__name__}: {err})"
+    if pg is not None and args.collective == "nccl":
+        flag = torch.tensor([failed], device=dev)
+        dist.all_reduce(flag)
+        if int(flag.item()) and args.collective != "torch":
+            fallback = fallback or "collective nccl failed on another rank"
+            args.collective = "torch"
+            print(f"bench: {fallback}; using collective torch", file=sys.stderr, flush=True)
+            sched = make_sched()
+            res = sched.schedule(lens, cls, tok_off, tokens)
+    elif failed:
+        raise RuntimeError(fallback)
     s0 = res.summary()
     l_b = sched.ctx.launches
     res = sched.schedule(lens, cls, tok_off, tokens)
@@ -619,7 +640,7 @@ def main():
         "inflight": inflight,
         "window_latency_ms": window_latency_ms,
         "c1": None if c1_ms is None else {
-            "collective": args.collective, "ms_per_window": c1_ms,
+            "collective": args.collective, "ms_per_window": c1_ms, "fallback": fallback,
             "bytes": 4 * cfg.l_max * cfg.n_classes,
             "what": "all-reduce (sum) of the uint32 [classes x l_max] length histogram"},
         "clocks": clocks,
