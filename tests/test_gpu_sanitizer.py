@@ -17,7 +17,8 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 
 @pytest.mark.parametrize("tool,args", [("memcheck", []), ("memcheck", ["--paths"]),
-                                       ("racecheck", ["--small"]), ("synccheck", ["--small"])])
+                                       ("racecheck", ["--small"]), ("synccheck", ["--small"]),
+                                       ("racecheck", ["--k0"]), ("memcheck", ["--k0"])])
 def test_sanitizer_clean(tool, args):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
