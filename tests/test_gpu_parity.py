@@ -144,6 +144,25 @@ def test_c2_full_1m_bit_exact():
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)
 
 
+def test_fullsize_windows_match_reference_hashes():
+    """The CUDA path against the unmodified reference directly at the bench's C2 window
+    (1M requests, seed 1234) and a C1 window: sha256 of every canonical result array
+    equals the reference's (tests/golden/fullsize_reference.json)."""
+    import json
+
+    from oracle.gen_fullsize_hashes import digest
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                        "fullsize_reference.json")
+    for w in json.load(open(path))["windows"]:
+        cfg, lens, cls = W.make_window(w["config"], n=w["n"], seed=w["seed"])
+        s = _sched(_cfg_spec(cfg), len(lens), device=torch.device("cuda", 0))
+        h = s.schedule(torch.as_tensor(lens).cuda(), torch.as_tensor(cls).cuda()).to_host()
+        g = _canon_gpu(h)
+        assert len(g["batch_meta"]) == w["batches"], w["config"]
+        assert digest(g) == w["sha256"], w["config"]
+        s.close()
+
+
 def test_c1_fixed_edges_1k():
     cfg, lens, cls = W.make_window("c1", seed=5)
     _compare_with_oracle(_cfg_spec(cfg), lens, cls, pack=True)

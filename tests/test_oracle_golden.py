@@ -5,6 +5,8 @@ BucketSet.assign / adjust_buckets / BatchController.form_batch over a window
 (oracle/ref_compose.py).  Bit-exact on every integer output; waste_ratio
 bit-exact too (same float64 expression order, memory_model.py:98-100)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -90,3 +92,32 @@ def test_dispatch_fixtures_cover_the_hazards():
         reordered += not np.array_equal(ref["disp_ids"], ref["batch_ids"])
         pending_differs += len(ref["disp_pending"]) != len(ref["pending"])
     assert reordered >= 10 and pending_differs >= 3
+
+
+FULLSIZE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                        "fullsize_reference.json")
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_oracle_matches_reference_at_benchmarked_size(idx):
+    """The oracle pinned to the unmodified reference at the bench's own C2 window (1M
+    requests, seed 1234; the reference takes ~40 s on it) and a C1 window: the sha256 of
+    every canonical result array equals the reference's (oracle/gen_fullsize_hashes.py,
+    run where the reference is importable)."""
+    import json
+
+    from oracle.gen_fullsize_hashes import digest, spec_of
+    from paper_2507_17120_b200 import workloads as W
+    w = json.load(open(FULLSIZE))["windows"][idx]
+    cfg, lens, cls = W.make_window(w["config"], n=w["n"], seed=w["seed"])
+    sp = spec_of(cfg)
+    ws = cpu.WindowSpec(l_max=sp["l_max"], n_classes=sp["n_classes"], policies=sp["policies"],
+                        theta=sp["theta"], adjust=sp["adjust"], init_edges=sp["init_edges"],
+                        kvpt=sp["kvpt"], current_safe=sp["current_safe"],
+                        accounting=sp["accounting"])
+    res = cpu.window(ws, lens, cls)
+    got = canonical(edges=res.edges, bucket=res.bucket, perm=res.perm, req_batch=res.req_batch,
+                    req_row=res.req_row, batches=res.batches, n_max=res.summary["n_max"],
+                    changes=res.changes)
+    assert len(got["batch_meta"]) == w["batches"]
+    assert digest(got) == w["sha256"]
