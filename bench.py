@@ -47,8 +47,13 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _pack_kernel(l_max, max_n):
-    """the K6 kernel(s) the library launches by default (k_pack.cu: launch_pack)."""
+def _pack_kernel(l_max, max_n, n_classes=1, dispatch=False, world=1):
+    """the K6 kernel(s) the library launches by default (k_pack.cu: launch_pack); windows
+    K0 takes (k_small.cu: small_window_ok — <= 2048 requests, l_max <= 8192, one rank, no
+    dispatch order) are copied by k_pack_rows."""
+    if (os.environ.get("BS_SMALL", "1") != "0" and not dispatch and world == 1
+            and max_n <= 2048 and l_max <= 8192 and l_max * n_classes <= 16384):
+        return "k_pack_rows"
     v = int(os.environ.get("BS_PACK_VARIANT", "0") or 0)
     if v not in (1, 5, 21):
         v = 1
@@ -493,13 +498,13 @@ def main():
 
     # ---------------- pack roofline ------------------------------------------------
     peak, peak_src = _peaks()
-    pk_name = _pack_kernel(cfg.l_max, n)
+    pk_name = _pack_kernel(cfg.l_max, n, cfg.n_classes, args.dispatch, world)
     admitted = int(s["admitted_tokens"])
     n_adm = n - int(s["n_rejected"]) - int(s["n_pending"])
     # SURVEY §8(d) algorithmic bytes: per admitted request 4*len (tokens) + 8 (offset)
     # read; per batch n * max_input_len * (4 + 1) written (int32 token + u8 mask)
     pack_bytes = 4 * admitted + 8 * n_adm + 5 * int(s["padded_tokens"])
-    # what K6 actually moves: rows padded to the 32-token pitch, + perm / row map / len
+    # what K6 actually moves: rows padded to the 16-token pitch, + perm / row map / len
     pack_bytes_pitch = 4 * admitted + 24 * n_adm + 5 * int(s["packed_elems"])
     pack_ms = stage_ms["pack"]
     pack_gbs = pack_bytes / (pack_ms / 1e3) / 1e9 if pack_ms > 0 else None
@@ -619,7 +624,7 @@ def main():
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
                   % (tokens.numel() * 4 / 1e9, int(s["packed_elems"]) * 5 / 1e9),
         },
-        "roofline": {"bound": "hbm", "kernel": pk_name + (" (+ k_pack_rowprep)" if pk_name == "k_pack_bulk" else ""),
+        "roofline": {"bound": "hbm", "kernel": pk_name,  # fused windows: K5e wrote the row records
                      "achieved": pack_gbs, "peak": peak,
                      "unit": "GB/s", "frac": (pack_gbs / peak) if pack_gbs else None,
                      "traffic": _profile_traffic(args.config, pk_name), "algorithmic_bytes": pack_bytes,

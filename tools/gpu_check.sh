@@ -27,6 +27,11 @@ timeout 900 ncu --set full --clock-control none --import-source on \
    -k regex:"k_pack_bulk|k_sort_pass|k_histogram|k_dispatch|k_bounds_small|k_size_next|k_chain_walk|k_size_outcome" -c 9 -f -o /tmp/full \
    python tools/stage_profile.py --config c2 --steps 1 --dispatch > $OUT/ncu_full.log 2>&1
 python tools/ncu_summary.py /tmp/full.ncu-rep --json $OUT/full_summary.json > $OUT/full_summary.txt 2>&1
+for c in c1 c3 c4; do  # the other configs' pack launch: DRAM bytes for their roofline.traffic
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+     --clock-control none -k regex:"k_pack_(bulk|rows)" --launch-skip 1 -c 1 --csv \
+     python tools/stage_profile.py --config $c --steps 1 > $OUT/pack_traffic_$c.csv 2>/dev/null
+done
 for k in k_pack_bulk k_histogram k_sort_pass k_dispatch k_size_next k_chain_walk; do
   python tools/ncu_source.py /tmp/full.ncu-rep $k 25 > $OUT/src_$k.txt 2>&1
 done

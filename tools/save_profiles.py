@@ -46,5 +46,21 @@ for e in full:
     if k == "k_histogram":
         ent.update(smem_atom_inst=e.get("smem_atom_inst"), gmem_atom_accesses=e.get("gmem_atom_accesses"))
     summ.setdefault(k, {}).setdefault("c2", ent)
+for c in ("c1", "c3", "c4"):  # pack launches of the other configs (gpu_check.sh)
+    f = os.path.join(S, f"pack_traffic_{c}.csv")
+    if not os.path.exists(f):
+        continue
+    rows = [r for r in csv.reader(open(f)) if len(r) > 10 and r[0] != "" and not r[0].startswith("{")]
+    if not rows or rows[0][0] != "ID":
+        continue
+    hdr, m = rows[0], {}
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        k = d["Kernel Name"].replace("void ", "").split("(")[0].split("<")[0].replace("bsk::", "")
+        m.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+    for k, v in m.items():
+        rd, wr = v.get("dram__bytes_read.sum", 0.0), v.get("dram__bytes_write.sum", 0.0)
+        summ.setdefault(k, {})[c] = {"dram_bytes": rd + wr, "dram_read": rd, "dram_write": wr,
+                                     "duration_us": v.get("gpu__time_duration.sum", 0.0) / 1e3}
 json.dump(summ, open(os.path.join(P, "ncu_summary.json"), "w"), indent=1)
 print(f"{len(out)} launches; kernels: {sorted(summ)}")
