@@ -139,6 +139,7 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_HIST_MAXB")) ctx->hist_maxb = std::max(1, atoi(v));
   if (const char* v = getenv("BS_SORT_ITEMS")) ctx->sort_items = atoi(v);
   if (const char* v = getenv("BS_CHAIN_WALK")) ctx->chain_walk = std::max(1, atoi(v));
+  if (const char* v = getenv("BS_CHAIN_PAIRS")) ctx->chain_pairs = atoi(v) != 0;
   if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
   if (const char* v = getenv("BS_PACK_REVERSE")) ctx->pack_reverse = atoi(v) != 0;
   if (const char* v = getenv("BS_BULK_WARPS")) ctx->pack_bulk_warps = atoi(v) == 8 ? 8 : 16;

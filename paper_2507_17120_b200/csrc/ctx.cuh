@@ -26,6 +26,7 @@ struct bs_ctx {
   int hist_ept = 4;         // K1 elements per thread (BS_HIST_EPT)
   int hist_maxb = 0;        // K1 CTA cap (BS_HIST_MAXB; default 2 per SM)
   int sort_items = 0;       // K4 keys per thread: 0 = by window size, 8 | 16 (BS_SORT_ITEMS)
+  int chain_pairs = 1;       // K5c walk two calls per round trip (BS_CHAIN_PAIRS=0: off)
   int chain_walk = 0;       // K5c serial-walk limit, 0 = default (BS_CHAIN_WALK)
   int pack_tma_blocks = 0;  // K6 TMA grid: co-resident CTAs per SM x SMs
   int pack_reverse = 1;     // K6 takes its 32-piece groups last batch first (BS_PACK_REVERSE=0: in order)

@@ -50,6 +50,7 @@ struct SizeArgs {
   int32_t ljf_mask;  // bit c: class c drains LJF (lengths descending)
   int32_t walk;      // K5c: chain calls followed serially before doubling is considered
   int32_t walk_forced;  // (tuning / test hook) hand every longer chain to doubling
+  int32_t pairs;        // K5c walk reads J1 = J0 o J0 too (k_chain_pairs)
 };
 
 struct Stat {
@@ -475,6 +476,18 @@ __device__ __forceinline__ SegArrays seg_arrays(int32_t* segw, int32_t n_segs) {
                    segw + 6 * w};
 }
 
+// J1 = J0 o J0 (the second successor) over every position, so a walk can take two calls
+// per dependent load pair (the loads of J0[pos] and J1[pos] are independent)
+__global__ void __launch_bounds__(256) k_chain_pairs(int64_t n, const int32_t* __restrict__ J0,
+                                                     int32_t* __restrict__ J1) {
+  pdl_prologue();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    const int32_t y = J0[j];
+    J1[j] = y == kEnd ? kEnd : J0[y];
+  }
+}
+
 __global__ void __launch_bounds__(256)
     k_chain_walk(SizeArgs a, const int32_t* __restrict__ kinfo, const int32_t* __restrict__ seg_off,
                  const int32_t* __restrict__ J0, int32_t* __restrict__ listB,
@@ -511,21 +524,31 @@ __global__ void __launch_bounds__(256)
     int32_t k = 0;
     listB[st] = (int32_t)st;
     int32_t limit = a.walk;
-    for (;;) {
-      const int32_t y = J0[pos];
-      if (y == kEnd) break;
+    const int32_t* J1 = J0 + a.n;  // second successors (k_chain_pairs)
+    // one call: false when the chain is handed to doubling instead
+    auto step = [&](int32_t y) -> bool {
       if (++k >= limit) {
-        if (a.walk_forced || k >= kWalkMax) { lng = 1; break; }
+        if (a.walk_forced || k >= kWalkMax) return false;
         // remaining calls at the average call size so far vs levels x positions
         const double avg = (double)(pos - st + 1) / (double)k;
         const double rest = (double)(en - pos) / avg;
         const double walk_us = rest * 0.25;
         const double dbl_us = 10.0 + (double)(en - st) * (log2(rest + k) + 1.0) * 1.9e-4;
-        if (walk_us > dbl_us) { lng = 1; break; }
+        if (walk_us > dbl_us) return false;
         limit = kWalkMax;
       }
       listB[st + k] = y;
       pos = y;
+      return true;
+    };
+    for (;;) {  // two calls per round trip
+      const int32_t y = J0[pos];
+      const int32_t y2 = a.pairs ? J1[pos] : kEnd;
+      if (y == kEnd) break;
+      if (!step(y)) { lng = 1; break; }
+      if (!a.pairs) continue;
+      if (y2 == kEnd) break;  // J0[y] == kEnd: the chain ends at y
+      if (!step(y2)) { lng = 1; break; }
     }
     if (!lng) {
       len = k + 1;
@@ -1048,6 +1071,7 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
   a.sjf_mask = a.ljf_mask = 0;
   a.walk = ctx->chain_walk > 0 ? ctx->chain_walk : kWalk;
   a.walk_forced = ctx->chain_walk > 0;
+  a.pairs = ctx->chain_pairs && ctx->r_cap >= 2;
   for (int c = 0; c < p.n_classes; ++c) {
     if (p.policy[c] == BS_POLICY_SJF) a.sjf_mask |= 1 << c;
     if (p.policy[c] == BS_POLICY_LJF) a.ljf_mask |= 1 << c;
@@ -1076,6 +1100,11 @@ cudaError_t launch_size(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
     int32_t* dseg = p.dispatch ? ctx->disp_cseg : nullptr;
     int32_t* dmin = p.dispatch ? ctx->disp_cmin : nullptr;
     int64_t* dsum = p.dispatch ? ctx->disp_csum : nullptr;
+    if (a.pairs) {
+      launch_k(ctx, k_chain_pairs, dim3(wblocks), dim3(256), 0, st, false, n, ctx->J, ctx->J + n);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      ++ctx->launches;
+    }
     launch_k(ctx, k_chain_walk, dim3((unsigned)(n_tiles + (segs_ub + 255) / 256)), dim3(256), 0, st,
              false, a, ctx->kinfo, seg_off, ctx->J, ctx->listB, ctx->sorted_len, ctx->bmask,
              ctx->bcnt, ctx->segw, misc, ctx->rg_tiles, n_tiles);
