@@ -72,6 +72,30 @@ def _profile_traffic(cfg_name, kernel):
         return None
 
 
+_ALL_CPUS = None
+
+
+def _bind_near_gpu(index):
+    """Run this rank on the CPU cores NVML reports as local to its GPU (the socket whose
+    PCIe root holds it), so the pinned host buffers of the e2e leg are allocated on that
+    NUMA node; returns the core count, or None when NVML cannot tell."""
+    global _ALL_CPUS
+    _ALL_CPUS = os.sched_getaffinity(0)
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
 
@@ -328,6 +352,7 @@ def main():
     local_dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_dev)
     dev = torch.device("cuda", local_dev)
+    numa_cpus = _bind_near_gpu(local_dev)
     pg = None
     if world > 1:
         backend = os.environ.get("BS_DIST_BACKEND", "nccl")
@@ -571,7 +596,9 @@ def main():
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        k_e2e = max(3, min(args.steps, 10))
+        # ~10 steps of a large window (seconds of PCIe), up to 100 of a small one (its
+        # ~0.1 ms steps are otherwise at the mercy of host scheduling noise)
+        k_e2e = max(3, min(args.steps, 10 if ntok * 4 > (64 << 20) else 100))
         e0.record()
         for cs in copy_streams:  # no copy of the timed steps starts before e0
             cs.wait_stream(torch.cuda.current_stream(dev))
@@ -598,6 +625,8 @@ def main():
     cpu_base = None
     if not args.no_cpu_baseline and world == 1:
         # the same window as the timed one (capped at 1M requests of host memory)
+        if _ALL_CPUS:  # the CPU baseline gets every host core back
+            os.sched_setaffinity(0, _ALL_CPUS)
         cpu_base = cpu_baseline(args.config, min(args.cpu_sample or (1 << 20), n))
 
     line = {
@@ -619,6 +648,8 @@ def main():
                 "nccl": "NCCL histogram all-reduce inside the window graph)",
                 "torch": f"torch.distributed ({os.environ.get('BS_DIST_BACKEND', 'nccl')}) "
                          "histogram all-reduce between K1 and K2)"}[args.collective],
+            "host_binding": (f"{numa_cpus} GPU-local cores (NVML CPU affinity)" if numa_cpus
+                             else "unbound"),
             "pipeline": f"{inflight} windows in flight (one scheduler context + CUDA stream each); "
                         "ms_per_step = timed region / steps",
             "l2": "inputs larger than L2 (token store %.2f GB/GPU, packed output %.2f GB/GPU); no flush"
