@@ -441,11 +441,13 @@ __global__ void __launch_bounds__(256)
 
 // ---------------------------------------------------------------------------- K5c
 // The chain of every segment, next(next(...)) from its start, is the sequence of its
-// form_batch calls.  Four plain (non-cooperative) kernels, so no launch waits for a whole
+// form_batch calls.  Plain (non-cooperative) kernels, so no launch waits for a whole
 // GPU to be free beside the pack of another window in flight:
-//   walk   one thread per segment follows its chain for up to `walk` calls (dependent L2
-//          hits; C2's longest chain is 75 calls) into listB; longer segments are listed;
-//          extra CTAs sum the admissible counts of 8192-group tiles (for Rg)
+//   pairs  J1 = J0 o J0 over every position (level 1 of the doubling table)
+//   walk   one thread per segment follows its chain for up to `walk` calls, two per round
+//          trip (J0[pos] and J1[pos] are independent loads; C2's longest chain is 75
+//          calls) into listB; longer segments are listed; extra CTAs sum the admissible
+//          counts of 8192-group tiles (for Rg)
 //   long   one 1024-thread CTA per listed segment: pointer doubling J[r+1] = J[r][J[r]]
 //          over the segment's positions only (__syncthreads per level, no grid barrier)
 //          until the start's 2^r-th successor is past the segment, then binary lifting
