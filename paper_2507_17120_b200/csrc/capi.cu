@@ -142,6 +142,18 @@ int bs_create(bs_ctx** out, int device, int64_t max_n, int32_t l_max_cap, int32_
   if (const char* v = getenv("BS_CHAIN_PAIRS")) ctx->chain_pairs = atoi(v) != 0;
   if (const char* v = getenv("BS_PDL")) ctx->pdl = atoi(v) != 0;
   if (const char* v = getenv("BS_PACK_REVERSE")) ctx->pack_reverse = atoi(v) != 0;
+  {  // launch priorities: the scheduling kernels of a window ahead of the packs of the
+     // windows in flight when both wait for an SM (C2 0.724 -> 0.714 ms, C3 11.89 ->
+     // 11.74 ms per window in flight); BS_PRIO=0 off, -1 the reverse (tuning hook)
+    const char* v = getenv("BS_PRIO");
+    const int mode = v ? atoi(v) : 1;
+    int lo = 0, hi = 0;  // least (numerically largest) and greatest priority
+    if (mode != 0 && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess && lo != hi) {
+      ctx->prio_on = 1;
+      ctx->prio_sched = mode > 0 ? hi : lo;
+      ctx->prio_pack = mode > 0 ? lo : hi;
+    }
+  }
   if (const char* v = getenv("BS_BULK_WARPS")) ctx->pack_bulk_warps = atoi(v) == 8 ? 8 : 16;
   ctx->carveout_uniform = max_n <= (4 << 20) ? 100 : 0;
   if (const char* v = getenv("BS_CARVEOUT")) ctx->carveout_uniform = std::max(0, std::min(100, atoi(v)));

@@ -36,6 +36,9 @@ struct bs_ctx {
                             // maximum (launch_k; bs_create: 100 for max_n <= 4M, BS_CARVEOUT)
   int64_t last_n = 0;       // requests of the last sized window (grid bound of the K6 row prep)
   int pdl = 1;              // programmatic dependent launch between the window's kernels (BS_PDL)
+  int prio_on = 0;          // per-launch priorities (bs_create; BS_PRIO): scheduling high, K6 low
+  int prio_sched = 0, prio_pack = 0;
+  mutable bool in_pack = false;  // set by launch_pack around the K6 launches
   int small_path = 1;       // K0 single-CTA path for small windows (BS_SMALL=0 disables)
   int small_smem_max = 0;   // its dynamic shared-memory opt-in (bytes)
   int small_timing = 0;     // K0 phase timestamps into summary.reserved (BS_SMALL_TIMING=1 ns, 2 cycles)
@@ -167,7 +170,7 @@ inline cudaError_t launch_k(const bs_ctx* ctx, void (*kernel)(KArgs...), dim3 gr
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[3];
+  cudaLaunchAttribute at[4];
   unsigned na = 0;
   if (ctx->carveout_uniform > 0) {
     // every kernel of the window at the maximum shared-memory carveout: an SM only runs
@@ -177,6 +180,11 @@ inline cudaError_t launch_k(const bs_ctx* ctx, void (*kernel)(KArgs...), dim3 gr
     // per window in flight); at 16M (C3) the gather-heavy K5 kernels want their L1 back.
     at[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
     at[na].val.sharedMemCarveout = (unsigned)ctx->carveout_uniform;  // percent of the maximum
+    ++na;
+  }
+  if (ctx->prio_on) {
+    at[na].id = cudaLaunchAttributePriority;
+    at[na].val.priority = ctx->in_pack ? ctx->prio_pack : ctx->prio_sched;
     ++na;
   }
   if (cooperative) {

@@ -962,15 +962,19 @@ cudaError_t launch_pack(bs_ctx* ctx, const int32_t* len, const int32_t* perm,
                         const bs_batch* batches, int64_t batch_begin, int64_t batch_end,
                         int32_t batches_cap, int32_t* out_tokens, uint8_t* out_mask,
                         int64_t out_capacity, bs_summary* summary, cudaStream_t st) {
-  // The TMA staging kernel for long-context windows (rows of many KB: C4 at 89-91 % of
-  // the copy peak with windows in flight; the register stream packs a C4 window faster
-  // alone, 96 %, but fills every SM and slows the windows in flight), the flattened
-  // 128-bit register stream with the uniform-group fast path otherwise (C2 758 vs 786
-  // us, C3 11.11 vs 11.45 ms against the stream without it).  ctx->pack_variant
-  // (BS_PACK_VARIANT at bs_create) forces one: 5 = TMA, 21 = register stream; both are
-  // bit-identical.  The slower forms measured in round 1 (per-row k_pack, persistent
-  // grids, a cp.async shared-memory ring, 8 vectors per lane) are recorded in DESIGN.md.
+  // pack_kernel_choice: the bulk-staged kernel whenever both outputs are 16-byte aligned
+  // (every config), else the TMA staging kernel for long-context windows or the
+  // flattened 128-bit register stream.  ctx->pack_variant (BS_PACK_VARIANT at bs_create)
+  // forces one: 1 = bulk, 5 = TMA, 21 = register stream; all are bit-identical.  The
+  // K6 launches carry the low launch priority (launch_k) so that the scheduling kernels
+  // of the windows in flight get SMs first.  The slower forms measured in rounds 1-2
+  // are recorded in DESIGN.md.
   const int v = pack_kernel_choice(ctx, p, out_tokens, out_mask);
+  struct PackScope {
+    bs_ctx* c;
+    explicit PackScope(bs_ctx* x) : c(x) { c->in_pack = true; }
+    ~PackScope() { c->in_pack = false; }
+  } scope(ctx);
   if (v == 1)
     return ctx->pack_bulk_warps == 8
                ? launch_pack_bulk<8>(ctx, len, perm, tok_off, tokens, p, batches, batch_begin, batch_end,
